@@ -1,0 +1,320 @@
+// tcgen05 GEMM for the decoder projections:
+//   C[m][n] (+)= sum_k A[m][k] B[n][k]  (+ bias[n]),  A = activations [M][K] bf16,
+//   B = weights [N][K] bf16 (nn.Linear layout; both operands K-major), fp32 accumulate.
+//
+// Blackwell structure (one CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer: 2-D tensor-map loads of A (128 x 64) and B (BN x 64) tiles
+//               into a 4-stage shared-memory ring, 128-byte swizzle, mbarrier complete_tx.
+//   warp 1      allocates TMEM (2 x BN fp32 columns: double-buffered accumulator) and one
+//               elected lane issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN, K=16);
+//               tcgen05.commit releases smem stages / publishes finished accumulators.
+//   warps 2..5  epilogue: tcgen05.ld 32x32b (each warp owns its TMEM lane quarter = 32 rows),
+//               bias / residual-accumulate / SwiGLU, vector stores to global memory.
+// Tiles are ordered m-fastest so the CTAs that share a weight tile run together and the
+// weight stream is read from HBM once (small-M decode GEMMs are weight-bandwidth-bound).
+#include <cuda.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "kernels.h"
+
+namespace {
+constexpr int BM = 128, BK = 64, STAGES = 4;
+constexpr int NTHREADS = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// K-major operand tile [rows][64 bf16] with 128-byte swizzle: SBO = 8 rows x 128 B.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm100)
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%"
+      "20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int BN>
+struct Smem {
+  alignas(1024) bf16 a[STAGES][BM * BK];
+  alignas(1024) bf16 b[STAGES][BN * BK];
+  uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  uint32_t tmem_base;
+};
+
+// MODE: GEMM_STORE (C = AB^T + bias), GEMM_ACCUM (C += AB^T), GEMM_SWIGLU (columns of each
+// BN tile are [gate(BN/2) | up(BN/2)] of interleaved weights; writes bf16 act[m][F]).
+template <int BN, int MODE>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* C,
+              const float* __restrict__ bias, bf16* act, int M, int N, int K) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem<BN>& sm = *reinterpret_cast<Smem<BN>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN, ntiles = mt * nt;
+  const int kb_n = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&sm.tfull[s], 1); mbar_init(&sm.tempty[s], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(&sm.empty[stage], phase ^ 1);
+          mbar_expect_tx(&sm.full[stage], (BM + BN) * BK * 2);
+          tma_load_2d(sm.a[stage], &tmA, &sm.full[stage], kb * BK, m0);
+          tma_load_2d(sm.b[stage], &tmB, &sm.full[stage], kb * BK, n0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = 128
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int as = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      mbar_wait(&sm.tempty[as], aph ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t d = tmem + as * BN;
+      for (int kb = 0; kb < kb_n; ++kb) {
+        mbar_wait(&sm.full[stage], phase);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(sm.a[stage]), b0 = smem_u32(sm.b[stage]);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(d, umma_desc(a0 + k * 32), umma_desc(b0 + k * 32), idesc, (kb | k) ? 1u : 0u);
+          umma_commit(&sm.empty[stage]);
+          if (kb == kb_n - 1) umma_commit(&sm.tfull[as]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int as = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+      mbar_wait(&sm.tfull[as], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int gm = m0 + row;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + as * BN;
+      if (MODE == GEMM_SWIGLU) {
+        const int F = N / 2;   // N = 2F interleaved in BN-wide tiles
+        const int f0 = (t / mt) * (BN / 2);
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 32) {
+          float g[32], u[32];
+          tmem_ld32(tbase + c, g);
+          tmem_ld32(tbase + BN / 2 + c, u);
+          if (gm < M) {
+            bf16* dst = act + (size_t)gm * F + f0 + c;
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              if (f0 + c + j + 8 <= F) {
+                __align__(16) bf16 o[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  float x = g[j + e];
+                  o[e] = __float2bfloat16_rn(x / (1.0f + __expf(-x)) * u[j + e]);
+                }
+                *reinterpret_cast<uint4*>(dst + j) = *reinterpret_cast<uint4*>(o);
+              }
+            }
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(tbase + c, v);
+          const int gn = n0 + c;
+          if (gm < M && gn < N) {
+            float* dst = C + (size_t)gm * N + gn;
+            if (gn + 32 <= N) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                if (bias) { x.x += bias[gn + j]; x.y += bias[gn + j + 1]; x.z += bias[gn + j + 2]; x.w += bias[gn + j + 3]; }
+                if (MODE == GEMM_ACCUM) {
+                  float4 y = *reinterpret_cast<float4*>(dst + j);
+                  x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
+                }
+                *reinterpret_cast<float4*>(dst + j) = x;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (gn + j < N) {
+                  float x = v[j] + (bias ? bias[gn + j] : 0.f);
+                  dst[j] = MODE == GEMM_ACCUM ? dst[j] + x : x;
+                }
+              }
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.tempty[as]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiled get_encode() {
+  static EncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiled)p;
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* ptr, int rows, int K, int box_rows) {
+  EncodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct MapCache {
+  std::map<std::tuple<const void*, int, int, int>, CUtensorMap> m;
+  const CUtensorMap* get(const void* p, int rows, int K, int box) {
+    auto key = std::make_tuple(p, rows, K, box);
+    auto it = m.find(key);
+    if (it != m.end()) return &it->second;
+    CUtensorMap t;
+    if (!make_map(&t, p, rows, K, box)) return nullptr;
+    return &(m[key] = t);
+  }
+};
+MapCache g_maps;
+int g_num_sms = 0;
+
+template <int BN, int MODE>
+bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
+               cudaStream_t s) {
+  const CUtensorMap* ma = g_maps.get(A, M, K, BM);
+  const CUtensorMap* mb = g_maps.get(B, N, K, BN);
+  if (!ma || !mb) return false;
+  const size_t smem = sizeof(Smem<BN>) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_tc<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
+  const int ntiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = ntiles < g_num_sms ? ntiles : g_num_sms;
+  k_gemm_tc<BN, MODE><<<grid, NTHREADS, smem, s>>>(*ma, *mb, C, bias, act, M, N, K);
+  return true;
+}
+}  // namespace
+
+bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
+                    int mode, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return true;
+  if (K % 8) return false;   // TMA row stride must be a multiple of 16 bytes
+  if (mode == GEMM_STORE) return launch_bn<256, GEMM_STORE>(A, B, bias, C, act, M, N, K, s);
+  if (mode == GEMM_ACCUM) return launch_bn<256, GEMM_ACCUM>(A, B, bias, C, act, M, N, K, s);
+  return launch_bn<256, GEMM_SWIGLU>(A, B, bias, C, act, M, N, K, s);
+}

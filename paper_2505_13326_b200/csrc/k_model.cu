@@ -1,0 +1,218 @@
+// Decoder elementwise kernels: weight init, embedding gather, RMSNorm, RoPE + paged KV
+// append, SwiGLU, PRM head tail.  (SURVEY §8(a) rows a2, a3, a5, a6, a8.)
+#include "kernels.h"
+
+// ------------------------------------------------------------ device weight init
+// N(0, std^2) via Philox + Box-Muller; norms 1 + N(0, 0.1^2).  Inputs only: the
+// values do not matter for timing runs (parity runs pass host_weights).
+template <typename T>
+__global__ void k_init_tensor(T* p, long long n, int tid, int is_norm, float std, unsigned long long seed) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    long long pr = i >> 1;
+    u32x4 w = philox4x32_10(u32x4{(uint32_t)pr, (uint32_t)(pr >> 32), (uint32_t)tid, 0xC0FFEEu},
+                            (uint32_t)seed, (uint32_t)(seed >> 32));
+    float u1 = ((w.x >> 8) + 0.5f) * (1.0f / 16777216.0f);
+    float u2 = ((w.y >> 8) + 0.5f) * (1.0f / 16777216.0f);
+    float r = sqrtf(-2.0f * logf(u1));
+    float z = (i & 1) ? r * sinpif(2.0f * u2) : r * cospif(2.0f * u2);
+    p[i] = from_f<T>(is_norm ? 1.0f + 0.1f * z : std * z);
+  }
+}
+template <typename T>
+void launch_init_tensor(T* p, long long n, int tid, int is_norm, float std, unsigned long long seed,
+                        cudaStream_t s) {
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  k_init_tensor<T><<<(int)blocks, 256, 0, s>>>(p, n, tid, is_norm, std, seed);
+}
+
+// ------------------------------------------------------------ embedding: h = E[tok]
+template <typename T>
+__global__ void k_embed(const int* __restrict__ tok, const T* __restrict__ emb, float* __restrict__ h, int d) {
+  int r = blockIdx.x;
+  const T* e = emb + (long long)tok[r] * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) h[(long long)r * d + i] = to_f(e[i]);
+}
+template <typename T>
+void launch_embed(const int* tok, const T* emb, float* h, int n, int d, cudaStream_t s) {
+  if (n > 0) k_embed<T><<<n, 256, 0, s>>>(tok, emb, h, d);
+}
+
+// ------------------------------------------------------------ RMSNorm
+// out = h * rsqrt(mean(h^2) + eps) * g ; rows with status != RUNNING are skipped when
+// status is given (the final norm keeps the z of finished rows for the PRM, O6).
+template <typename T>
+__global__ void k_rmsnorm(const float* __restrict__ h, const T* __restrict__ g, T* __restrict__ out,
+                          float* __restrict__ out32, const int* __restrict__ status, int d, float eps) {
+  int r = blockIdx.x;
+  if (status && status[r] != RUNNING_ST) return;
+  const float* x = h + (long long)r * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += x[i] * x[i];
+  __shared__ float red[32];
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  float inv = rsqrtf(red[0] / d + eps);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float y = x[i] * inv * to_f(g[i]);
+    out[(long long)r * d + i] = from_f<T>(y);
+    if (out32) out32[(long long)r * d + i] = y;
+  }
+}
+template <typename T>
+void launch_rmsnorm(const float* h, const T* g, T* out, float* out32, const int* status, int n, int d,
+                    float eps, cudaStream_t s) {
+  if (n > 0) k_rmsnorm<T><<<n, 256, 0, s>>>(h, g, out, out32, status, d, eps);
+}
+
+// ------------------------------------------------------------ RoPE + KV append
+// qkv (fp32, bias included) -> q (rotated) into qout[r][qh][hd]; k (rotated), v into the
+// paged pool.  Decode: suffix entry l of row r at table[r][l/bs], slot l%bs, position
+// P-1+l.  Prefill: prefix position p0+r at prefix[slot][p/bs], slot p%bs.
+template <typename T>
+__global__ void k_rope_append(const float* __restrict__ qkv, T* __restrict__ qout, T* __restrict__ pool,
+                              const float* __restrict__ rope_cs, Dims D, int layer, Rows rows, Reqs reqs,
+                              RopeArgs a) {
+  int r = blockIdx.x;
+  int pos, blk, slot_in_blk;
+  bool write_kv = true;
+  if (a.prefill_slot >= 0) {
+    pos = a.p0 + r;
+    blk = reqs.prefix[(long long)a.prefill_slot * D.MPB + pos / D.bs];
+    slot_in_blk = pos % D.bs;
+  } else {
+    if (rows.status[r] != RUNNING_ST) return;
+    int l = rows.ell[r];
+    pos = reqs.P[rows.slot[r]] - 1 + l;
+    blk = rows.table[(long long)r * D.MBR + l / D.bs];
+    slot_in_blk = l % D.bs;
+  }
+  const int half = D.hd / 2;
+  const float* x = qkv + (long long)r * D.qkv;
+  const float* cs = rope_cs + (long long)pos * D.hd;   // [cos(half) | sin(half)]
+  int pairs = (D.qh + 2 * D.kvh) * half;
+  for (int t = threadIdx.x; t < pairs; t += blockDim.x) {
+    int head = t / half, i = t % half;
+    float x1 = x[head * D.hd + i], x2 = x[head * D.hd + i + half];
+    if (head < D.qh + D.kvh) {                      // q or k: rotate-half
+      float c = cs[i], sn = cs[half + i];
+      float y1 = x1 * c - x2 * sn, y2 = x2 * c + x1 * sn;
+      x1 = y1; x2 = y2;
+    }
+    if (head < D.qh) {
+      T* q = qout + ((long long)r * D.qh + head) * D.hd;
+      q[i] = from_f<T>(x1);
+      q[i + half] = from_f<T>(x2);
+    } else if (write_kv) {
+      int kv = head < D.qh + D.kvh ? 0 : 1;
+      int h = kv == 0 ? head - D.qh : head - D.qh - D.kvh;
+      T* tile = pool + kv_tile_off(D, layer, blk, kv, h);
+      tile[kv_swz<T>(slot_in_blk, i, D.hd)] = from_f<T>(x1);
+      tile[kv_swz<T>(slot_in_blk, i + half, D.hd)] = from_f<T>(x2);
+    }
+  }
+}
+template <typename T>
+void launch_rope_append(const float* qkv, T* qout, T* pool, const float* rope_cs, Dims D, int layer, Rows rows,
+                        Reqs reqs, RopeArgs a, int n, cudaStream_t s) {
+  if (n > 0) k_rope_append<T><<<n, 256, 0, s>>>(qkv, qout, pool, rope_cs, D, layer, rows, reqs, a);
+}
+
+// ------------------------------------------------------------ SwiGLU: act = SiLU(g) * u
+template <typename T>
+__global__ void k_swiglu(const float* __restrict__ gu, T* __restrict__ act, int F) {
+  int r = blockIdx.x;
+  const float* x = gu + (long long)r * 2 * F;
+  for (int i = threadIdx.x; i < F; i += blockDim.x) {
+    float g = x[i], u = x[F + i];
+    act[(long long)r * F + i] = from_f<T>(g / (1.0f + expf(-g)) * u);
+  }
+}
+template <typename T>
+void launch_swiglu(const float* gu, T* act, int n, int F, cudaStream_t s) {
+  if (n > 0) k_swiglu<T><<<n, 256, 0, s>>>(gu, act, F);
+}
+
+// ------------------------------------------------------------ PRM head tail
+// hid = z W1^T + b1 (fp32, from the GEMM); score = softmax(ReLU(hid) W2^T + b2)[1].
+__global__ void k_prm_head2(const float* __restrict__ hid, const float* __restrict__ w2,
+                            const float* __restrict__ b2, float* __restrict__ score, int d) {
+  int r = blockIdx.x;
+  float a0 = 0.f, a1 = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float x = fmaxf(hid[(long long)r * d + i], 0.f);
+    a0 += x * w2[i];
+    a1 += x * w2[d + i];
+  }
+  __shared__ float r0[32], r1[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+  }
+  if ((threadIdx.x & 31) == 0) { r0[threadIdx.x >> 5] = a0; r1[threadIdx.x >> 5] = a1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float l0 = b2[0], l1 = b2[1];
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { l0 += r0[w]; l1 += r1[w]; }
+    float m = fmaxf(l0, l1);
+    float e0 = expf(l0 - m), e1 = expf(l1 - m);
+    score[r] = e1 / (e0 + e1);
+  }
+}
+void launch_prm_head2(const float* hid, const float* w2, const float* b2, float* score, int n, int d,
+                      cudaStream_t s) {
+  if (n > 0) k_prm_head2<<<n, 256, 0, s>>>(hid, w2, b2, score, d);
+}
+
+template <typename T>
+__global__ void k_convert(const float* __restrict__ in, T* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = from_f<T>(in[i]);
+}
+template <typename T>
+void launch_convert(const float* in, T* out, long long n, cudaStream_t s) {
+  if (n > 0) k_convert<T><<<(int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(in, out, n);
+}
+template <typename T>
+__global__ void k_to_f32(const T* __restrict__ in, float* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = to_f(in[i]);
+}
+template <typename T>
+void launch_to_f32(const T* in, float* out, long long n, cudaStream_t s) {
+  if (n > 0) k_to_f32<T><<<(int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(in, out, n);
+}
+
+#define INST(T)                                                                                        \
+  template void launch_init_tensor<T>(T*, long long, int, int, float, unsigned long long, cudaStream_t); \
+  template void launch_embed<T>(const int*, const T*, float*, int, int, cudaStream_t);                  \
+  template void launch_rmsnorm<T>(const float*, const T*, T*, float*, const int*, int, int, float,      \
+                                  cudaStream_t);                                                        \
+  template void launch_rope_append<T>(const float*, T*, T*, const float*, Dims, int, Rows, Reqs,        \
+                                      RopeArgs, int, cudaStream_t);                                     \
+  template void launch_swiglu<T>(const float*, T*, int, int, cudaStream_t);                             \
+  template void launch_convert<T>(const float*, T*, long long, cudaStream_t);                           \
+  template void launch_to_f32<T>(const T*, float*, long long, cudaStream_t);
+INST(float)
+INST(bf16)
+
+// gate|up rows [2F][d] -> 256-row tiles [gate 128 | up 128] for the fused SwiGLU epilogue
+__global__ void k_interleave(const bf16* __restrict__ src, bf16* __restrict__ dst, int F, int d) {
+  const int r = blockIdx.x;              // destination row
+  const int tile = r / 256, w = r % 256;
+  const int sr = w < 128 ? tile * 128 + w : F + tile * 128 + (w - 128);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) dst[(long long)r * d + i] = src[(long long)sr * d + i];
+}
+void launch_interleave_gate_up(bf16* w, bf16* tmp, int F, int d, cudaStream_t s) {
+  cudaMemcpyAsync(tmp, w, sizeof(bf16) * 2 * (size_t)F * d, cudaMemcpyDeviceToDevice, s);
+  k_interleave<<<2 * F, 256, 0, s>>>(tmp, w, F, d);
+}

@@ -1,0 +1,100 @@
+// Seeded counter-based sampler with EOS / cap / forced-length detection.
+//   y_s = argmax_v ( logit_v / tau + G_v ),  G_v = -ln(-ln u_v),
+//   u_v = ((w >> 8) + 0.5) 2^-24,  w = Philox4x32-10((v>>2, s, rid, b), seed)[v & 3]
+// (readings R24, R25).  Ties go to the lowest v.  fp32 arithmetic; -ln u is evaluated as
+// log1p(-(2^24 - x - 0.5) 2^-24) in the upper half so u is represented exactly.
+#include "kernels.h"
+
+__device__ __forceinline__ float gumbel_from_word(uint32_t w) {
+  uint32_t x = w >> 8;
+  float lnu;
+  if (x < (1u << 23)) lnu = logf(((float)x + 0.5f) * (1.0f / 16777216.0f));
+  else lnu = log1pf(-(((float)((1u << 24) - x)) - 0.5f) * (1.0f / 16777216.0f));
+  return -logf(-lnu);
+}
+
+__device__ __forceinline__ void better(float& bk, int& bv, float k, int v) {
+  if (k > bk || (k == bk && v < bv)) { bk = k; bv = v; }
+}
+
+__global__ void __launch_bounds__(512) k_sample(const float* __restrict__ logits, Dims D, Rows rows, Reqs reqs,
+                                                Ctr* ctr, int* dbg_tok) {
+  const int r = blockIdx.x;
+  if (rows.status[r] != RUNNING_ST) return;
+  const int slot = rows.slot[r], b = rows.b[r];
+  const int s = rows.ell[r] + 1;
+  const long long sb = (long long)slot * SART_MAXN + b;
+  const int forced_len = reqs.sc_len[sb];   // 0 = no scripted EOS step
+  const float* lg = logits + (long long)r * D.V;
+  const uint32_t rid = (uint32_t)reqs.id[slot];
+  const uint32_t k0 = (uint32_t)D.seed, k1 = (uint32_t)(D.seed >> 32);
+  const bool mask_eos = forced_len > 0;
+  int y;
+  __shared__ float sk[32];
+  __shared__ int sv[32];
+  if (forced_len > 0 && s == forced_len) {
+    y = D.eos;
+  } else {
+    float bk = -INFINITY;
+    int bv = 0x7fffffff;
+    const int ngrp = (D.V + 3) >> 2;
+    for (int g4 = threadIdx.x; g4 < ngrp; g4 += blockDim.x) {
+      u32x4 w{0, 0, 0, 0};
+      if (D.tau > 0.f) w = philox4x32_10(u32x4{(uint32_t)g4, (uint32_t)s, rid, (uint32_t)b}, k0, k1);
+      uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int v = 4 * g4 + j;
+        if (v >= D.V) break;
+        if (mask_eos && v == D.eos) continue;
+        float key = D.tau > 0.f ? lg[v] / D.tau + gumbel_from_word(ws[j]) : lg[v];
+        better(bk, bv, key, v);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      int ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      better(bk, bv, ok, ov);
+    }
+    if ((threadIdx.x & 31) == 0) { sk[threadIdx.x >> 5] = bk; sv[threadIdx.x >> 5] = bv; }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      bk = threadIdx.x < (blockDim.x >> 5) ? sk[threadIdx.x] : -INFINITY;
+      bv = threadIdx.x < (blockDim.x >> 5) ? sv[threadIdx.x] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        float ok = __shfl_xor_sync(0xffffffffu, bk, o);
+        int ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        better(bk, bv, ok, ov);
+      }
+    }
+    y = bv;
+  }
+  if (threadIdx.x != 0) return;
+  if (dbg_tok) dbg_tok[r] = y;
+  if (reqs.has_forced[slot]) y = reqs.forced[sb * D.cap + (s - 1)];   // teacher forcing
+  reqs.hist[sb * D.cap + (s - 1)] = y;
+  rows.tok[r] = y;
+  rows.ell[r] = s;
+  atomicAdd((unsigned long long*)&ctr->branch_tokens, 1ull);
+  int st = RUNNING_ST;
+  if (y == D.eos) st = ST_EOS;                  // O5 / R17
+  else if (s == D.cap) st = ST_CAP;
+  if (st != RUNNING_ST) {
+    rows.status[r] = st;
+    rows.done_step[r] = s;
+    rows.done_wstep[r] = ctr->wstep;
+    atomicSub(&ctr->live, 1);
+  }
+}
+
+void launch_sample(const float* logits, Dims D, Rows rows, Reqs reqs, Ctr* ctr, int n, int* dbg_tok,
+                   cudaStream_t s) {
+  if (n > 0) k_sample<<<n, 512, 0, s>>>(logits, D, rows, reqs, ctr, dbg_tok);
+}
+
+__global__ void k_step_begin(Ctr* ctr) {
+  if (ctr->live > 0) { ctr->wstep += 1; ctr->steps += 1; }
+}
+void launch_step_begin(Ctr* ctr, cudaStream_t s) { k_step_begin<<<1, 1, 0, s>>>(ctr); }

@@ -1,0 +1,59 @@
+// Host-callable launchers of the SART device kernels (all on the given stream).
+#pragma once
+#include "common.cuh"
+
+// ---- model (k_model.cu)
+template <typename T> void launch_init_tensor(T* p, long long n, int tensor_id, int is_norm, float std,
+                                              unsigned long long seed, cudaStream_t s);
+template <typename T> void launch_embed(const int* tok, const T* emb, float* h, int n, int d, cudaStream_t s);
+template <typename T> void launch_rmsnorm(const float* h, const T* g, T* out, float* out32, const int* status,
+                                          int n, int d, float eps, cudaStream_t s);
+struct RopeArgs {
+  // decode mode (slot == -1): per-row positions from Rows/Reqs; prefill mode: slot >= 0
+  int prefill_slot, p0;
+};
+template <typename T> void launch_rope_append(const float* qkv, T* qout, T* pool, const float* rope_cs,
+                                              Dims D, int layer, Rows rows, Reqs reqs, RopeArgs a, int n,
+                                              cudaStream_t s);
+template <typename T> void launch_swiglu(const float* gu, T* act, int n, int F, cudaStream_t s);
+void launch_prm_head2(const float* hid, const float* w2, const float* b2, float* score, int n, int d,
+                      cudaStream_t s);
+template <typename T> void launch_convert(const float* in, T* out, long long n, cudaStream_t s);
+template <typename T> void launch_to_f32(const T* in, float* out, long long n, cudaStream_t s);
+
+// ---- GEMM (k_gemm.cu): C[m][n] (+)= A[m][k] . B[n][k]^T (+ bias[n]); fp32 accumulate.
+enum { GEMM_STORE = 0, GEMM_ACCUM = 1, GEMM_SWIGLU = 2 };
+template <typename T> void launch_gemm_simt(const T* A, const T* B, const float* bias, float* C, int M, int N,
+                                            int K, int mode, cudaStream_t s);
+
+// tcgen05 GEMM (k_gemm_tc.cu), bf16 operands.  GEMM_SWIGLU: B rows interleaved in 256-row
+// tiles as [gate 128 | up 128]; writes act[m][N/2] = SiLU(gate) * up as bf16.
+// Returns false when the shape is unsupported (caller falls back to nothing: it is an error).
+bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
+                    int mode, cudaStream_t s);
+void launch_interleave_gate_up(bf16* w, bf16* tmp, int F, int d, cudaStream_t s);
+
+// ---- attention (k_attn.cu)
+template <typename T> void launch_attn_decode_simple(const T* q, const T* pool, T* out, float* dbg, Dims D,
+                                                     int layer, Rows rows, Reqs reqs, int n, cudaStream_t s);
+template <typename T> void launch_attn_prefill(const T* q, const T* pool, T* out, Dims D, int layer, Reqs reqs,
+                                               int slot, int p0, int n, cudaStream_t s);
+
+// ---- sampler (k_sample.cu)
+void launch_sample(const float* logits, Dims D, Rows rows, Reqs reqs, Ctr* ctr, int n, int* dbg_tok,
+                   cudaStream_t s);
+void launch_step_begin(Ctr* ctr, cudaStream_t s);
+
+// ---- control (k_ctl.cu)
+// type 0 = prefill (pop the prefix blocks, init meta[i], Alg. 1 L16), 1 = new row (L5)
+struct AdmitEvent {
+  int type, slot, b, pop_off, row, first_tok;
+  int N, M, P, beta, prune, npre, has_script, has_answer, has_forced, nbnd;
+  float alpha;
+  long long id;
+};
+void launch_admit(const AdmitEvent* ev, int n_ev, int total_pop, int new_rows, int commit_delta, Dims D,
+                  Rows rows, Reqs reqs, int* free_stack, Ctr* ctr, cudaStream_t s);
+void launch_boundary(Dims D, Rows rows, Rows tmp, Reqs reqs, const float* prm_score, int* free_stack,
+                     Ctr* ctr, DevResult* res, int* slot_row, int n, cudaStream_t s);
+void launch_window_begin(Ctr* ctr, int n, cudaStream_t s);

@@ -1,0 +1,1063 @@
+// C-ABI (include/sart.h) and host orchestrator of the SART decode engine.
+//
+// Host side (this file): the FCFS request_queue and branch_queue of Algorithm 1
+// (P:218-219), the fill loop L3-11 with commitment admission (R34), prefill launches
+// (L14-20), the window loop (L12, L21-22) and result collection.  Everything
+// that touches per-branch state -- sampling, EOS, pruning, early stop, reclamation,
+// compaction, voting -- runs in device kernels; the host reads one counter record per
+// window.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <set>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/sart.h"
+#include "kernels.h"
+
+namespace {
+thread_local std::string g_last_error;
+
+int set_err(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+struct HostScript {
+  std::vector<int32_t> forced_len, answer, forced_tokens;
+  std::vector<float> scores, final_score;
+  int n_bnd = 0;
+};
+struct HostReq {
+  int64_t id;
+  std::vector<int32_t> prompt;
+  int N, M, beta;
+  float alpha;
+  bool has_script = false;
+  HostScript sc;
+  int64_t arrival_ns, admit_ns;
+};
+struct SlotInfo {
+  int64_t id = -1;
+  int N = 0;
+  int64_t arrival_ns = 0, prefill_ns = 0;
+  int first_tok = 0;
+  bool live = false;
+};
+struct HostResult {
+  sart_result r;
+  std::vector<int32_t> tokens;
+};
+}  // namespace
+
+struct sart_ctx {
+  sart_config cfg{};
+  Dims D{};
+  bool bf16 = true;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  bool poisoned = false;
+  bool gemm_failed = false;
+  int W = 0;   // workspace rows
+  int PC = 0;  // prefill chunk
+
+  // device memory
+  std::vector<void*> allocs;
+  void* wblob = nullptr;   // all weight tensors (model dtype)
+  std::vector<size_t> woff;  // element offset of each tensor in weight_names order
+  float* fparams = nullptr;  // fp32 copies: bqkv per layer, prm_b1, prm_w2, prm_b2
+  size_t f_bqkv = 0, f_prm_b1 = 0, f_prm_w2 = 0, f_prm_b2 = 0;
+  void* pool = nullptr;
+  Rows rows{}, tmp{};
+  Reqs reqs{};
+  Ctr* ctr = nullptr;
+  int* free_stack = nullptr;
+  DevResult* res = nullptr;
+  int* slot_row = nullptr;
+  float *h = nullptr, *qkv = nullptr, *gu = nullptr, *z32 = nullptr, *logits = nullptr, *prm_hid = nullptr,
+        *prm_score = nullptr, *rope_cs = nullptr, *dbg_attn = nullptr;
+  void *a = nullptr, *q = nullptr, *o = nullptr, *act = nullptr, *zT = nullptr;
+  int* dbg_tok = nullptr;
+  int *dbg_slot = nullptr, *dbg_b = nullptr;
+  int* d_prompt = nullptr;
+  AdmitEvent* d_events = nullptr;
+  int ev_cap = 0;
+
+  // host state
+  std::deque<HostReq> request_queue;
+  std::deque<std::pair<int, int>> branch_queue;  // (slot, branch)
+  std::vector<SlotInfo> slots;
+  std::vector<int> free_slots;
+  std::set<int64_t> seen_ids;
+  std::deque<HostResult> results;
+  int n_rows = 0;
+  long long free_top = 0, committed = 0;
+  int windows = 0, steps = 0, finalized_total = 0;
+  long long branch_tokens = 0;
+  int last_n = 0;
+  Ctr* h_ctr = nullptr;  // pinned
+  int* h_live = nullptr; // pinned
+  std::vector<int64_t> last_slot_id;
+
+  // profiling
+  std::vector<cudaEvent_t> ev_pool;
+  int ev_used = 0;
+  double attn_ms = 0, attn_bytes = 0, prefill_ms = 0;
+  long long attn_launches = 0, launches = 0;
+
+  template <typename T> T* W_(int idx) const { return (T*)wblob + woff[idx]; }
+};
+
+namespace {
+// tensor indices in weight_names order
+int t_embed() { return 0; }
+int t_layer(int l, int k) { return 1 + 8 * l + k; }  // k: 0 attn_norm 1 wqkv 2 bqkv 3 wo 4 mlp_norm 5 wgate 6 wup 7 wdown
+int t_final(const Dims& D) { return 1 + 8 * D.L; }
+int t_lm(const Dims& D) { return 2 + 8 * D.L; }
+int t_prm_w1(const Dims& D) { return 3 + 8 * D.L; }
+int t_prm_b1(const Dims& D) { return 4 + 8 * D.L; }
+int t_prm_w2(const Dims& D) { return 5 + 8 * D.L; }
+int t_prm_b2(const Dims& D) { return 6 + 8 * D.L; }
+
+std::vector<size_t> tensor_sizes(const Dims& D) {
+  std::vector<size_t> s;
+  s.push_back((size_t)D.V * D.d);
+  for (int l = 0; l < D.L; ++l) {
+    s.push_back(D.d);
+    s.push_back((size_t)D.qkv * D.d);
+    s.push_back(D.qkv);
+    s.push_back((size_t)D.d * D.qh * D.hd);
+    s.push_back(D.d);
+    s.push_back((size_t)D.F * D.d);
+    s.push_back((size_t)D.F * D.d);
+    s.push_back((size_t)D.d * D.F);
+  }
+  s.push_back(D.d);
+  s.push_back((size_t)D.V * D.d);
+  s.push_back((size_t)D.d * D.d);
+  s.push_back(D.d);
+  s.push_back((size_t)2 * D.d);
+  s.push_back(2);
+  return s;
+}
+bool is_norm_tensor(const Dims& D, int idx) {
+  if (idx == t_final(D)) return true;
+  if (idx >= 1 && idx < 1 + 8 * D.L) {
+    int k = (idx - 1) % 8;
+    return k == 0 || k == 4;
+  }
+  return false;
+}
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) {                                                               \
+      ctx->poisoned = true;                                                                \
+      return set_err(SART_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));        \
+    }                                                                                      \
+  } while (0)
+
+template <typename P>
+cudaError_t dalloc(sart_ctx* ctx, P** p, size_t bytes, bool zero = true) {
+  void* v = nullptr;
+  cudaError_t e = cudaMalloc(&v, bytes ? bytes : 16);
+  if (e != cudaSuccess) return e;
+  ctx->allocs.push_back(v);
+  if (zero) e = cudaMemset(v, 0, bytes ? bytes : 16);
+  *p = (P*)v;
+  return e;
+}
+
+cudaError_t alloc_rows(sart_ctx* ctx, Rows& r) {
+  const Dims& D = ctx->D;
+  cudaError_t e;
+  int** ints[] = {&r.slot, &r.b, &r.ell, &r.status, &r.done_step, &r.done_wstep, &r.nbnd, &r.tok, &r.term, &r.nblk};
+  for (auto p : ints)
+    if ((e = dalloc(ctx, p, sizeof(int) * D.R)) != cudaSuccess) return e;
+  if ((e = dalloc(ctx, &r.score, sizeof(float) * D.R)) != cudaSuccess) return e;
+  return dalloc(ctx, &r.table, sizeof(int) * (size_t)D.R * D.MBR);
+}
+
+cudaError_t alloc_reqs(sart_ctx* ctx) {
+  const Dims& D = ctx->D;
+  Reqs& q = ctx->reqs;
+  cudaError_t e;
+  size_t S = D.S, S32 = (size_t)D.S * SART_MAXN;
+  if ((e = dalloc(ctx, &q.id, sizeof(long long) * S)) != cudaSuccess) return e;
+  int** ints[] = {&q.N, &q.M, &q.P, &q.beta, &q.prune, &q.phase, &q.maxp, &q.nc, &q.np, &q.nes, &q.npre,
+                  &q.first_tok, &q.has_script, &q.has_answer, &q.has_forced, &q.nbnd, &q.final_flag};
+  for (auto p : ints)
+    if ((e = dalloc(ctx, p, sizeof(int) * S)) != cudaSuccess) return e;
+  if ((e = dalloc(ctx, &q.alpha, sizeof(float) * S)) != cudaSuccess) return e;
+  if ((e = dalloc(ctx, &q.thr, sizeof(float) * S)) != cudaSuccess) return e;
+  if ((e = dalloc(ctx, &q.prefix, sizeof(int) * S * D.MPB)) != cudaSuccess) return e;
+  int** i32[] = {&q.br_state, &q.br_len, &q.br_label, &q.sc_len, &q.sc_answer};
+  for (auto p : i32)
+    if ((e = dalloc(ctx, p, sizeof(int) * S32)) != cudaSuccess) return e;
+  if ((e = dalloc(ctx, &q.br_score, sizeof(float) * S32)) != cudaSuccess) return e;
+  if ((e = dalloc(ctx, &q.sc_final, sizeof(float) * S32)) != cudaSuccess) return e;
+  if ((e = dalloc(ctx, &q.sc_scores, sizeof(float) * S32 * D.nbnd_max)) != cudaSuccess) return e;
+  if ((e = dalloc(ctx, &q.hist, sizeof(int) * S32 * D.cap)) != cudaSuccess) return e;
+  q.forced = nullptr;
+  if (ctx->cfg.enable_forced_tokens)
+    if ((e = dalloc(ctx, &q.forced, sizeof(int) * S32 * D.cap)) != cudaSuccess) return e;
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ model step
+// bf16: tcgen05 GEMM; fp32 parity mode: SIMT FFMA GEMM (tf32 tensor cores would not hold 1e-5).
+template <typename T>
+void gemm(sart_ctx* ctx, const T* A, const T* B, const float* bias, float* C, int M, int N, int K, int mode) {
+  if constexpr (std::is_same<T, bf16>::value) {
+    if (!launch_gemm_tc(A, B, bias, C, nullptr, M, N, K, mode, ctx->st)) ctx->gemm_failed = true;
+  } else {
+    launch_gemm_simt<T>(A, B, bias, C, M, N, K, mode, ctx->st);
+  }
+  ctx->launches++;
+}
+
+// MLP up-projection + SwiGLU: fused tcgen05 epilogue on gate/up-interleaved weights (bf16),
+// or GEMM + elementwise kernel (fp32 mode).
+template <typename T>
+void mlp_up(sart_ctx* ctx, int l, int n) {
+  const Dims& D = ctx->D;
+  if constexpr (std::is_same<T, bf16>::value) {
+    if (!launch_gemm_tc((bf16*)ctx->a, ctx->W_<bf16>(t_layer(l, 5)), nullptr, nullptr, (bf16*)ctx->act, n, 2 * D.F,
+                        D.d, GEMM_SWIGLU, ctx->st))
+      ctx->gemm_failed = true;
+    ctx->launches++;
+  } else {
+    gemm<T>(ctx, (T*)ctx->a, ctx->W_<T>(t_layer(l, 5)), nullptr, ctx->gu, n, 2 * D.F, D.d, GEMM_STORE);
+    launch_swiglu<T>(ctx->gu, (T*)ctx->act, n, D.F, ctx->st);
+    ctx->launches++;
+  }
+}
+
+template <typename T>
+void layer_attention(sart_ctx* ctx, int l, int n) {
+  const Dims& D = ctx->D;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->cfg.profile && ctx->ev_used + 2 <= (int)ctx->ev_pool.size()) {
+    e0 = ctx->ev_pool[ctx->ev_used++];
+    e1 = ctx->ev_pool[ctx->ev_used++];
+    cudaEventRecord(e0, ctx->st);
+  }
+  float* dbg = ctx->dbg_attn ? ctx->dbg_attn + (size_t)l * D.R * D.qh * D.hd : nullptr;
+  launch_attn_decode_simple<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, dbg, D, l, ctx->rows, ctx->reqs, n, ctx->st);
+  ctx->launches++;
+  ctx->attn_launches++;
+  if (e1) cudaEventRecord(e1, ctx->st);
+}
+
+template <typename T>
+void decode_step(sart_ctx* ctx, int n) {
+  const Dims& D = ctx->D;
+  cudaStream_t s = ctx->st;
+  launch_step_begin(ctx->ctr, s);
+  launch_embed<T>(ctx->rows.tok, ctx->W_<T>(t_embed()), ctx->h, n, D.d, s);
+  ctx->launches += 2;
+  for (int l = 0; l < D.L; ++l) {
+    launch_rmsnorm<T>(ctx->h, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, n, D.d, D.eps, s);
+    gemm<T>(ctx, (T*)ctx->a, ctx->W_<T>(t_layer(l, 1)), ctx->fparams + ctx->f_bqkv + (size_t)l * D.qkv, ctx->qkv, n,
+            D.qkv, D.d, GEMM_STORE);
+    launch_rope_append<T>(ctx->qkv, (T*)ctx->q, (T*)ctx->pool, ctx->rope_cs, D, l, ctx->rows, ctx->reqs,
+                          RopeArgs{-1, 0}, n, s);
+    ctx->launches += 2;
+    layer_attention<T>(ctx, l, n);
+    gemm<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), nullptr, ctx->h, n, D.d, D.qh * D.hd, GEMM_ACCUM);
+    launch_rmsnorm<T>(ctx->h, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, n, D.d, D.eps, s);
+    mlp_up<T>(ctx, l, n);
+    gemm<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), nullptr, ctx->h, n, D.d, D.F, GEMM_ACCUM);
+    ctx->launches += 1;
+  }
+  launch_rmsnorm<T>(ctx->h, ctx->W_<T>(t_final(D)), (T*)ctx->zT, ctx->z32, ctx->rows.status, n, D.d, D.eps, s);
+  gemm<T>(ctx, (T*)ctx->zT, ctx->W_<T>(t_lm(D)), nullptr, ctx->logits, n, D.V, D.d, GEMM_STORE);
+  launch_sample(ctx->logits, D, ctx->rows, ctx->reqs, ctx->ctr, n, ctx->dbg_tok, s);
+  ctx->launches += 2;
+}
+
+template <typename T>
+void prefill(sart_ctx* ctx, int slot, int P) {
+  const Dims& D = ctx->D;
+  cudaStream_t s = ctx->st;
+  const int ntok = P - 1;
+  for (int p0 = 0; p0 < ntok; p0 += ctx->PC) {
+    const int c = std::min(ctx->PC, ntok - p0);
+    launch_embed<T>(ctx->d_prompt + p0, ctx->W_<T>(t_embed()), ctx->h, c, D.d, s);
+    ctx->launches++;
+    for (int l = 0; l < D.L; ++l) {
+      launch_rmsnorm<T>(ctx->h, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, c, D.d, D.eps, s);
+      gemm<T>(ctx, (T*)ctx->a, ctx->W_<T>(t_layer(l, 1)), ctx->fparams + ctx->f_bqkv + (size_t)l * D.qkv, ctx->qkv,
+              c, D.qkv, D.d, GEMM_STORE);
+      launch_rope_append<T>(ctx->qkv, (T*)ctx->q, (T*)ctx->pool, ctx->rope_cs, D, l, ctx->rows, ctx->reqs,
+                            RopeArgs{slot, p0}, c, s);
+      ctx->launches += 2;
+      if (l == D.L - 1) break;  // the last layer's output is not part of the prefix KV
+      launch_attn_prefill<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, D, l, ctx->reqs, slot, p0, c, s);
+      gemm<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), nullptr, ctx->h, c, D.d, D.qh * D.hd, GEMM_ACCUM);
+      launch_rmsnorm<T>(ctx->h, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, c, D.d, D.eps, s);
+      mlp_up<T>(ctx, l, c);
+      gemm<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), nullptr, ctx->h, c, D.d, D.F, GEMM_ACCUM);
+      ctx->launches += 2;
+    }
+  }
+}
+
+template <typename T>
+void prm_scores(sart_ctx* ctx, int n) {
+  const Dims& D = ctx->D;
+  gemm<T>(ctx, (T*)ctx->zT, ctx->W_<T>(t_prm_w1(D)), ctx->fparams + ctx->f_prm_b1, ctx->prm_hid, n, D.d, D.d,
+          GEMM_STORE);
+  launch_prm_head2(ctx->prm_hid, ctx->fparams + ctx->f_prm_w2, ctx->fparams + ctx->f_prm_b2, ctx->prm_score, n,
+                   D.d, ctx->st);
+  ctx->launches++;
+}
+
+// ------------------------------------------------------------------ admission (fill loop)
+int flush_events(sart_ctx* ctx, std::vector<AdmitEvent>& ev, int& pop_off, int& new_rows, int& commit_delta) {
+  if (ev.empty()) return SART_OK;
+  if ((int)ev.size() > ctx->ev_cap) return set_err(SART_EINVAL, "too many admission events");
+  CK(cudaMemcpyAsync(ctx->d_events, ev.data(), sizeof(AdmitEvent) * ev.size(), cudaMemcpyHostToDevice, ctx->st));
+  launch_admit(ctx->d_events, (int)ev.size(), pop_off, new_rows, commit_delta, ctx->D, ctx->rows, ctx->reqs,
+               ctx->free_stack, ctx->ctr, ctx->st);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  ctx->free_top -= pop_off;
+  ctx->n_rows += new_rows;
+  ev.clear();
+  pop_off = new_rows = commit_delta = 0;
+  return SART_OK;
+}
+
+int upload_request(sart_ctx* ctx, const HostReq& q, int slot) {
+  const Dims& D = ctx->D;
+  cudaStream_t s = ctx->st;
+  size_t sb = (size_t)slot * SART_MAXN;
+  if (!q.sc.forced_len.empty()) {
+    CK(cudaMemcpyAsync(ctx->reqs.sc_len + sb, q.sc.forced_len.data(), sizeof(int) * q.N, cudaMemcpyHostToDevice, s));
+  } else {
+    std::vector<int> z(q.N, 0);
+    CK(cudaMemcpyAsync(ctx->reqs.sc_len + sb, z.data(), sizeof(int) * q.N, cudaMemcpyHostToDevice, s));
+  }
+  if (q.has_script) {
+    CK(cudaMemcpyAsync(ctx->reqs.sc_final + sb, q.sc.final_score.data(), sizeof(float) * q.N,
+                       cudaMemcpyHostToDevice, s));
+    int nb = std::min(q.sc.n_bnd, D.nbnd_max);
+    CK(cudaMemcpy2DAsync(ctx->reqs.sc_scores + sb * D.nbnd_max, sizeof(float) * D.nbnd_max, q.sc.scores.data(),
+                         sizeof(float) * q.sc.n_bnd, sizeof(float) * nb, q.N, cudaMemcpyHostToDevice, s));
+  }
+  if (!q.sc.answer.empty())
+    CK(cudaMemcpyAsync(ctx->reqs.sc_answer + sb, q.sc.answer.data(), sizeof(int) * q.N, cudaMemcpyHostToDevice, s));
+  if (!q.sc.forced_tokens.empty())
+    CK(cudaMemcpyAsync(ctx->reqs.forced + sb * D.cap, q.sc.forced_tokens.data(), sizeof(int) * (size_t)q.N * D.cap,
+                       cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->d_prompt, q.prompt.data(), sizeof(int) * q.prompt.size(), cudaMemcpyHostToDevice, s));
+  return SART_OK;
+}
+
+int fill(sart_ctx* ctx) {
+  const Dims& D = ctx->D;
+  const int RC = cdiv(D.cap, D.bs);
+  const int nfirst = cdiv(std::min(D.T, D.cap), D.bs);
+  std::vector<AdmitEvent> ev;
+  int pop_off = 0, new_rows = 0, commit_delta = 0;
+  while (ctx->n_rows + new_rows < ctx->cfg.max_rows) {  // L3
+    if (!ctx->branch_queue.empty()) {                   // L4-5
+      auto [slot, b] = ctx->branch_queue.front();
+      if (ctx->committed + RC > D.NB) break;            // R34: no skipping
+      ctx->branch_queue.pop_front();
+      ctx->committed += RC;
+      commit_delta += RC;
+      AdmitEvent e{};
+      e.type = 1;
+      e.slot = slot;
+      e.b = b;
+      e.pop_off = pop_off;
+      e.row = ctx->n_rows + new_rows;
+      e.first_tok = ctx->slots[slot].first_tok;   // prompt[P-1] (R22)
+      ev.push_back(e);
+      pop_off += nfirst;
+      new_rows++;
+    } else if (!ctx->request_queue.empty()) {           // L6-7
+      HostReq& q = ctx->request_queue.front();
+      const int P = (int)q.prompt.size();
+      const int npre = cdiv(P - 1, D.bs);
+      if (ctx->committed + npre + RC > D.NB) break;
+      if (ctx->free_slots.empty()) break;               // slot table full (max_requests)
+      const int slot = ctx->free_slots.back();
+      ctx->free_slots.pop_back();
+      ctx->committed += npre;
+      commit_delta += npre;
+      AdmitEvent e{};
+      e.type = 0;
+      e.slot = slot;
+      e.pop_off = pop_off;
+      e.first_tok = q.prompt[P - 1];
+      e.N = q.N;
+      e.M = q.M;
+      e.P = P;
+      e.beta = q.beta;
+      e.prune = q.alpha >= 0.f ? 1 : 0;
+      e.npre = npre;
+      e.has_script = q.has_script ? 1 : 0;
+      e.has_answer = q.sc.answer.empty() ? 0 : 1;
+      e.has_forced = q.sc.forced_tokens.empty() ? 0 : 1;
+      e.nbnd = q.has_script ? std::min(q.sc.n_bnd, D.nbnd_max) : 0;
+      e.alpha = q.alpha;
+      e.id = q.id;
+      ev.push_back(e);
+      pop_off += npre;
+      int rc = upload_request(ctx, q, slot);
+      if (rc) return rc;
+      rc = flush_events(ctx, ev, pop_off, new_rows, commit_delta);
+      if (rc) return rc;
+      // L15: perform prefilling (prefix = prompt[0:P-1], R22)
+      int64_t t0 = now_ns();
+      if (ctx->bf16) prefill<bf16>(ctx, slot, P);
+      else prefill<float>(ctx, slot, P);
+      CK(cudaGetLastError());
+      SlotInfo& si = ctx->slots[slot];
+      si.id = q.id;
+      si.N = q.N;
+      si.arrival_ns = q.arrival_ns;
+      si.prefill_ns = t0;
+      si.first_tok = q.prompt[P - 1];
+      si.live = true;
+      ctx->last_slot_id[slot] = q.id;
+      for (int j = 0; j < q.N; ++j) ctx->branch_queue.emplace_back(slot, j);  // L17-19
+      ctx->prefill_ms += (now_ns() - t0) * 1e-6;
+      ctx->request_queue.pop_front();
+    } else {
+      break;  // L8-9
+    }
+  }
+  return flush_events(ctx, ev, pop_off, new_rows, commit_delta);
+}
+
+// ------------------------------------------------------------------ boundary read-back
+int read_boundary(sart_ctx* ctx) {
+  const Dims& D = ctx->D;
+  CK(cudaMemcpyAsync(ctx->h_ctr, ctx->ctr, sizeof(Ctr) + sizeof(int) * D.S, cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  Ctr& c = *ctx->h_ctr;
+  // the device applied the releases; the host mirror adopts its counters
+  ctx->n_rows = c.n_rows;
+  ctx->free_top = c.free_top;
+  ctx->committed = c.committed;
+  ctx->windows = c.windows;
+  ctx->steps = c.steps;
+  ctx->branch_tokens = c.branch_tokens;
+  const int nf = c.n_final;
+  if (nf == 0) return SART_OK;
+  std::vector<int> fslots(c.final_slots, c.final_slots + nf);
+  std::sort(fslots.begin(), fslots.end(),
+            [&](int a, int b) { return ctx->slots[a].id < ctx->slots[b].id; });
+  std::vector<DevResult> dr(nf);
+  for (int i = 0; i < nf; ++i)
+    CK(cudaMemcpyAsync(&dr[i], ctx->res + fslots[i], sizeof(DevResult), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  const int64_t tnow = now_ns();
+  for (int i = 0; i < nf; ++i) {
+    const int slot = fslots[i];
+    SlotInfo& si = ctx->slots[slot];
+    HostResult hr;
+    sart_result& r = hr.r;
+    memset(&r, 0, sizeof(r));
+    const DevResult& d = dr[i];
+    r.request_id = d.request_id;
+    r.answer_vote = d.answer_vote;
+    r.vote_count = d.vote_count;
+    r.chosen_max_reward = d.chosen_max_reward;
+    r.answer_max_reward = d.answer_max_reward;
+    r.num_completed = d.num_completed;
+    r.num_pruned = d.num_pruned;
+    r.num_early_stopped = d.num_early_stopped;
+    r.finalize_reason = d.finalize_reason;
+    r.phase_at_end = d.phase_at_end;
+    r.threshold_at_end = d.threshold_at_end;
+    r.selected_branch = d.selected_branch;
+    for (int b = 0; b < si.N; ++b) {
+      r.branch_len[b] = d.branch_len[b];
+      r.branch_state[b] = (uint8_t)d.branch_state[b];
+      r.branch_score[b] = d.branch_score[b];
+    }
+    // R7: queued branches of a finalized request are discarded at no cost
+    int disc = 0;
+    std::deque<std::pair<int, int>> keep;
+    for (auto& p : ctx->branch_queue) {
+      if (p.first == slot) {
+        r.branch_state[p.second] = SART_BR_DISCARDED;
+        ++disc;
+      } else {
+        keep.push_back(p);
+      }
+    }
+    ctx->branch_queue.swap(keep);
+    r.num_discarded_queued = disc;
+    r.t_arrival_ns = si.arrival_ns;
+    r.t_prefill_ns = si.prefill_ns;
+    r.t_final_ns = tnow;
+    r.window_final = ctx->windows - 1;
+    const int sel = d.selected_branch;
+    r.tokens_len = d.branch_len[sel];
+    hr.tokens.resize(r.tokens_len);
+    if (r.tokens_len > 0)
+      CK(cudaMemcpyAsync(hr.tokens.data(), ctx->reqs.hist + ((size_t)slot * SART_MAXN + sel) * D.cap,
+                         sizeof(int) * r.tokens_len, cudaMemcpyDeviceToHost, ctx->st));
+    ctx->results.push_back(std::move(hr));
+    si.live = false;
+    ctx->free_slots.push_back(slot);
+    ctx->finalized_total++;
+  }
+  CK(cudaStreamSynchronize(ctx->st));
+  return SART_OK;
+}
+
+template <typename T>
+int run_window(sart_ctx* ctx) {
+  const Dims& D = ctx->D;
+  const int n = ctx->n_rows;
+  ctx->last_n = n;
+  ctx->ev_used = 0;
+  launch_window_begin(ctx->ctr, n, ctx->st);
+  ctx->launches++;
+  for (int k = 1; k <= D.T; ++k) {
+    if (k > 1 && (k % 8) == 1) {
+      // live rows read back asynchronously; a window ends early when none is live (R31)
+      CK(cudaMemcpyAsync(ctx->h_live, &ctx->ctr->live, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+      CK(cudaStreamSynchronize(ctx->st));
+      if (*ctx->h_live == 0) break;
+    }
+    decode_step<T>(ctx, n);
+  }
+  CK(cudaGetLastError());
+  if (ctx->gemm_failed) return set_err(SART_EINVAL, "GEMM shape unsupported by the tcgen05 kernel");
+  // rows of this window (debug), then the boundary: PRM head -> control kernel
+  CK(cudaMemcpyAsync(ctx->dbg_slot, ctx->rows.slot, sizeof(int) * n, cudaMemcpyDeviceToDevice, ctx->st));
+  CK(cudaMemcpyAsync(ctx->dbg_b, ctx->rows.b, sizeof(int) * n, cudaMemcpyDeviceToDevice, ctx->st));
+  prm_scores<T>(ctx, n);
+  launch_boundary(D, ctx->rows, ctx->tmp, ctx->reqs, ctx->prm_score, ctx->free_stack, ctx->ctr, ctx->res,
+                  ctx->slot_row, n, ctx->st);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  int rc = read_boundary(ctx);
+  if (rc) return rc;
+  if (ctx->cfg.profile) {
+    for (int i = 0; i + 1 < ctx->ev_used; i += 2) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev_pool[i], ctx->ev_pool[i + 1]);
+      ctx->attn_ms += ms;
+    }
+  }
+  return SART_OK;
+}
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* sart_strerror(int code) {
+  switch (code) {
+    case SART_OK: return "SART_OK";
+    case SART_EINVAL: return "SART_EINVAL";
+    case SART_ENOMEM: return "SART_ENOMEM";
+    case SART_ECUDA: return "SART_ECUDA";
+    case SART_EFULL: return "SART_EFULL";
+    case SART_ESTATE: return "SART_ESTATE";
+    case SART_EDUP: return "SART_EDUP";
+    default: return "SART_UNKNOWN";
+  }
+}
+const char* sart_last_error(void) { return g_last_error.c_str(); }
+
+int sart_destroy(sart_ctx* ctx) {
+  if (!ctx) return SART_OK;
+  cudaSetDevice(ctx->cfg.device);
+  if (ctx->st) cudaStreamSynchronize(ctx->st);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->wblob) cudaFree(ctx->wblob);
+  if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
+  if (ctx->h_live) cudaFreeHost(ctx->h_live);
+  if (ctx->own_stream && ctx->st) cudaStreamDestroy(ctx->st);
+  delete ctx;
+  return SART_OK;
+}
+
+int sart_init(const sart_config* cfg_in, sart_ctx** out) {
+  if (!cfg_in || !out) return set_err(SART_EINVAL, "null argument");
+  *out = nullptr;
+  sart_config cfg = *cfg_in;
+  if (cfg.block_size == 0) cfg.block_size = 64;
+  if (cfg.max_rows == 0) cfg.max_rows = 1024;
+  if (cfg.max_requests == 0) cfg.max_requests = 256;
+  if (cfg.max_prompt == 0) cfg.max_prompt = 8193;
+  if (cfg.ctl_interval == 0) cfg.ctl_interval = 400;
+  if (cfg.weight_std == 0.f) cfg.weight_std = 0.02f;
+  if (cfg.n_layers < 1 || cfg.d_model < 1 || cfg.n_heads < 1 || cfg.n_kv_heads < 1 || cfg.d_ff < 1 ||
+      cfg.vocab < 2)
+    return set_err(SART_EINVAL, "model dims must be positive");
+  if (cfg.head_dim != 64 && cfg.head_dim != 128) return set_err(SART_EINVAL, "head_dim must be 64 or 128");
+  if (cfg.n_heads % cfg.n_kv_heads || cfg.n_heads / cfg.n_kv_heads > 16)
+    return set_err(SART_EINVAL, "n_heads must be a multiple of n_kv_heads with ratio <= 16");
+  if (cfg.d_model % 8 || cfg.d_ff % 8) return set_err(SART_EINVAL, "d_model and d_ff must be multiples of 8");
+  if (cfg.dtype != SART_BF16 && cfg.dtype != SART_FP32) return set_err(SART_EINVAL, "dtype");
+  if (cfg.block_size != 16 && cfg.block_size != 32 && cfg.block_size != 64)
+    return set_err(SART_EINVAL, "block_size must be 16, 32 or 64");
+  if (cfg.max_new_tokens < 1 || cfg.ctl_interval < 1 || cfg.max_rows < 1 || cfg.max_requests < 1 ||
+      cfg.max_requests > 1024 || cfg.max_prompt < 1)
+    return set_err(SART_EINVAL, "cap, T, max_rows >= 1; 1 <= max_requests <= 1024");
+  if (cfg.eos_id < 0 || cfg.eos_id >= cfg.vocab) return set_err(SART_EINVAL, "eos_id out of range");
+  if (!(cfg.temperature >= 0.f)) return set_err(SART_EINVAL, "temperature must be >= 0");
+  if (cfg.select_mode != 0 && cfg.select_mode != 1) return set_err(SART_EINVAL, "select_mode");
+  if (cfg.attn_mode != 0 && cfg.attn_mode != 1) return set_err(SART_EINVAL, "attn_mode");
+
+  sart_ctx* ctx = new sart_ctx();
+  ctx->cfg = cfg;
+  ctx->bf16 = cfg.dtype == SART_BF16;
+  Dims& D = ctx->D;
+  D.L = cfg.n_layers; D.d = cfg.d_model; D.qh = cfg.n_heads; D.kvh = cfg.n_kv_heads; D.hd = cfg.head_dim;
+  D.F = cfg.d_ff; D.V = cfg.vocab; D.qkv = (D.qh + 2 * D.kvh) * D.hd; D.g = D.qh / D.kvh;
+  D.bs = cfg.block_size; D.R = cfg.max_rows; D.S = cfg.max_requests;
+  D.cap = cfg.max_new_tokens; D.T = cfg.ctl_interval; D.eos = cfg.eos_id;
+  D.MBR = cdiv(D.cap, D.bs);
+  D.MPB = std::max(1, cdiv(cfg.max_prompt - 1, D.bs));
+  D.nbnd_max = cdiv(D.cap, D.T) + 1;
+  D.max_pos = cfg.max_prompt + D.cap;
+  D.theta = cfg.rope_theta; D.eps = cfg.rms_eps; D.tau = cfg.temperature; D.seed = cfg.sampler_seed;
+  D.select_mode = cfg.select_mode;
+  ctx->PC = 256;
+  ctx->W = std::max(D.R, ctx->PC);
+  const size_t es = ctx->bf16 ? 2 : 4;
+
+  cudaError_t e;
+#define IC(x)                                                                   \
+  do {                                                                          \
+    e = (x);                                                                    \
+    if (e != cudaSuccess) {                                                     \
+      int code = e == cudaErrorMemoryAllocation ? SART_ENOMEM : SART_ECUDA;     \
+      set_err(code, std::string(#x) + ": " + cudaGetErrorString(e));            \
+      sart_destroy(ctx);                                                        \
+      return code;                                                              \
+    }                                                                           \
+  } while (0)
+  IC(cudaSetDevice(cfg.device));
+  if (cfg.stream) {
+    ctx->st = (cudaStream_t)cfg.stream;
+  } else {
+    IC(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  // ---- weights
+  std::vector<size_t> sizes = tensor_sizes(D);
+  size_t total = 0;
+  for (size_t s : sizes) { ctx->woff.push_back(total); total += s; }
+  IC(cudaMalloc(&ctx->wblob, total * es));
+  if (cfg.host_weights) {
+    IC(cudaMemcpy(ctx->wblob, cfg.host_weights, total * es, cudaMemcpyHostToDevice));
+  } else {
+    for (size_t i = 0; i < sizes.size(); ++i) {
+      bool norm = is_norm_tensor(D, (int)i);
+      if (ctx->bf16)
+        launch_init_tensor<bf16>((bf16*)ctx->wblob + ctx->woff[i], (long long)sizes[i], (int)i, norm, cfg.weight_std,
+                                 cfg.weight_seed, ctx->st);
+      else
+        launch_init_tensor<float>((float*)ctx->wblob + ctx->woff[i], (long long)sizes[i], (int)i, norm,
+                                  cfg.weight_std, cfg.weight_seed, ctx->st);
+    }
+    IC(cudaGetLastError());
+  }
+  if (ctx->bf16) {
+    if (D.F % 128 != 0) {
+      set_err(SART_EINVAL, "bf16 mode needs d_ff % 128 == 0 (fused SwiGLU tiles)");
+      sart_destroy(ctx);
+      return SART_EINVAL;
+    }
+    bf16* tmpw = nullptr;
+    IC(cudaMalloc(&tmpw, sizeof(bf16) * 2 * (size_t)D.F * D.d));
+    for (int l = 0; l < D.L; ++l) launch_interleave_gate_up(ctx->W_<bf16>(t_layer(l, 5)), tmpw, D.F, D.d, ctx->st);
+    IC(cudaStreamSynchronize(ctx->st));
+    cudaFree(tmpw);
+  }
+  // fp32 copies of the small vectors used in epilogues
+  size_t nf = (size_t)D.L * D.qkv + D.d + 2 * (size_t)D.d + 2;
+  IC(dalloc(ctx, &ctx->fparams, nf * sizeof(float)));
+  ctx->f_bqkv = 0;
+  ctx->f_prm_b1 = (size_t)D.L * D.qkv;
+  ctx->f_prm_w2 = ctx->f_prm_b1 + D.d;
+  ctx->f_prm_b2 = ctx->f_prm_w2 + 2 * (size_t)D.d;
+  auto tof = [&](int idx, size_t off, size_t n) {
+    if (ctx->bf16) launch_to_f32<bf16>(ctx->W_<bf16>(idx), ctx->fparams + off, (long long)n, ctx->st);
+    else launch_to_f32<float>(ctx->W_<float>(idx), ctx->fparams + off, (long long)n, ctx->st);
+  };
+  for (int l = 0; l < D.L; ++l) tof(t_layer(l, 2), (size_t)l * D.qkv, D.qkv);
+  tof(t_prm_b1(D), ctx->f_prm_b1, D.d);
+  tof(t_prm_w2(D), ctx->f_prm_w2, 2 * (size_t)D.d);
+  tof(t_prm_b2(D), ctx->f_prm_b2, 2);
+  IC(cudaGetLastError());
+  // ---- RoPE table (fp64 on the host, stored fp32): [pos][cos(hd/2) | sin(hd/2)]
+  {
+    std::vector<float> cs((size_t)D.max_pos * D.hd);
+    const int half = D.hd / 2;
+    for (int p = 0; p < D.max_pos; ++p)
+      for (int i = 0; i < half; ++i) {
+        double inv = std::pow((double)D.theta, -2.0 * i / D.hd);
+        double ang = p * inv;
+        cs[(size_t)p * D.hd + i] = (float)std::cos(ang);
+        cs[(size_t)p * D.hd + half + i] = (float)std::sin(ang);
+      }
+    IC(dalloc(ctx, &ctx->rope_cs, cs.size() * sizeof(float), false));
+    IC(cudaMemcpy(ctx->rope_cs, cs.data(), cs.size() * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  // ---- state
+  IC(alloc_rows(ctx, ctx->rows));
+  IC(alloc_rows(ctx, ctx->tmp));
+  IC(alloc_reqs(ctx));
+  IC(dalloc(ctx, &ctx->ctr, sizeof(Ctr) + sizeof(int) * D.S));
+  IC(dalloc(ctx, &ctx->res, sizeof(DevResult) * D.S));
+  IC(dalloc(ctx, &ctx->slot_row, sizeof(int) * (size_t)D.S * SART_MAXN));
+  IC(cudaMemset(ctx->slot_row, 0xff, sizeof(int) * (size_t)D.S * SART_MAXN));
+  // ---- workspaces
+  const size_t W = ctx->W;
+  IC(dalloc(ctx, &ctx->h, W * D.d * 4));
+  IC(dalloc(ctx, &ctx->qkv, W * D.qkv * 4));
+  IC(dalloc(ctx, &ctx->gu, W * 2 * D.F * 4));
+  IC(dalloc(ctx, &ctx->z32, (size_t)D.R * D.d * 4));
+  IC(dalloc(ctx, &ctx->logits, (size_t)D.R * D.V * 4));
+  IC(dalloc(ctx, &ctx->prm_hid, (size_t)D.R * D.d * 4));
+  IC(dalloc(ctx, &ctx->prm_score, (size_t)D.R * 4));
+  IC(dalloc(ctx, &ctx->a, W * D.d * es));
+  IC(dalloc(ctx, &ctx->q, W * D.qh * D.hd * es));
+  IC(dalloc(ctx, &ctx->o, W * D.qh * D.hd * es));
+  IC(dalloc(ctx, &ctx->act, W * D.F * es));
+  IC(dalloc(ctx, &ctx->zT, (size_t)D.R * D.d * es));
+  IC(dalloc(ctx, &ctx->dbg_tok, (size_t)D.R * 4));
+  IC(dalloc(ctx, &ctx->dbg_slot, (size_t)D.R * 4));
+  IC(dalloc(ctx, &ctx->dbg_b, (size_t)D.R * 4));
+  IC(dalloc(ctx, &ctx->d_prompt, (size_t)cfg.max_prompt * 4));
+  ctx->ev_cap = D.R + D.S + 64;
+  IC(dalloc(ctx, &ctx->d_events, sizeof(AdmitEvent) * ctx->ev_cap));
+  if (cfg.debug_capture) IC(dalloc(ctx, &ctx->dbg_attn, (size_t)D.L * D.R * D.qh * D.hd * 4));
+  IC(cudaMallocHost(&ctx->h_ctr, sizeof(Ctr) + sizeof(int) * D.S));
+  IC(cudaMallocHost(&ctx->h_live, sizeof(int)));
+  // ---- KV pool
+  const size_t blk_bytes = (size_t)D.L * 2 * D.kvh * D.bs * D.hd * es;
+  long long NB = cfg.num_blocks;
+  if (NB <= 0) {
+    size_t fr = 0, tot = 0;
+    IC(cudaMemGetInfo(&fr, &tot));
+    const size_t reserve = (size_t)3 << 30;
+    NB = fr > reserve ? (long long)((fr - reserve) / blk_bytes) : 0;
+  }
+  if (NB < cdiv(D.cap, D.bs)) {
+    set_err(SART_ENOMEM, "KV pool cannot hold one branch of max_new_tokens");
+    sart_destroy(ctx);
+    return SART_ENOMEM;
+  }
+  D.NB = NB;
+  IC(dalloc(ctx, &ctx->pool, (size_t)NB * blk_bytes));
+  IC(dalloc(ctx, &ctx->free_stack, sizeof(int) * (size_t)NB, false));
+  {
+    std::vector<int> fs(NB);
+    for (long long i = 0; i < NB; ++i) fs[i] = (int)(NB - 1 - i);   // bottom -> top: NB-1 ... 0
+    IC(cudaMemcpy(ctx->free_stack, fs.data(), sizeof(int) * NB, cudaMemcpyHostToDevice));
+    Ctr c0{};
+    c0.free_top = NB;
+    IC(cudaMemcpy(ctx->ctr, &c0, sizeof(Ctr), cudaMemcpyHostToDevice));
+  }
+  ctx->free_top = NB;
+  ctx->slots.resize(D.S);
+  ctx->last_slot_id.assign(D.S, -1);
+  for (int s = D.S - 1; s >= 0; --s) ctx->free_slots.push_back(s);
+  if (cfg.profile) {
+    ctx->ev_pool.resize(2 * D.L * D.T + 2);
+    for (auto& ev : ctx->ev_pool) IC(cudaEventCreate(&ev));
+  }
+  IC(cudaStreamSynchronize(ctx->st));
+  *out = ctx;
+  return SART_OK;
+}
+
+int sart_admit(sart_ctx* ctx, const sart_request* r) {
+  if (!ctx || !r) return set_err(SART_EINVAL, "null argument");
+  if (ctx->poisoned) return set_err(SART_ESTATE, "ctx poisoned by an earlier CUDA error");
+  const Dims& D = ctx->D;
+  if (!(1 <= r->M && r->M <= r->N && r->N <= SART_MAXN)) return set_err(SART_EINVAL, "need 1 <= M <= N <= 32");
+  int beta = r->beta == -1 ? r->N / 2 : r->beta;
+  if (beta < 0 || beta > r->N - 1) return set_err(SART_EINVAL, "need 0 <= beta <= N-1");
+  if (std::isnan(r->prune_threshold) || r->prune_threshold > 1.f) return set_err(SART_EINVAL, "alpha > 1 or NaN");
+  if (!r->prompt || r->prompt_len < 1 || r->prompt_len > ctx->cfg.max_prompt)
+    return set_err(SART_EINVAL, "prompt_len out of range");
+  for (int i = 0; i < r->prompt_len; ++i)
+    if (r->prompt[i] < 0 || r->prompt[i] >= D.V) return set_err(SART_EINVAL, "prompt token out of range");
+  HostReq q;
+  q.id = r->request_id;
+  q.N = r->N;
+  q.M = r->M;
+  q.beta = beta;
+  q.alpha = r->prune_threshold;
+  if (r->script) {
+    const sart_script* s = r->script;
+    if ((s->scores == nullptr) != (s->final_score == nullptr))
+      return set_err(SART_EINVAL, "scores and final_score must both be given or both NULL");
+    if (s->scores) {
+      if (s->n_bnd < 1) return set_err(SART_EINVAL, "n_bnd >= 1 required with scores");
+      q.has_script = true;
+      q.sc.n_bnd = s->n_bnd;
+      q.sc.scores.assign(s->scores, s->scores + (size_t)r->N * s->n_bnd);
+      q.sc.final_score.assign(s->final_score, s->final_score + r->N);
+    }
+    if (s->forced_len) {
+      for (int b = 0; b < r->N; ++b)
+        if (s->forced_len[b] < 1 || s->forced_len[b] > D.cap) return set_err(SART_EINVAL, "forced_len out of range");
+      q.sc.forced_len.assign(s->forced_len, s->forced_len + r->N);
+    }
+    if (s->answer) q.sc.answer.assign(s->answer, s->answer + r->N);
+    if (s->forced_tokens) {
+      if (!ctx->cfg.enable_forced_tokens) return set_err(SART_EINVAL, "forced_tokens needs enable_forced_tokens");
+      q.sc.forced_tokens.assign(s->forced_tokens, s->forced_tokens + (size_t)r->N * D.cap);
+    }
+  }
+  const long long need = cdiv(r->prompt_len - 1, D.bs) + cdiv(D.cap, D.bs);
+  if (need > D.NB) return set_err(SART_ENOMEM, "request can never fit the KV pool");
+  if (ctx->seen_ids.count(r->request_id)) return set_err(SART_EDUP, "request_id reused");
+  ctx->seen_ids.insert(r->request_id);
+  q.prompt.assign(r->prompt, r->prompt + r->prompt_len);
+  q.admit_ns = now_ns();
+  q.arrival_ns = r->arrival_ns ? r->arrival_ns : q.admit_ns;
+  ctx->request_queue.push_back(std::move(q));
+  return SART_OK;
+}
+
+static void fill_stats(sart_ctx* ctx, sart_stats* o) {
+  if (!o) return;
+  o->windows = ctx->windows;
+  o->steps = ctx->steps;
+  o->live_rows = ctx->n_rows;
+  o->queued_branches = (int)ctx->branch_queue.size();
+  o->queued_requests = (int)ctx->request_queue.size();
+  o->finalized_total = ctx->finalized_total;
+  o->free_blocks = (int)ctx->free_top;
+  o->committed_blocks = (int)ctx->committed;
+  o->branch_tokens = ctx->branch_tokens;
+}
+
+int sart_step(sart_ctx* ctx, int32_t max_windows, sart_stats* out) {
+  if (!ctx) return set_err(SART_EINVAL, "null ctx");
+  if (ctx->poisoned) return set_err(SART_ESTATE, "ctx poisoned by an earlier CUDA error");
+  if (max_windows < 0) return set_err(SART_EINVAL, "max_windows < 0");
+  cudaSetDevice(ctx->cfg.device);
+  for (int w = 0; w < max_windows; ++w) {
+    int rc = fill(ctx);
+    if (rc) return rc;
+    if (ctx->n_rows == 0) break;   // idle
+    rc = ctx->bf16 ? run_window<bf16>(ctx) : run_window<float>(ctx);
+    if (rc) return rc;
+  }
+  fill_stats(ctx, out);
+  return SART_OK;
+}
+
+int sart_export_counters(sart_ctx* ctx, void* dev) {
+  if (!ctx || !dev) return set_err(SART_EINVAL, "null argument");
+  if (ctx->poisoned) return set_err(SART_ESTATE, "ctx poisoned");
+  int32_t c[16] = {ctx->n_rows, (int32_t)ctx->branch_queue.size(), (int32_t)ctx->request_queue.size(),
+                   (int32_t)ctx->free_top, (int32_t)ctx->committed, ctx->finalized_total, ctx->windows, ctx->steps,
+                   (int32_t)(ctx->branch_tokens & 0xffffffff), (int32_t)(ctx->branch_tokens >> 32), 0, 0, 0, 0, 0, 0};
+  CK(cudaMemcpyAsync(dev, c, sizeof(c), cudaMemcpyHostToDevice, ctx->st));
+  return SART_OK;
+}
+
+int sart_collect(sart_ctx* ctx, sart_result* out, int32_t cap, int32_t* n_out, int32_t* tokens_out,
+                 int64_t tokens_cap) {
+  if (!ctx || !n_out || (cap > 0 && !out)) return set_err(SART_EINVAL, "null argument");
+  if (ctx->poisoned) return set_err(SART_ESTATE, "ctx poisoned");
+  int n = 0;
+  int64_t used = 0;
+  while (!ctx->results.empty() && n < cap) {
+    HostResult& hr = ctx->results.front();
+    if (used + hr.r.tokens_len > tokens_cap || (hr.r.tokens_len > 0 && !tokens_out)) break;
+    out[n] = hr.r;
+    out[n].tokens_offset = used;
+    if (hr.r.tokens_len > 0) memcpy(tokens_out + used, hr.tokens.data(), sizeof(int32_t) * hr.r.tokens_len);
+    used += hr.r.tokens_len;
+    ++n;
+    ctx->results.pop_front();
+  }
+  *n_out = n;
+  if (!ctx->results.empty()) return set_err(SART_EFULL, "output buffers full; remaining results kept");
+  return SART_OK;
+}
+
+int sart_get_state(sart_ctx* ctx, sart_state* st) {
+  if (!ctx || !st) return set_err(SART_EINVAL, "null argument");
+  if (ctx->poisoned) return set_err(SART_ESTATE, "ctx poisoned");
+  const Dims& D = ctx->D;
+  CK(cudaStreamSynchronize(ctx->st));
+  const int n = ctx->n_rows;
+  st->n_rows = n;
+  st->n_free = (int)ctx->free_top;
+  st->committed = (int)ctx->committed;
+  if (n > st->rows_cap || st->n_free > st->free_cap) return set_err(SART_EFULL, "state buffers too small");
+  std::vector<int> slot(n), b(n), ell(n), nbnd(n), nblk(n), tab((size_t)n * D.MBR);
+  if (n) {
+    CK(cudaMemcpy(slot.data(), ctx->rows.slot, 4 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b.data(), ctx->rows.b, 4 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ell.data(), ctx->rows.ell, 4 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(nbnd.data(), ctx->rows.nbnd, 4 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(nblk.data(), ctx->rows.nblk, 4 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tab.data(), ctx->rows.table, 4 * tab.size(), cudaMemcpyDeviceToHost));
+  }
+  for (int r = 0; r < n; ++r) {
+    if (st->row_request_id) st->row_request_id[r] = ctx->slots[slot[r]].id;
+    if (st->row_branch) st->row_branch[r] = b[r];
+    if (st->row_ell) st->row_ell[r] = ell[r];
+    if (st->row_nbnd) st->row_nbnd[r] = nbnd[r];
+    if (st->row_table)
+      for (int j = 0; j < st->table_cap; ++j)
+        st->row_table[(size_t)r * st->table_cap + j] = j < nblk[r] && j < D.MBR ? tab[(size_t)r * D.MBR + j] : -1;
+  }
+  if (st->free_stack && st->n_free)
+    CK(cudaMemcpy(st->free_stack, ctx->free_stack, 4 * (size_t)st->n_free, cudaMemcpyDeviceToHost));
+  // live requests ascending by id
+  std::vector<std::pair<int64_t, int>> live;
+  for (int s = 0; s < D.S; ++s)
+    if (ctx->slots[s].live) live.emplace_back(ctx->slots[s].id, s);
+  std::sort(live.begin(), live.end());
+  st->n_live = (int)live.size();
+  if ((int)live.size() > st->live_cap) return set_err(SART_EFULL, "live_cap too small");
+  for (size_t i = 0; i < live.size(); ++i) {
+    const int s = live[i].second;
+    int v[6];
+    float thr;
+    CK(cudaMemcpy(&v[0], ctx->reqs.phase + s, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&thr, ctx->reqs.thr + s, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&v[1], ctx->reqs.maxp + s, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&v[2], ctx->reqs.nc + s, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&v[3], ctx->reqs.np + s, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&v[4], ctx->reqs.npre + s, 4, cudaMemcpyDeviceToHost));
+    if (st->live_request_id) st->live_request_id[i] = live[i].first;
+    if (st->live_phase) st->live_phase[i] = v[0];
+    if (st->live_threshold) st->live_threshold[i] = thr;
+    if (st->live_max_pruned) st->live_max_pruned[i] = v[1];
+    if (st->live_completed) st->live_completed[i] = v[2];
+    if (st->live_pruned) st->live_pruned[i] = v[3];
+    if (st->live_prefix_n) st->live_prefix_n[i] = v[4];
+    if (st->live_prefix && v[4] > 0) {
+      std::vector<int> pre(v[4]);
+      CK(cudaMemcpy(pre.data(), ctx->reqs.prefix + (size_t)s * D.MPB, 4 * v[4], cudaMemcpyDeviceToHost));
+      for (int j = 0; j < st->prefix_cap; ++j)
+        st->live_prefix[i * st->prefix_cap + j] = j < v[4] ? pre[j] : -1;
+    }
+  }
+  return SART_OK;
+}
+
+int sart_debug_fetch(sart_ctx* ctx, int32_t what, int32_t layer, void* host_out, size_t bytes, int32_t* n_rows) {
+  if (!ctx || !host_out) return set_err(SART_EINVAL, "null argument");
+  if (ctx->poisoned) return set_err(SART_ESTATE, "ctx poisoned");
+  const Dims& D = ctx->D;
+  const int n = ctx->last_n;
+  if (n_rows) *n_rows = n;
+  CK(cudaStreamSynchronize(ctx->st));
+  size_t need = 0;
+  const void* src = nullptr;
+  switch (what) {
+    case SART_DBG_LOGITS: need = (size_t)n * D.V * 4; src = ctx->logits; break;
+    case SART_DBG_TOKENS: need = (size_t)n * 4; src = ctx->dbg_tok; break;
+    case SART_DBG_SCORES:
+    case SART_DBG_PRM_SCORES: need = (size_t)n * 4; src = ctx->prm_score; break;
+    case SART_DBG_Z: need = (size_t)n * D.d * 4; src = ctx->z32; break;
+    case SART_DBG_ATTN:
+      if (!ctx->dbg_attn || layer < 0 || layer >= D.L) return set_err(SART_EINVAL, "needs debug_capture and a layer");
+      need = (size_t)n * D.qh * D.hd * 4;
+      src = ctx->dbg_attn + (size_t)layer * D.R * D.qh * D.hd;
+      break;
+    case SART_DBG_ROWIDS: {
+      need = (size_t)n * 8;
+      if (bytes < need) return set_err(SART_EFULL, "buffer too small");
+      std::vector<int> slot(n), b(n);
+      if (n) {
+        CK(cudaMemcpy(slot.data(), ctx->dbg_slot, 4 * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(b.data(), ctx->dbg_b, 4 * n, cudaMemcpyDeviceToHost));
+      }
+      int64_t* o = (int64_t*)host_out;
+      for (int r = 0; r < n; ++r) o[r] = (ctx->last_slot_id[slot[r]] << 8) | b[r];
+      return SART_OK;
+    }
+    default: return set_err(SART_EINVAL, "unknown debug tensor");
+  }
+  if (bytes < need) return set_err(SART_EFULL, "buffer too small");
+  if (need) CK(cudaMemcpy(host_out, src, need, cudaMemcpyDeviceToHost));
+  return SART_OK;
+}
+
+int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const uint16_t* B, const float* bias,
+                    float* C, int32_t mode) {
+  if (M < 1 || N < 1 || K < 1 || !A || !B || !C || mode < 0 || mode > 2) return set_err(SART_EINVAL, "bad args");
+  bf16 *dA = nullptr, *dB = nullptr, *dact = nullptr;
+  float *dC = nullptr, *dbias = nullptr;
+  const size_t outn = mode == GEMM_SWIGLU ? (size_t)M * (N / 2) : (size_t)M * N;
+  cudaError_t e = cudaSuccess;
+  auto chk = [&](cudaError_t x) { if (x != cudaSuccess && e == cudaSuccess) e = x; };
+  chk(cudaMalloc(&dA, 2 * (size_t)M * K));
+  chk(cudaMalloc(&dB, 2 * (size_t)N * K));
+  chk(cudaMalloc(&dC, 4 * (size_t)M * N));
+  chk(cudaMalloc(&dact, 2 * outn));
+  if (bias) chk(cudaMalloc(&dbias, 4 * (size_t)N));
+  if (e == cudaSuccess) {
+    chk(cudaMemcpy(dA, A, 2 * (size_t)M * K, cudaMemcpyHostToDevice));
+    chk(cudaMemcpy(dB, B, 2 * (size_t)N * K, cudaMemcpyHostToDevice));
+    if (bias) chk(cudaMemcpy(dbias, bias, 4 * (size_t)N, cudaMemcpyHostToDevice));
+    if (mode == GEMM_ACCUM) chk(cudaMemcpy(dC, C, 4 * (size_t)M * N, cudaMemcpyHostToDevice));
+    if (!launch_gemm_tc(dA, dB, dbias, dC, dact, M, N, K, mode, 0)) e = cudaErrorInvalidValue;
+    chk(cudaGetLastError());
+    chk(cudaDeviceSynchronize());
+    if (mode == GEMM_SWIGLU) {
+      std::vector<uint16_t> h(outn);
+      chk(cudaMemcpy(h.data(), dact, 2 * outn, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < outn; ++i) {
+        uint32_t u = (uint32_t)h[i] << 16;
+        memcpy(&C[i], &u, 4);
+      }
+    } else {
+      chk(cudaMemcpy(C, dC, 4 * (size_t)M * N, cudaMemcpyDeviceToHost));
+    }
+  }
+  cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dact); if (dbias) cudaFree(dbias);
+  if (e != cudaSuccess) return set_err(SART_ECUDA, cudaGetErrorString(e));
+  return SART_OK;
+}
+
+int sart_get_profile(sart_ctx* ctx, sart_profile* o) {
+  if (!ctx || !o) return set_err(SART_EINVAL, "null argument");
+  o->attn_ms = ctx->attn_ms;
+  o->attn_launches = ctx->attn_launches;
+  o->attn_bytes = ctx->attn_bytes;
+  o->kernel_launches = ctx->launches;
+  o->prefill_ms = ctx->prefill_ms;
+  return SART_OK;
+}
+int sart_reset_profile(sart_ctx* ctx) {
+  if (!ctx) return set_err(SART_EINVAL, "null argument");
+  ctx->attn_ms = ctx->attn_bytes = ctx->prefill_ms = 0;
+  ctx->attn_launches = ctx->launches = 0;
+  return SART_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,336 @@
+"""ctypes binding of include/sart.h (argument marshalling only).
+
+Names follow the C-ABI: ``Engine.admit`` -> ``sart_admit``, ``Engine.step`` ->
+``sart_step``, ``Engine.collect`` -> ``sart_collect`` ...  No torch types cross the
+boundary: device memory, if any, is passed as a plain integer address.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, List, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsart.so")
+
+SART_OK, SART_EINVAL, SART_ENOMEM, SART_ECUDA, SART_EFULL, SART_ESTATE, SART_EDUP = 0, -1, -2, -3, -4, -5, -6
+SART_BF16, SART_FP32 = 0, 1
+SART_ATTN_CASCADE, SART_ATTN_FLAT = 0, 1
+(BR_QUEUED, BR_RUNNING, BR_COMPLETED_EOS, BR_COMPLETED_CAP, BR_PRUNED, BR_EARLY_STOPPED,
+ BR_DISCARDED) = range(7)
+DBG_LOGITS, DBG_TOKENS, DBG_ROWIDS, DBG_SCORES, DBG_ATTN, DBG_Z, DBG_PRM_SCORES = range(7)
+
+
+class SartError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{msg} ({code})")
+        self.code = code
+
+
+class SartConfig(C.Structure):
+    _fields_ = [
+        ("n_layers", C.c_int32), ("d_model", C.c_int32), ("n_heads", C.c_int32),
+        ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("d_ff", C.c_int32), ("vocab", C.c_int32),
+        ("rope_theta", C.c_float), ("rms_eps", C.c_float), ("dtype", C.c_int32),
+        ("weight_seed", C.c_uint64), ("weight_std", C.c_float), ("host_weights", C.c_void_p),
+        ("block_size", C.c_int32), ("num_blocks", C.c_int64), ("max_rows", C.c_int32),
+        ("max_requests", C.c_int32), ("max_prompt", C.c_int32), ("ctl_interval", C.c_int32),
+        ("max_new_tokens", C.c_int32), ("eos_id", C.c_int32), ("temperature", C.c_float),
+        ("sampler_seed", C.c_uint64), ("select_mode", C.c_int32), ("attn_mode", C.c_int32),
+        ("device", C.c_int32), ("stream", C.c_void_p), ("enable_forced_tokens", C.c_int32),
+        ("debug_capture", C.c_int32), ("profile", C.c_int32),
+    ]
+
+
+class SartScript(C.Structure):
+    _fields_ = [("forced_len", C.POINTER(C.c_int32)), ("scores", C.POINTER(C.c_float)),
+                ("final_score", C.POINTER(C.c_float)), ("answer", C.POINTER(C.c_int32)),
+                ("n_bnd", C.c_int32), ("forced_tokens", C.POINTER(C.c_int32))]
+
+
+class SartRequest(C.Structure):
+    _fields_ = [("request_id", C.c_int64), ("prompt", C.POINTER(C.c_int32)), ("prompt_len", C.c_int32),
+                ("N", C.c_int32), ("M", C.c_int32), ("prune_threshold", C.c_float), ("beta", C.c_int32),
+                ("script", C.POINTER(SartScript)), ("arrival_ns", C.c_int64)]
+
+
+class SartStats(C.Structure):
+    _fields_ = [("windows", C.c_int32), ("steps", C.c_int32), ("live_rows", C.c_int32),
+                ("queued_branches", C.c_int32), ("queued_requests", C.c_int32),
+                ("finalized_total", C.c_int32), ("free_blocks", C.c_int32),
+                ("committed_blocks", C.c_int32), ("branch_tokens", C.c_int64)]
+
+
+class SartResult(C.Structure):
+    _fields_ = [("request_id", C.c_int64), ("answer_vote", C.c_int32), ("vote_count", C.c_int32),
+                ("chosen_max_reward", C.c_int32), ("answer_max_reward", C.c_int32),
+                ("num_completed", C.c_int32), ("num_pruned", C.c_int32), ("num_early_stopped", C.c_int32),
+                ("num_discarded_queued", C.c_int32), ("finalize_reason", C.c_int32),
+                ("phase_at_end", C.c_int32), ("threshold_at_end", C.c_float),
+                ("branch_len", C.c_int32 * 32), ("branch_state", C.c_uint8 * 32),
+                ("branch_score", C.c_float * 32), ("t_arrival_ns", C.c_int64), ("t_prefill_ns", C.c_int64),
+                ("t_final_ns", C.c_int64), ("window_final", C.c_int32), ("selected_branch", C.c_int32),
+                ("tokens_offset", C.c_int64), ("tokens_len", C.c_int32)]
+
+
+P32 = C.POINTER(C.c_int32)
+P64 = C.POINTER(C.c_int64)
+PF = C.POINTER(C.c_float)
+
+
+class SartState(C.Structure):
+    _fields_ = [("n_rows", C.c_int32), ("row_request_id", P64), ("row_branch", P32), ("row_ell", P32),
+                ("row_nbnd", P32), ("row_table", P32), ("rows_cap", C.c_int32), ("table_cap", C.c_int32),
+                ("n_free", C.c_int32), ("free_stack", P32), ("free_cap", C.c_int32), ("committed", C.c_int32),
+                ("n_live", C.c_int32), ("live_request_id", P64), ("live_phase", P32),
+                ("live_threshold", PF), ("live_max_pruned", P32), ("live_completed", P32),
+                ("live_pruned", P32), ("live_prefix", P32), ("live_prefix_n", P32), ("live_cap", C.c_int32),
+                ("prefix_cap", C.c_int32)]
+
+
+class SartProfile(C.Structure):
+    _fields_ = [("attn_ms", C.c_double), ("attn_launches", C.c_int64), ("attn_bytes", C.c_double),
+                ("kernel_launches", C.c_int64), ("prefill_ms", C.c_double)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Load libsart.so; raises if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -m paper_2505_13326_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(path)
+    lib.sart_init.argtypes = [C.POINTER(SartConfig), C.POINTER(C.c_void_p)]
+    lib.sart_admit.argtypes = [C.c_void_p, C.POINTER(SartRequest)]
+    lib.sart_step.argtypes = [C.c_void_p, C.c_int32, C.POINTER(SartStats)]
+    lib.sart_export_counters.argtypes = [C.c_void_p, C.c_void_p]
+    lib.sart_collect.argtypes = [C.c_void_p, C.POINTER(SartResult), C.c_int32, P32, P32, C.c_int64]
+    lib.sart_destroy.argtypes = [C.c_void_p]
+    lib.sart_strerror.argtypes = [C.c_int]
+    lib.sart_strerror.restype = C.c_char_p
+    lib.sart_last_error.restype = C.c_char_p
+    lib.sart_get_state.argtypes = [C.c_void_p, C.POINTER(SartState)]
+    lib.sart_debug_fetch.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t, P32]
+    lib.sart_get_profile.argtypes = [C.c_void_p, C.POINTER(SartProfile)]
+    lib.sart_reset_profile.argtypes = [C.c_void_p]
+    lib.sart_debug_gemm.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_int32]
+    for f in ("sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
+              "sart_get_state", "sart_debug_fetch", "sart_get_profile", "sart_reset_profile", "sart_debug_gemm"):
+        getattr(lib, f).restype = C.c_int
+    _lib = lib
+    return lib
+
+
+EXPORTED = ["sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
+            "sart_strerror", "sart_last_error", "sart_get_state", "sart_debug_fetch", "sart_get_profile",
+            "sart_reset_profile", "sart_debug_gemm"]
+
+
+def debug_gemm(A_bits: np.ndarray, B_bits: np.ndarray, bias=None, C=None, mode: int = 0) -> np.ndarray:
+    """sart_debug_gemm: A [M][K], B [N][K] as bf16 bit patterns (uint16)."""
+    lib = load_library()
+    A = np.ascontiguousarray(A_bits, np.uint16)
+    B = np.ascontiguousarray(B_bits, np.uint16)
+    M, K = A.shape
+    N = B.shape[0]
+    out = np.zeros((M, N // 2 if mode == 2 else N), np.float32) if C is None else np.ascontiguousarray(C, np.float32)
+    if mode == 1 and C is None:
+        raise ValueError("accumulate mode needs C")
+    bptr = None
+    if bias is not None:
+        bias = np.ascontiguousarray(bias, np.float32)
+        bptr = bias.ctypes.data
+    _check(lib.sart_debug_gemm(M, N, K, A.ctypes.data, B.ctypes.data, bptr, out.ctypes.data, mode))
+    return out
+
+
+def _check(rc: int):
+    if rc != SART_OK:
+        lib = load_library()
+        raise SartError(rc, f"{lib.sart_strerror(rc).decode()}: {lib.sart_last_error().decode()}")
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+class Engine:
+    """One sart_ctx on one GPU."""
+
+    def __init__(self, shape, dtype: str = "bf16", *, host_weights: Optional[np.ndarray] = None,
+                 weight_seed: int = 0, weight_std: float = 0.02, block_size: int = 64, num_blocks: int = 0,
+                 max_rows: int = 0, max_requests: int = 0, max_prompt: int = 0, T: int = 400, cap: int = 4096,
+                 eos_id: int = 1, temperature: float = 1.0, sampler_seed: int = 0, select_mode: int = 0,
+                 attn_mode: int = SART_ATTN_CASCADE, device: int = 0, stream: int = 0,
+                 enable_forced_tokens: bool = False, debug_capture: bool = False, profile: bool = False):
+        self.lib = load_library()
+        self.shape = shape
+        self.cap, self.T = cap, T
+        cfg = SartConfig()
+        cfg.n_layers, cfg.d_model, cfg.n_heads = shape.n_layers, shape.d_model, shape.n_heads
+        cfg.n_kv_heads, cfg.head_dim, cfg.d_ff, cfg.vocab = shape.n_kv_heads, shape.head_dim, shape.d_ff, shape.vocab
+        cfg.rope_theta, cfg.rms_eps = shape.rope_theta, shape.rms_eps
+        cfg.dtype = SART_BF16 if dtype == "bf16" else SART_FP32
+        cfg.weight_seed, cfg.weight_std = weight_seed, weight_std
+        self._weights = None
+        if host_weights is not None:
+            self._weights = np.ascontiguousarray(host_weights)
+            cfg.host_weights = self._weights.ctypes.data
+        cfg.block_size, cfg.num_blocks, cfg.max_rows = block_size, num_blocks, max_rows
+        cfg.max_requests, cfg.max_prompt, cfg.ctl_interval = max_requests, max_prompt, T
+        cfg.max_new_tokens, cfg.eos_id, cfg.temperature = cap, eos_id, temperature
+        cfg.sampler_seed, cfg.select_mode, cfg.attn_mode = sampler_seed, select_mode, attn_mode
+        cfg.device, cfg.stream = device, stream or None
+        cfg.enable_forced_tokens, cfg.debug_capture = int(enable_forced_tokens), int(debug_capture)
+        cfg.profile = int(profile)
+        h = C.c_void_p()
+        _check(self.lib.sart_init(C.byref(cfg), C.byref(h)))
+        self._weights = None
+        self.ctx = h
+        self.cfg = cfg
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.sart_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- sart_admit
+    def admit(self, req, forced_tokens: Optional[np.ndarray] = None, use_script_scores: bool = True,
+              use_answers: bool = True, forced_len: bool = True) -> None:
+        keep = []
+        prompt = _i32(req.prompt)
+        keep.append(prompt)
+        r = SartRequest()
+        r.request_id = req.request_id
+        r.prompt = prompt.ctypes.data_as(P32)
+        r.prompt_len = len(prompt)
+        r.N, r.M = req.N, req.M
+        r.prune_threshold = req.alpha
+        r.beta = req.beta
+        r.arrival_ns = getattr(req, "arrival_ns", 0)
+        sc = getattr(req, "script", None)
+        if sc is not None or forced_tokens is not None:
+            s = SartScript()
+            if sc is not None:
+                if forced_len:
+                    fl = _i32(sc.forced_len); keep.append(fl); s.forced_len = fl.ctypes.data_as(P32)
+                if use_script_scores:
+                    scores = np.ascontiguousarray(sc.scores, np.float32); keep.append(scores)
+                    fin = np.ascontiguousarray(sc.final_score, np.float32); keep.append(fin)
+                    s.scores, s.final_score = scores.ctypes.data_as(PF), fin.ctypes.data_as(PF)
+                    s.n_bnd = scores.shape[1]
+                if use_answers and sc.answer is not None:
+                    an = _i32(sc.answer); keep.append(an); s.answer = an.ctypes.data_as(P32)
+            if forced_tokens is not None:
+                ft = _i32(forced_tokens); keep.append(ft); s.forced_tokens = ft.ctypes.data_as(P32)
+            keep.append(s)
+            r.script = C.pointer(s)
+        _check(self.lib.sart_admit(self.ctx, C.byref(r)))
+
+    # ---------------------------------------------------------------- sart_step
+    def step(self, max_windows: int = 1) -> Dict[str, int]:
+        st = SartStats()
+        _check(self.lib.sart_step(self.ctx, max_windows, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in SartStats._fields_}
+
+    def export_counters(self, dev_ptr: int) -> None:
+        _check(self.lib.sart_export_counters(self.ctx, C.c_void_p(dev_ptr)))
+
+    # ---------------------------------------------------------------- sart_collect
+    def collect(self, cap: int = 4096, tokens_cap: int = 1 << 24) -> List[dict]:
+        out: List[dict] = []
+        while True:
+            res = (SartResult * cap)()
+            toks = np.zeros(tokens_cap, np.int32)
+            n = C.c_int32()
+            rc = self.lib.sart_collect(self.ctx, res, cap, C.byref(n), toks.ctypes.data_as(P32), tokens_cap)
+            if rc not in (SART_OK, SART_EFULL):
+                _check(rc)
+            for i in range(n.value):
+                r = res[i]
+                N = 32
+                d = {f: getattr(r, f) for f, _ in SartResult._fields_
+                     if f not in ("branch_len", "branch_state", "branch_score")}
+                d["branch_len"] = list(r.branch_len)[:N]
+                d["branch_state"] = list(r.branch_state)[:N]
+                d["branch_score"] = list(r.branch_score)[:N]
+                d["tokens"] = toks[r.tokens_offset:r.tokens_offset + r.tokens_len].tolist()
+                out.append(d)
+            if rc == SART_OK:
+                return out
+
+    # ---------------------------------------------------------------- test hooks
+    def state(self, rows_cap: int = 4096, table_cap: int = 512, free_cap: int = 1 << 22,
+              live_cap: int = 1024, prefix_cap: int = 256) -> dict:
+        s = SartState()
+        bufs = dict(row_request_id=np.zeros(rows_cap, np.int64), row_branch=np.zeros(rows_cap, np.int32),
+                    row_ell=np.zeros(rows_cap, np.int32), row_nbnd=np.zeros(rows_cap, np.int32),
+                    row_table=np.zeros(rows_cap * table_cap, np.int32), free_stack=np.zeros(free_cap, np.int32),
+                    live_request_id=np.zeros(live_cap, np.int64), live_phase=np.zeros(live_cap, np.int32),
+                    live_threshold=np.zeros(live_cap, np.float32), live_max_pruned=np.zeros(live_cap, np.int32),
+                    live_completed=np.zeros(live_cap, np.int32), live_pruned=np.zeros(live_cap, np.int32),
+                    live_prefix=np.zeros(live_cap * prefix_cap, np.int32), live_prefix_n=np.zeros(live_cap, np.int32))
+        for k, v in bufs.items():
+            ptype = P64 if v.dtype == np.int64 else (PF if v.dtype == np.float32 else P32)
+            setattr(s, k, v.ctypes.data_as(ptype))
+        s.rows_cap, s.table_cap, s.free_cap, s.live_cap, s.prefix_cap = rows_cap, table_cap, free_cap, live_cap, prefix_cap
+        _check(self.lib.sart_get_state(self.ctx, C.byref(s)))
+        n, nl = s.n_rows, s.n_live
+        tab = bufs["row_table"][: n * table_cap].reshape(n, table_cap)
+        pre = bufs["live_prefix"][: nl * prefix_cap].reshape(nl, prefix_cap)
+        return dict(
+            rows=[(int(bufs["row_request_id"][i]), int(bufs["row_branch"][i]), int(bufs["row_ell"][i]),
+                   int(bufs["row_nbnd"][i])) for i in range(n)],
+            tables=[[int(x) for x in tab[i] if x >= 0] for i in range(n)],
+            free=bufs["free_stack"][: s.n_free].tolist(), committed=s.committed,
+            meta={int(bufs["live_request_id"][i]): (int(bufs["live_phase"][i]), float(bufs["live_threshold"][i]),
+                                                    int(bufs["live_max_pruned"][i]), int(bufs["live_completed"][i]),
+                                                    int(bufs["live_pruned"][i]),
+                                                    [int(x) for x in pre[i][: bufs["live_prefix_n"][i]]])
+                  for i in range(nl)})
+
+    def debug_fetch(self, what: int, layer: int = 0) -> np.ndarray:
+        sh = self.shape
+        n = C.c_int32()
+        # query row count first with a tiny fetch
+        probe = np.zeros(1 << 16, np.int64)
+        _check(self.lib.sart_debug_fetch(self.ctx, DBG_ROWIDS, 0, probe.ctypes.data, probe.nbytes, C.byref(n)))
+        rows = n.value
+        if what == DBG_ROWIDS:
+            return probe[:rows].copy()
+        if what == DBG_LOGITS:
+            out = np.zeros((rows, sh.vocab), np.float32)
+        elif what in (DBG_TOKENS,):
+            out = np.zeros(rows, np.int32)
+        elif what in (DBG_SCORES, DBG_PRM_SCORES):
+            out = np.zeros(rows, np.float32)
+        elif what == DBG_ATTN:
+            out = np.zeros((rows, sh.n_heads * sh.head_dim), np.float32)
+        elif what == DBG_Z:
+            out = np.zeros((rows, sh.d_model), np.float32)
+        else:
+            raise ValueError(what)
+        _check(self.lib.sart_debug_fetch(self.ctx, what, layer, out.ctypes.data, out.nbytes, C.byref(n)))
+        return out
+
+    def profile(self) -> dict:
+        p = SartProfile()
+        _check(self.lib.sart_get_profile(self.ctx, C.byref(p)))
+        return {f: getattr(p, f) for f, _ in SartProfile._fields_}
+
+    def reset_profile(self) -> None:
+        _check(self.lib.sart_reset_profile(self.ctx))

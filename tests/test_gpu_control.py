@@ -1,0 +1,82 @@
+"""PP2: branch control on the GPU is bit-exact with the oracle replay.
+
+Scripted workloads (forced EOS steps, scripted rewards and labels) make every control
+decision a function of the script, so the oracle's Algorithm 1 engine (oracle/engine.py)
+and the CUDA path (boundary/admission kernels through the C-ABI) must agree on every
+integer after every window: row order, per-row steps, block tables, the free stack
+(contents and order), commitment, meta[i] (phase, threshold bits, caps, counters, prefix
+blocks), and the finalized records (votes, max-reward choice, branch states, lengths).
+"""
+import numpy as np
+import pytest
+
+from gpu_common import (compare_results, first_diff, gpu_engine, norm_gpu_state, norm_oracle_snapshot,
+                        oracle_engine)
+from synth import SHAPES, gen_requests, gen_weights
+
+pytestmark = pytest.mark.gpu
+
+
+def run_pair(shape, reqs, bs, nb, T, cap, B, select=0, windows=100000, check_every=1):
+    g = gpu_engine(shape, "bf16", None, block_size=bs, num_blocks=nb, max_rows=B, max_requests=64, max_prompt=2048,
+                   T=T, cap=cap, eos_id=1, select_mode=select, weight_seed=3)
+    o = oracle_engine(bs, nb, T, cap, B=B, select=select)
+    for r in reqs:
+        g.admit(r)
+        o.admit(r)
+    w = 0
+    while w < windows:
+        gs = g.step(1)
+        o.step(1)
+        w += 1
+        if w % check_every == 0 or gs["live_rows"] == 0:
+            a = norm_oracle_snapshot(o.snapshot())
+            b = norm_gpu_state(g.state())
+            d = first_diff(a, b)
+            assert d is None, f"window {w}: first diverging field {d[0]}\n oracle={d[1]}\n gpu   ={d[2]}"
+            assert gs["branch_tokens"] == o.branch_tokens and gs["steps"] == o.steps
+        if gs["live_rows"] == 0 and gs["queued_requests"] == 0 and gs["queued_branches"] == 0:
+            break
+    gres, ores = g.collect(), o.collect()
+    compare_results(gres, ores, {r.request_id: r.N for r in reqs})
+    g.close()
+    return gres
+
+
+def test_trace_A_on_gpu():
+    from tests_traces import trace_A_request
+    shape = SHAPES["tiny"]
+    res = run_pair(shape, [trace_A_request()], bs=16, nb=4096, T=16, cap=64, B=1 << 20)
+    assert res[0]["num_pruned"] == 3 and res[0]["finalize_reason"] == 1
+
+
+def test_trace_B_on_gpu():
+    from tests_traces import trace_B_request
+    shape = SHAPES["tiny"]
+    run_pair(shape, [trace_B_request()], bs=16, nb=17, T=16, cap=64, B=1 << 20)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_scripted_workloads(seed):
+    rng = np.random.default_rng(100 + seed)
+    shape = SHAPES["tiny"]
+    bs = int(rng.choice([16, 64]))
+    T = int(rng.choice([1, 4, 16]))
+    cap = int(rng.integers(8, 160))
+    N = int(rng.integers(1, 9))
+    M = int(rng.integers(1, N + 1))
+    reqs = gen_requests(int(rng.integers(2, 7)), shape, N, M, 0.5 if rng.random() < 0.7 else -1.0,
+                        int(rng.integers(0, N)), cap, T, eos_id=1, p_range=(1, 150), length="uniform",
+                        len_range=(1, cap), root_seed=seed)
+    need = max(-(-(len(r.prompt) - 1) // bs) for r in reqs) + -(-cap // bs)
+    nb = int(need + rng.integers(0, 3 * need))
+    B = int(rng.integers(1, 3 * N + 1)) if rng.random() < 0.5 else 1024
+    run_pair(shape, reqs, bs, nb, T, cap, B, select=int(rng.integers(0, 2)))
+
+
+def test_paper_defaults_many_requests():
+    """N=8, M=N/2, alpha=0.5, beta=N/2, a pool that forces queuing."""
+    shape = SHAPES["tiny"]
+    cap, T, bs = 96, 16, 16
+    reqs = gen_requests(12, shape, 8, 4, 0.5, 4, cap, T, eos_id=1, p_range=(20, 120), root_seed=11)
+    run_pair(shape, reqs, bs, nb=3 * (8 * 6 + 8), T=T, cap=cap, B=40, check_every=1)

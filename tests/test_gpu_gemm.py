@@ -1,0 +1,52 @@
+"""tcgen05 GEMM (k_gemm_tc.cu) through sart_debug_gemm vs a numpy fp64 product of the same
+bf16 operands.  fp32 accumulation over K: tolerance 1e-4 relative to max |C| (K <= 9K)."""
+import numpy as np
+import pytest
+
+from synth import bf16_bits, bits_to_f32
+
+pytestmark = pytest.mark.gpu
+
+
+def rnd(rng, shape, scale=1.0):
+    return bf16_bits(rng.standard_normal(shape).astype(np.float32) * scale)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 256, 64), (7, 512, 128), (128, 256, 256), (130, 2048, 1536),
+                                   (512, 1536, 8960), (37, 151936, 1536), (300, 4608, 3584), (129, 96, 64)])
+def test_gemm_store_bias(M, N, K):
+    rng = np.random.default_rng(M * 7 + N)
+    A, B = rnd(rng, (M, K)), rnd(rng, (N, K), 0.05)
+    bias = rng.standard_normal(N).astype(np.float32)
+    from paper_2505_13326_b200.sart import debug_gemm
+    C = debug_gemm(A, B, bias=bias, mode=0)
+    ref = bits_to_f32(A).astype(np.float64) @ bits_to_f32(B).astype(np.float64).T + bias
+    err = np.max(np.abs(C - ref)) / np.max(np.abs(ref))
+    assert err < 1e-4, err
+
+
+def test_gemm_accumulate():
+    rng = np.random.default_rng(1)
+    M, N, K = 200, 1536, 1536
+    A, B = rnd(rng, (M, K)), rnd(rng, (N, K), 0.05)
+    C0 = rng.standard_normal((M, N)).astype(np.float32)
+    from paper_2505_13326_b200.sart import debug_gemm
+    C = debug_gemm(A, B, C=C0.copy(), mode=1)
+    ref = C0 + bits_to_f32(A).astype(np.float64) @ bits_to_f32(B).astype(np.float64).T
+    assert np.max(np.abs(C - ref)) / np.max(np.abs(ref)) < 1e-4
+
+
+def test_gemm_swiglu_interleaved():
+    rng = np.random.default_rng(2)
+    M, F, K = 70, 1024, 512
+    A = rnd(rng, (M, K))
+    Wg, Wu = rnd(rng, (F, K), 0.05), rnd(rng, (F, K), 0.05)
+    # interleave in 256-row tiles [gate 128 | up 128]
+    B = np.concatenate([np.concatenate([Wg[t * 128:(t + 1) * 128], Wu[t * 128:(t + 1) * 128]]) for t in range(F // 128)])
+    from paper_2505_13326_b200.sart import debug_gemm
+    act = debug_gemm(A, B, mode=2)
+    a = bits_to_f32(A).astype(np.float64)
+    g = a @ bits_to_f32(Wg).astype(np.float64).T
+    u = a @ bits_to_f32(Wu).astype(np.float64).T
+    ref = g / (1 + np.exp(-g)) * u
+    assert np.max(np.abs(act - ref)) / np.max(np.abs(ref)) < 1e-2     # bf16 output rounding
