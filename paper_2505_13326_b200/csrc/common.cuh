@@ -91,6 +91,7 @@ struct Ctr {
   int n_final;
   int windows;
   long long branch_tokens;
+  double attn_bytes;   // algorithmic attention bytes (profiling)
   int final_slots[1]; // [S] (allocated with the struct)
 };
 

@@ -39,6 +39,20 @@ template <typename T> void launch_attn_decode_simple(const T* q, const T* pool, 
 template <typename T> void launch_attn_prefill(const T* q, const T* pool, T* out, Dims D, int layer, Reqs reqs,
                                                int slot, int p0, int n, cudaStream_t s);
 
+// cascade attention (k_attn_cascade.cu).  Per-window plan of work units.
+struct AttnPlan {
+  int4* units;      // {type (1 prefix / 0 suffix), group or row, chunk, 0}
+  int* n_units;
+  int* grp_slot;    // [R]
+  int* grp_n;       // [R]
+  int* grp_rows;    // [R][qr_max]
+  int qr_max, CH, npc_max, nslot;
+};
+void launch_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat, cudaStream_t s);
+void launch_attn_account(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, double* acc, cudaStream_t s);
+void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse,
+                         Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s);
+
 // ---- sampler (k_sample.cu)
 void launch_sample(const float* logits, Dims D, Rows rows, Reqs reqs, Ctr* ctr, int n, int* dbg_tok,
                    cudaStream_t s);

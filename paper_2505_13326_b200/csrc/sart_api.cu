@@ -96,6 +96,8 @@ struct sart_ctx {
   int* d_prompt = nullptr;
   AdmitEvent* d_events = nullptr;
   int ev_cap = 0;
+  AttnPlan plan{};
+  float *part_o = nullptr, *part_lse = nullptr;
 
   // host state
   std::deque<HostReq> request_queue;
@@ -116,7 +118,7 @@ struct sart_ctx {
   // profiling
   std::vector<cudaEvent_t> ev_pool;
   int ev_used = 0;
-  double attn_ms = 0, attn_bytes = 0, prefill_ms = 0;
+  double attn_ms = 0, attn_bytes = 0, attn_bytes_base = 0, prefill_ms = 0;
   long long attn_launches = 0, launches = 0;
 
   template <typename T> T* W_(int idx) const { return (T*)wblob + woff[idx]; }
@@ -258,8 +260,14 @@ void layer_attention(sart_ctx* ctx, int l, int n) {
     cudaEventRecord(e0, ctx->st);
   }
   float* dbg = ctx->dbg_attn ? ctx->dbg_attn + (size_t)l * D.R * D.qh * D.hd : nullptr;
-  launch_attn_decode_simple<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, dbg, D, l, ctx->rows, ctx->reqs, n, ctx->st);
-  ctx->launches++;
+  if constexpr (std::is_same<T, bf16>::value) {
+    launch_attn_cascade((bf16*)ctx->q, (bf16*)ctx->pool, (bf16*)ctx->o, dbg, ctx->part_o, ctx->part_lse, D, l,
+                        ctx->rows, ctx->reqs, ctx->plan, n, ctx->st);
+    ctx->launches += 2;
+  } else {
+    launch_attn_decode_simple<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, dbg, D, l, ctx->rows, ctx->reqs, n, ctx->st);
+    ctx->launches++;
+  }
   ctx->attn_launches++;
   if (e1) cudaEventRecord(e1, ctx->st);
 }
@@ -271,6 +279,10 @@ void decode_step(sart_ctx* ctx, int n) {
   launch_step_begin(ctx->ctr, s);
   launch_embed<T>(ctx->rows.tok, ctx->W_<T>(t_embed()), ctx->h, n, D.d, s);
   ctx->launches += 2;
+  if (ctx->cfg.profile) {
+    launch_attn_account(D, ctx->rows, ctx->reqs, ctx->plan, n, &ctx->ctr->attn_bytes, s);
+    ctx->launches++;
+  }
   for (int l = 0; l < D.L; ++l) {
     launch_rmsnorm<T>(ctx->h, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, n, D.d, D.eps, s);
     gemm<T>(ctx, (T*)ctx->a, ctx->W_<T>(t_layer(l, 1)), ctx->fparams + ctx->f_bqkv + (size_t)l * D.qkv, ctx->qkv, n,
@@ -462,6 +474,7 @@ int read_boundary(sart_ctx* ctx) {
   ctx->windows = c.windows;
   ctx->steps = c.steps;
   ctx->branch_tokens = c.branch_tokens;
+  ctx->attn_bytes = c.attn_bytes - ctx->attn_bytes_base;
   const int nf = c.n_final;
   if (nf == 0) return SART_OK;
   std::vector<int> fslots(c.final_slots, c.final_slots + nf);
@@ -536,6 +549,10 @@ int run_window(sart_ctx* ctx) {
   ctx->ev_used = 0;
   launch_window_begin(ctx->ctr, n, ctx->st);
   ctx->launches++;
+  if (ctx->bf16) {   // work units of the cascade attention for this window's batch
+    launch_attn_plan(D, ctx->rows, ctx->reqs, ctx->plan, n, ctx->cfg.attn_mode == SART_ATTN_FLAT, ctx->st);
+    ctx->launches++;
+  }
   for (int k = 1; k <= D.T; ++k) {
     if (k > 1 && (k % 8) == 1) {
       // live rows read back asynchronously; a window ends early when none is live (R31)
@@ -753,6 +770,24 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   ctx->ev_cap = D.R + D.S + 64;
   IC(dalloc(ctx, &ctx->d_events, sizeof(AdmitEvent) * ctx->ev_cap));
   if (cfg.debug_capture) IC(dalloc(ctx, &ctx->dbg_attn, (size_t)D.L * D.R * D.qh * D.hd * 4));
+  {  // cascade attention plan and partial outputs
+    AttnPlan& pl = ctx->plan;
+    pl.CH = 512;
+    pl.qr_max = std::max(1, std::min(SART_MAXN, 64 / D.g));
+    pl.npc_max = std::max(1, cdiv(cfg.max_prompt - 1, pl.CH));
+    const int nsc_max = cdiv(D.cap, pl.CH);
+    pl.nslot = pl.npc_max + nsc_max;
+    const size_t max_units = (size_t)D.R * (pl.npc_max + nsc_max);
+    IC(dalloc(ctx, &pl.units, sizeof(int4) * max_units));
+    IC(dalloc(ctx, &pl.n_units, sizeof(int)));
+    IC(dalloc(ctx, &pl.grp_slot, sizeof(int) * D.R));
+    IC(dalloc(ctx, &pl.grp_n, sizeof(int) * D.R));
+    IC(dalloc(ctx, &pl.grp_rows, sizeof(int) * (size_t)D.R * pl.qr_max));
+    if (ctx->bf16) {
+      IC(dalloc(ctx, &ctx->part_o, sizeof(float) * (size_t)D.R * D.qh * pl.nslot * D.hd, false));
+      IC(dalloc(ctx, &ctx->part_lse, sizeof(float) * (size_t)D.R * D.qh * pl.nslot, false));
+    }
+  }
   IC(cudaMallocHost(&ctx->h_ctr, sizeof(Ctr) + sizeof(int) * D.S));
   IC(cudaMallocHost(&ctx->h_live, sizeof(int)));
   // ---- KV pool
@@ -1055,6 +1090,7 @@ int sart_get_profile(sart_ctx* ctx, sart_profile* o) {
 }
 int sart_reset_profile(sart_ctx* ctx) {
   if (!ctx) return set_err(SART_EINVAL, "null argument");
+  ctx->attn_bytes_base += ctx->attn_bytes;
   ctx->attn_ms = ctx->attn_bytes = ctx->prefill_ms = 0;
   ctx->attn_launches = ctx->launches = 0;
   return SART_OK;
