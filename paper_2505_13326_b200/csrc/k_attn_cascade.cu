@@ -4,28 +4,29 @@
 //                                                           suffix (l+1 tokens, per branch)]
 //
 // PAPER P:306 shares the prompt's KV across a request's branches.  We read it ONCE per
-// request and kv head: a "prefix unit" multiplies the shared prefix KV by the queries of
-// all live branches of the request at once (up to 64 query rows = rows x g heads), while a
-// "suffix unit" covers one branch's private KV.  Every unit covers a chunk of <= CH tokens;
-// each writes a normalised partial output and its log-sum-exp, and a merge kernel combines
-// the partials of each (row, head) in a fixed order (deterministic, PP4).
+// request and kv head: a "prefix task" multiplies a chunk of the shared prefix KV by up to
+// 16 query rows (branches x g heads) of the request, a "suffix task" covers one branch's
+// private KV.  Every task covers <= CH tokens and writes a normalised partial output and its
+// log-sum-exp; a merge kernel combines the partials of each (row, head) in a fixed order, so
+// the result does not depend on scheduling (deterministic, PP4).
 //
-// Kernel structure (one persistent CTA per SM, 8 consumer warps + 1 producer warp):
-//   producer   one lane issues 1-D bulk copies (cp.async.bulk ... mbarrier::complete_tx) of
-//              whole paged blocks (bs x hd K tile and V tile, contiguous in the pool) into a
-//              4-stage ring of 64-token stages;
-//   consumers  two groups of 4 warps take alternate stages; mma.sync m16n8k16 bf16 for
-//              S = Q K^T and O += P V with fp32 online softmax; the pool's XOR pre-swizzle
-//              (common.cuh kv_swz) makes the ldmatrix reads bank-conflict free.
+// Kernel structure ("warp-autonomous" persistent kernel, one CTA per SM):
+//   * every warp takes items (task, kv head) from a work counter (dynamic load balance; an
+//     item's result does not depend on which warp computes it) and streams the item's KV
+//     through its OWN 2-stage ring of 32-token stages with 1-D bulk copies
+//     (cp.async.bulk ... mbarrier::complete_tx) of page-table tiles; the issue cursor runs
+//     ahead across item boundaries, so a warp always has its next 2 stages in flight;
+//   * mma.sync m16n8k16 bf16 computes S = Q K^T and O += P V with an fp32 online softmax;
+//     the pool's XOR pre-swizzle (common.cuh kv_swz) keeps the ldmatrix reads conflict-free;
+//   * no CTA-wide barriers and no cross-warp merges: warps never wait on each other.
 // Tensor cores are used because QK^T / PV are dense contractions, but the kernel is
-// HBM-bound (about g flop per byte); the design goal is bytes in flight, not MMA rate.
+// HBM-bound (about g flop per byte): the design goal is bytes in flight per SM.
 #include "kernels.h"
 
 namespace {
-constexpr int NCW = 8;                 // consumer warps
-constexpr int NTH = (NCW + 1) * 32;    // + producer warp
-constexpr int STG = 4;                 // pipeline stages
-constexpr int ST_TOK = 64;             // tokens per stage
+constexpr int NW = 6;          // warps per CTA (all consumers)
+constexpr int NS = 2;          // stages per warp ring
+constexpr int SW = 32;         // tokens per stage
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
@@ -33,9 +34,6 @@ __device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
 }
 __device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mb_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t par) {
   asm volatile(
@@ -45,9 +43,8 @@ __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t par) {
       "r"(par)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   s_u32(dst)),
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(s_u32(bar))
                : "memory");
 }
@@ -73,145 +70,151 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// Decoded work item.  Units come from the per-window plan; the token range depends on the
-// current step (rows grow by one token per step).
-struct ItemInfo {
-  int valid;        // 0: skip
-  int nq;           // query rows (<= 64)
-  int t0, t1;       // token range in the source sequence
-  const int* tab;   // block table of the source (prefix table or row table)
-  int slot_idx;     // partial-output slot index
-  int unit;
+// A decoded item: task (prefix/suffix chunk, m-tile) x kv head; token range for this step.
+struct Item {
+  int valid, task, h, t0, t1, nq, slot_idx;
+  const int* tab;
 };
 
-__device__ __forceinline__ ItemInfo decode_item(const AttnPlan& pl, const Dims& D, const Rows& rows, const Reqs& reqs,
-                                                int unit) {
-  ItemInfo it{};
-  it.unit = unit;
-  const int4 u = pl.units[unit];
-  const int type = u.x, c = u.z;
-  if (type == 0) {                               // suffix unit: (row, chunk)
+__device__ __forceinline__ Item decode_item(const AttnPlan& pl, const Dims& D, const Rows& rows, const Reqs& reqs,
+                                            int item) {
+  Item it{};
+  it.task = item / D.kvh;
+  it.h = item % D.kvh;
+  const int4 u = pl.units[it.task];
+  const int c = u.z;
+  if (u.x == 0) {                                // suffix task: (row, chunk)
     const int r = u.y;
     if (rows.status[r] != RUNNING_ST) return it;
-    const int len = rows.ell[r] + 1;
     it.t0 = c * pl.CH;
-    it.t1 = min(it.t0 + pl.CH, len);
-    if (it.t0 >= it.t1) return it;
+    it.t1 = min(it.t0 + pl.CH, rows.ell[r] + 1);
     it.nq = D.g;
     it.tab = rows.table + (long long)r * D.MBR;
     it.slot_idx = pl.npc_max + c;
-  } else {                                       // prefix unit: (group, chunk)
-    const int gi = u.y;
-    const int slot = pl.grp_slot[gi];
+  } else {                                       // prefix task: (group, chunk, m-tile)
+    const int gi = u.y, mt = u.w;
     const int n = pl.grp_n[gi];
+    const int q0 = mt * 16, q1 = min(n * D.g, q0 + 16);
     bool any = false;
-    for (int k = 0; k < n; ++k) any |= rows.status[pl.grp_rows[gi * pl.qr_max + k]] == RUNNING_ST;
+    for (int j = q0; j < q1; ++j) any |= rows.status[pl.grp_rows[gi * pl.qr_max + j / D.g]] == RUNNING_ST;
     if (!any) return it;
-    const int len = reqs.P[slot] - 1;
+    const int slot = pl.grp_slot[gi];
     it.t0 = c * pl.CH;
-    it.t1 = min(it.t0 + pl.CH, len);
-    if (it.t0 >= it.t1) return it;
-    it.nq = n * D.g;
+    it.t1 = min(it.t0 + pl.CH, reqs.P[slot] - 1);
+    it.nq = q1 - q0;
     it.tab = reqs.prefix + (long long)slot * D.MPB;
     it.slot_idx = c;
   }
-  it.valid = 1;
+  it.valid = it.t0 < it.t1;
   return it;
 }
 
-// query row j of an item -> (batch row, q head)
-__device__ __forceinline__ void q_of(const AttnPlan& pl, const Dims& D, int unit, int kvh, int j, int& row, int& head) {
-  const int4 u = pl.units[unit];
+// query row i (0..15) of an item -> (batch row, q head); false if beyond nq
+__device__ __forceinline__ bool q_of(const AttnPlan& pl, const Dims& D, const Item& it, int i, int& row,
+                                     int& head) {
+  if (i >= it.nq) return false;
+  const int4 u = pl.units[it.task];
   if (u.x == 0) {
     row = u.y;
-    head = kvh * D.g + j;
+    head = it.h * D.g + i;
   } else {
+    const int j = u.w * 16 + i;
     row = pl.grp_rows[u.y * pl.qr_max + j / D.g];
-    head = kvh * D.g + j % D.g;
+    head = it.h * D.g + j % D.g;
   }
+  return true;
 }
 
 template <int HD>
-struct SmemA {
-  alignas(128) bf16 k[STG][ST_TOK * HD];
-  alignas(128) bf16 v[STG][ST_TOK * HD];
-  float mo[NCW][16][HD];       // per-warp partial O (merge)
-  float mm[NCW][16], ml[NCW][16];
-  uint64_t full[STG], empty[STG];
+struct WarpSmem {
+  bf16 k[NS][SW * HD];
+  bf16 v[NS][SW * HD];
+  uint64_t full[NS];
+  uint64_t pad[8 - NS];
 };
 
 template <int HD>
-__global__ void __launch_bounds__(NTH, 1)
+__global__ void __launch_bounds__(NW * 32, 1)
     k_attn_cascade(const bf16* __restrict__ q, const bf16* __restrict__ pool, float* __restrict__ part_o,
                    float* __restrict__ part_lse, Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl) {
   extern __shared__ __align__(128) uint8_t sraw[];
-  SmemA<HD>& sm = *reinterpret_cast<SmemA<HD>*>(sraw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpSmem<HD>& sm = reinterpret_cast<WarpSmem<HD>*>(sraw)[warp];
   const int n_items = *pl.n_units * D.kvh;
+  int* work = pl.work + layer;
   const float sl2 = 1.4426950408889634f * rsqrtf((float)HD);   // log2(e) / sqrt(hd)
 
-  for (int e = threadIdx.x; e < STG * ST_TOK * HD / 8; e += NTH) {
+  // zero the ring once (masked tokens multiply V by 0, so stale smem must be finite)
+  for (int e = lane; e < NS * SW * HD / 8; e += 32) {
     reinterpret_cast<uint4*>(sm.k)[e] = make_uint4(0, 0, 0, 0);
     reinterpret_cast<uint4*>(sm.v)[e] = make_uint4(0, 0, 0, 0);
   }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes before bulk copies
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STG; ++s) { mb_init(&sm.full[s], 1); mb_init(&sm.empty[s], 4); }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
+  if (lane == 0)
+    for (int s = 0; s < NS; ++s) mb_init(&sm.full[s], 1);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
 
-  if (warp == NCW) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      const uint32_t tile_bytes = (uint32_t)D.bs * HD * 2;
-      for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
-        const int unit = i / D.kvh, h = i % D.kvh;
-        const ItemInfo it = decode_item(pl, D, rows, reqs, unit);
-        if (!it.valid) continue;
-        for (int s0 = it.t0; s0 < it.t1; s0 += ST_TOK) {
-          const int ntok = min(ST_TOK, it.t1 - s0);
-          const int nb = (ntok + D.bs - 1) / D.bs;
-          mb_wait(&sm.empty[stage], phase ^ 1);
-          mb_expect(&sm.full[stage], 2u * nb * tile_bytes);
-          for (int j = 0; j < nb; ++j) {
-            const long long blk = it.tab[(s0 / D.bs) + j];
-            const bf16* kt = pool + kv_tile_off(D, layer, blk, 0, h);
-            const bf16* vt = pool + kv_tile_off(D, layer, blk, 1, h);
-            bulk_g2s(sm.k[stage] + j * D.bs * HD, kt, tile_bytes, &sm.full[stage]);
-            bulk_g2s(sm.v[stage] + j * D.bs * HD, vt, tile_bytes, &sm.full[stage]);
-          }
-          if (++stage == STG) { stage = 0; phase ^= 1; }
+  // ---- issue side (warp-uniform state): ring of decoded items; the issue cursor runs up
+  //      to NS stages ahead of the consume cursor, across item boundaries
+  Item ring[NS + 1];
+  int r_head = 0, r_cnt = 0;       // consume item = ring[r_head]
+  int iss_idx = -1, iss_s0 = 0;    // ring index of the item being issued, next stage start
+  uint32_t issued = 0, consumed = 0;
+  bool exhausted = false;
+
+  auto refill = [&]() {
+    while (issued - consumed < (uint32_t)NS) {
+      if (iss_idx < 0 || iss_s0 >= ring[iss_idx].t1) {
+        if (exhausted || r_cnt == NS + 1) return;
+        Item nx{};
+        for (;;) {
+          int v = 0;
+          if (lane == 0) v = atomicAdd(work, 1);
+          const int i = __shfl_sync(0xffffffffu, v, 0);
+          if (i >= n_items) { exhausted = true; return; }
+          nx = decode_item(pl, D, rows, reqs, i);
+          if (nx.valid) break;
+        }
+        iss_idx = (r_head + r_cnt) % (NS + 1);
+        ring[iss_idx] = nx;
+        ++r_cnt;
+        iss_s0 = nx.t0;
+      }
+      const Item& it = ring[iss_idx];
+      const int slot = issued % NS;
+      if (lane == 0) {
+        // stage = tokens [iss_s0, iss_s0 + ntok): whole blocks (bs <= 32) or half a block (bs = 64)
+        const int ntok = min(SW, it.t1 - iss_s0);
+        const int tpb = min(D.bs, SW);
+        const int pieces = (ntok + tpb - 1) / tpb;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mb_expect(&sm.full[slot], 2u * pieces * tpb * HD * 2);
+        for (int p = 0; p < pieces; ++p) {
+          const int tok = iss_s0 + p * tpb;
+          const long long blk = it.tab[tok / D.bs];
+          const int inblk = tok % D.bs;
+          const bf16* kt = pool + kv_tile_off(D, layer, blk, 0, it.h) + (long long)inblk * HD;
+          const bf16* vt = pool + kv_tile_off(D, layer, blk, 1, it.h) + (long long)inblk * HD;
+          bulk_g2s(s_u32(sm.k[slot] + p * tpb * HD), kt, tpb * HD * 2, &sm.full[slot]);
+          bulk_g2s(s_u32(sm.v[slot] + p * tpb * HD), vt, tpb * HD * 2, &sm.full[slot]);
         }
       }
+      iss_s0 += SW;
+      ++issued;
     }
-    return;
-  }
+  };
 
-  // -------------------------------------------------------------- consumers
-  const int grp = warp >> 2, wg = warp & 3;          // stage group, warp within group
-  uint32_t gk = 0;                                   // CTA-global stage counter (same as the producer's)
-  for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
-    const int unit = i / D.kvh, h = i % D.kvh;
-    const ItemInfo it = decode_item(pl, D, rows, reqs, unit);
-    if (!it.valid) continue;
-    const int mt = it.nq <= 16 ? 1 : (it.nq <= 32 ? 2 : 4);   // m-tiles of 16 query rows
-    const int wpt = 4 / mt;                                   // warps per m-tile within a group
-    const int mtile = wg % mt;
-    const int slice = wg / mt;                                // token slice of the stage
-    const int slice_tok = ST_TOK / wpt;                       // 64, 32 or 16 tokens
-    // Q fragments of this warp's m-tile (16 rows x HD), zero beyond nq
+  refill();
+  while (r_cnt > 0) {
+    const Item it = ring[r_head];
+    // Q fragments (16 rows x HD) of this item, zero beyond nq
     uint32_t qa[HD / 16][4];
     {
-      const int r0 = mtile * 16 + (lane >> 2), r1 = r0 + 8;
-      const bf16* q0 = nullptr;
-      const bf16* q1 = nullptr;
+      const int r0 = lane >> 2, r1 = r0 + 8, cc = 2 * (lane & 3);
       int row, head;
-      if (r0 < it.nq) { q_of(pl, D, unit, h, r0, row, head); q0 = q + ((long long)row * D.qh + head) * HD; }
-      if (r1 < it.nq) { q_of(pl, D, unit, h, r1, row, head); q1 = q + ((long long)row * D.qh + head) * HD; }
-      const int cc = 2 * (lane & 3);
+      const bf16* q0 = q_of(pl, D, it, r0, row, head) ? q + ((long long)row * D.qh + head) * HD : nullptr;
+      const bf16* q1 = q_of(pl, D, it, r1, row, head) ? q + ((long long)row * D.qh + head) * HD : nullptr;
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
         qa[kk][0] = q0 ? *reinterpret_cast<const uint32_t*>(q0 + 16 * kk + cc) : 0u;
@@ -225,131 +228,120 @@ __global__ void __launch_bounds__(NTH, 1)
     for (int nt = 0; nt < HD / 8; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
-    for (int s0 = it.t0; s0 < it.t1; s0 += ST_TOK, ++gk) {
-      const int stage = gk % STG;
-      const uint32_t phase = (gk / STG) & 1;
-      if ((gk & 1) == (uint32_t)grp) {                // the two warp groups take alternate stages
-        mb_wait(&sm.full[stage], phase);
-        const int ntok = min(ST_TOK, it.t1 - s0);
-        const uint32_t kb = s_u32(sm.k[stage]), vb = s_u32(sm.v[stage]);
-        for (int sub = slice * slice_tok; sub < slice * slice_tok + slice_tok; sub += 16) {
-          if (sub >= ntok) break;
-          // S = Q K^T for 16 tokens [sub, sub+16)
-          float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    for (int s0 = it.t0; s0 < it.t1; s0 += SW) {
+      const int slot = consumed % NS;
+      mb_wait(&sm.full[slot], (consumed / NS) & 1);
+      const int ntok = min(SW, it.t1 - s0);
+      const uint32_t kb = s_u32(sm.k[slot]), vb = s_u32(sm.v[slot]);
 #pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            const int mi = lane >> 3;
-            const int tok = sub + (lane & 7) + 8 * (mi >> 1);
-            const int ch = 2 * kk + (mi & 1);
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4(kb + tok * (HD * 2) + ((ch ^ (tok & 7)) << 4), b0, b1, b2, b3);
+      for (int sub = 0; sub < SW; sub += 16) {
+        if (sub >= ntok) break;
+        float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        float s2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};   // 2nd accumulator: shorter chains
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const int mi = lane >> 3;
+          const int tok = sub + (lane & 7) + 8 * (mi >> 1);
+          const int ch = 2 * kk + (mi & 1);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(kb + tok * (HD * 2) + ((ch ^ (tok & 7)) << 4), b0, b1, b2, b3);
+          if (kk & 1) {
+            mma16816(s2[0], qa[kk], b0, b1);
+            mma16816(s2[1], qa[kk], b2, b3);
+          } else {
             mma16816(s[0], qa[kk], b0, b1);
             mma16816(s[1], qa[kk], b2, b3);
           }
-          // mask tokens beyond the valid range
-          const int cbase = sub + 2 * (lane & 3);
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (cbase + nt * 8 + (e & 1) >= ntok) s[nt][e] = -INFINITY;
-          // online softmax (rows r = lane/4 -> m0/l0, r+8 -> m1/l1)
-          float mx0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
-          float mx1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
-          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-          const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
-          const float u0 = n0 == -INFINITY ? 0.f : n0, u1 = n1 == -INFINITY ? 0.f : n1;
-          const float c0 = exp2f((m0 - u0) * sl2), c1 = exp2f((m1 - u1) * sl2);
-          m0 = n0;
-          m1 = n1;
-          float p[2][4];
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            p[nt][0] = exp2f((s[nt][0] - u0) * sl2);
-            p[nt][1] = exp2f((s[nt][1] - u0) * sl2);
-            p[nt][2] = exp2f((s[nt][2] - u1) * sl2);
-            p[nt][3] = exp2f((s[nt][3] - u1) * sl2);
-          }
-          l0 = l0 * c0 + p[0][0] + p[0][1] + p[1][0] + p[1][1];
-          l1 = l1 * c1 + p[0][2] + p[0][3] + p[1][2] + p[1][3];
-#pragma unroll
-          for (int nt = 0; nt < HD / 8; ++nt) { o[nt][0] *= c0; o[nt][1] *= c0; o[nt][2] *= c1; o[nt][3] *= c1; }
-          uint32_t pa[4];
-          pa[0] = pack_bf16(p[0][0], p[0][1]);
-          pa[1] = pack_bf16(p[0][2], p[0][3]);
-          pa[2] = pack_bf16(p[1][0], p[1][1]);
-          pa[3] = pack_bf16(p[1][2], p[1][3]);
-          // O += P V : V rows = tokens [sub, sub+16), ldmatrix.trans per pair of hd n-tiles
-#pragma unroll
-          for (int dp = 0; dp < HD / 16; ++dp) {
-            const int mi = lane >> 3;
-            const int tok = sub + (lane & 7) + 8 * (mi & 1);
-            const int ch = 2 * dp + (mi >> 1);
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(vb + tok * (HD * 2) + ((ch ^ (tok & 7)) << 4), b0, b1, b2, b3);
-            mma16816(o[2 * dp], pa, b0, b1);
-            mma16816(o[2 * dp + 1], pa, b2, b3);
-          }
         }
-        __syncwarp();
-        if (lane == 0) mb_arrive(&sm.empty[stage]);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) s[nt][e] += s2[nt][e];
+        const int cbase = sub + 2 * (lane & 3);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (cbase + nt * 8 + (e & 1) >= ntok) s[nt][e] = -INFINITY;
+        float mx0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
+        float mx1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+        const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
+        const float u0 = n0 == -INFINITY ? 0.f : n0, u1 = n1 == -INFINITY ? 0.f : n1;
+        const float c0 = exp2f((m0 - u0) * sl2), c1 = exp2f((m1 - u1) * sl2);
+        m0 = n0;
+        m1 = n1;
+        float p[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          p[nt][0] = exp2f((s[nt][0] - u0) * sl2);
+          p[nt][1] = exp2f((s[nt][1] - u0) * sl2);
+          p[nt][2] = exp2f((s[nt][2] - u1) * sl2);
+          p[nt][3] = exp2f((s[nt][3] - u1) * sl2);
+        }
+        l0 = l0 * c0 + p[0][0] + p[0][1] + p[1][0] + p[1][1];
+        l1 = l1 * c1 + p[0][2] + p[0][3] + p[1][2] + p[1][3];
+#pragma unroll
+        for (int nt = 0; nt < HD / 8; ++nt) { o[nt][0] *= c0; o[nt][1] *= c0; o[nt][2] *= c1; o[nt][3] *= c1; }
+        uint32_t pa[4];
+        pa[0] = pack_bf16(p[0][0], p[0][1]);
+        pa[1] = pack_bf16(p[0][2], p[0][3]);
+        pa[2] = pack_bf16(p[1][0], p[1][1]);
+        pa[3] = pack_bf16(p[1][2], p[1][3]);
+#pragma unroll
+        for (int dp = 0; dp < HD / 16; ++dp) {
+          const int mi = lane >> 3;
+          const int tok = sub + (lane & 7) + 8 * (mi & 1);
+          const int ch = 2 * dp + (mi >> 1);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(vb + tok * (HD * 2) + ((ch ^ (tok & 7)) << 4), b0, b1, b2, b3);
+          mma16816(o[2 * dp], pa, b0, b1);
+          mma16816(o[2 * dp + 1], pa, b2, b3);
+        }
       }
+      __syncwarp();
+      ++consumed;
+      refill();              // re-fill the slot just consumed (next stage of this or a later item)
     }
-    // ---- per-warp row sums, then cross-warp merge through shared memory
+    // ---- item done: normalise and write the partial (rows r = lane/4 and r + 8)
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
     {
-      const int r = lane >> 2, cc = 2 * (lane & 3);
+      const int r0 = lane >> 2, cc = 2 * (lane & 3);
 #pragma unroll
-      for (int nt = 0; nt < HD / 8; ++nt) {
-        sm.mo[warp][r][nt * 8 + cc] = o[nt][0];
-        sm.mo[warp][r][nt * 8 + cc + 1] = o[nt][1];
-        sm.mo[warp][r + 8][nt * 8 + cc] = o[nt][2];
-        sm.mo[warp][r + 8][nt * 8 + cc + 1] = o[nt][3];
-      }
-      if ((lane & 3) == 0) {
-        sm.mm[warp][r] = m0; sm.ml[warp][r] = l0;
-        sm.mm[warp][r + 8] = m1; sm.ml[warp][r + 8] = l1;
+      for (int half = 0; half < 2; ++half) {
+        int row, head;
+        if (!q_of(pl, D, it, r0 + 8 * half, row, head)) continue;
+        const float m = half ? m1 : m0, l = half ? l1 : l0;
+        const float inv = 1.0f / l;
+        const long long pi = ((long long)row * D.qh + head) * pl.nslot + it.slot_idx;
+        float* dst = part_o + pi * HD;
+#pragma unroll
+        for (int nt = 0; nt < HD / 8; ++nt)
+          *reinterpret_cast<float2*>(dst + nt * 8 + cc) =
+              make_float2(o[nt][2 * half] * inv, o[nt][2 * half + 1] * inv);
+        if ((lane & 3) == 0) part_lse[pi] = (m == -INFINITY ? 0.f : m) * sl2 + log2f(l);
       }
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32));
-    // merge: warps with the same m-tile are {g*4 + s*mt + mtile}; thread handles (row, col) pairs
-    for (int e = threadIdx.x; e < mt * 16 * HD; e += NCW * 32) {
-      const int qrow = e / HD, col = e % HD;
-      const int mtl = qrow / 16, rr = qrow % 16;
-      if (qrow >= it.nq) continue;
-      float M = -INFINITY;
-      for (int g2 = 0; g2 < 2; ++g2)
-        for (int s2 = 0; s2 < wpt; ++s2) M = fmaxf(M, sm.mm[g2 * 4 + s2 * mt + mtl][rr]);
-      float L = 0.f, O = 0.f;
-      const float Mu = M == -INFINITY ? 0.f : M;
-      for (int g2 = 0; g2 < 2; ++g2)
-        for (int s2 = 0; s2 < wpt; ++s2) {
-          const int w2 = g2 * 4 + s2 * mt + mtl;
-          const float wgt = exp2f((sm.mm[w2][rr] - Mu) * sl2);
-          L += sm.ml[w2][rr] * wgt;
-          O += sm.mo[w2][rr][col] * wgt;
-        }
-      int row, head;
-      q_of(pl, D, unit, h, qrow, row, head);
-      const long long pi = ((long long)row * D.qh + head) * pl.nslot + it.slot_idx;
-      part_o[pi * HD + col] = O / L;
-      if (col == 0) part_lse[pi] = Mu * sl2 + log2f(L);          // log2-domain LSE
-    }
-    asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32));
+    r_head = (r_head + 1) % (NS + 1);
+    --r_cnt;
+    if (r_cnt == 0) iss_idx = -1;
+    refill();
   }
 }
 
-// merge the partials of each (row, head) in fixed slot order; o (bf16) and optional fp32 debug
+// merge the partials of each (row, head) in fixed slot order; o (bf16) and optional fp32 debug.
+// Block 0 also resets this layer's work counter for the next step.
 template <int HD>
 __global__ void k_attn_merge(const float* __restrict__ part_o, const float* __restrict__ part_lse,
-                             bf16* __restrict__ out, float* __restrict__ dbg, Dims D, Rows rows, Reqs reqs,
-                             AttnPlan pl, int n) {
+                             bf16* __restrict__ out, float* __restrict__ dbg, Dims D, int layer, Rows rows,
+                             Reqs reqs, AttnPlan pl, int n) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) pl.work[layer] = 0;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= n * D.qh) return;
   const int r = wid / D.qh, head = wid % D.qh;
@@ -380,24 +372,24 @@ __global__ void k_attn_merge(const float* __restrict__ part_o, const float* __re
 }
 
 // ------------------------------------------------------------------ per-window plan
-// Units: prefix units first (type 1: group, chunk), then suffix units (type 0: row, chunk).
-// Groups: the window's rows of one request in batch order, qr rows per group (cascade) or
-// one row per group (flat mode).  Built once per window: rows only change at boundaries.
+// Tasks: prefix tasks first (type 1: group, chunk, m-tile), then suffix tasks (type 0: row,
+// chunk).  Groups: the window's rows of one request in batch order, qr rows per group
+// (cascade) or one row per group (flat mode).  Built once per window: the batch only
+// changes at boundaries; tasks whose rows finished mid-window are skipped at run time.
 __global__ void __launch_bounds__(1024) k_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat) {
   const int tid = threadIdx.x;
   __shared__ int s_rank[1024], s_nrows[1024];
   const int qr = flat ? 1 : pl.qr_max;
-  // rank of each row among the rows of its request (batch order); count at the leader
   for (int r = tid; r < n; r += 1024) {
     const int slot = rows.slot[r];
     int rank = 0, tot = 0;
     for (int r2 = 0; r2 < n; ++r2)
       if (rows.slot[r2] == slot) { rank += r2 < r; ++tot; }
-    if (r < 1024) { s_rank[r] = rank; s_nrows[r] = tot; }
+    s_rank[r] = rank;
+    s_nrows[r] = tot;
   }
   __syncthreads();
   if (tid == 0) {
-    // groups in batch order of their leaders; prefix units; suffix units
     int ng = 0, nu = 0;
     for (int r = 0; r < n; ++r) {
       if (s_rank[r] != 0) continue;
@@ -408,9 +400,10 @@ __global__ void __launch_bounds__(1024) k_attn_plan(Dims D, Rows rows, Reqs reqs
         const int gi = ng + k;
         pl.grp_slot[gi] = slot;
         pl.grp_n[gi] = min(qr, s_nrows[r] - k * qr);
-        for (int c = 0; c < npc; ++c) pl.units[nu++] = make_int4(1, gi, c, 0);
+        const int mts = (pl.grp_n[gi] * D.g + 15) / 16;
+        for (int c = 0; c < npc; ++c)
+          for (int mt = 0; mt < mts; ++mt) pl.units[nu++] = make_int4(1, gi, c, mt);
       }
-      // rows of this request in batch order fill the groups
       int k = 0;
       for (int r2 = r; r2 < n; ++r2)
         if (rows.slot[r2] == slot) { pl.grp_rows[(ng + k / qr) * pl.qr_max + k % qr] = r2; ++k; }
@@ -427,15 +420,13 @@ __global__ void __launch_bounds__(1024) k_attn_plan(Dims D, Rows rows, Reqs reqs
 
 // algorithmic KV bytes of one step's attention (all layers): prefix once per request with a
 // running row, each running suffix once, plus q and o (profiling only)
-__global__ void __launch_bounds__(1024) k_attn_account(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n,
-                                                       double* acc) {
+__global__ void __launch_bounds__(1024) k_attn_account(Dims D, Rows rows, Reqs reqs, int n, double* acc) {
   __shared__ double red[32];
   double b = 0.0;
   const double kvtok = 2.0 * D.kvh * D.hd * 2.0;   // K+V bytes per token per layer (bf16)
   for (int r = threadIdx.x; r < n; r += 1024) {
     if (rows.status[r] != RUNNING_ST) continue;
     b += (rows.ell[r] + 1) * kvtok + 2.0 * D.qh * D.hd * 2.0;
-    // prefix once per request: counted at the lowest running row of the request
     bool first = true;
     for (int r2 = 0; r2 < r; ++r2)
       if (rows.slot[r2] == rows.slot[r] && rows.status[r2] == RUNNING_ST) { first = false; break; }
@@ -456,25 +447,28 @@ void launch_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat
   k_attn_plan<<<1, 1024, 0, s>>>(D, rows, reqs, pl, n, flat);
 }
 void launch_attn_account(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, double* acc, cudaStream_t s) {
-  k_attn_account<<<1, 1024, 0, s>>>(D, rows, reqs, pl, n, acc);
+  (void)pl;
+  k_attn_account<<<1, 1024, 0, s>>>(D, rows, reqs, n, acc);
 }
 
 static int g_sms = 0;
+template <int HD>
+static void launch_hd(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse, Dims D,
+                      int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s) {
+  const size_t sm = sizeof(WarpSmem<HD>) * NW;
+  static bool a = false;
+  if (!a) {
+    cudaFuncSetAttribute(k_attn_cascade<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    a = true;
+  }
+  k_attn_cascade<HD><<<g_sms, NW * 32, sm, s>>>(q, pool, part_o, part_lse, D, layer, rows, reqs, pl);
+  k_attn_merge<HD><<<(n * D.qh * 32 + 255) / 256, 256, 0, s>>>(part_o, part_lse, out, dbg, D, layer, rows, reqs, pl,
+                                                               n);
+}
 void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse,
                          Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s) {
   if (n <= 0) return;
   if (!g_sms) cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0);
-  if (D.hd == 128) {
-    const size_t sm = sizeof(SmemA<128>);
-    static bool a = false;
-    if (!a) { cudaFuncSetAttribute(k_attn_cascade<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); a = true; }
-    k_attn_cascade<128><<<g_sms, NTH, sm, s>>>(q, pool, part_o, part_lse, D, layer, rows, reqs, pl);
-    k_attn_merge<128><<<(n * D.qh * 32 + 255) / 256, 256, 0, s>>>(part_o, part_lse, out, dbg, D, rows, reqs, pl, n);
-  } else {
-    const size_t sm = sizeof(SmemA<64>);
-    static bool a = false;
-    if (!a) { cudaFuncSetAttribute(k_attn_cascade<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); a = true; }
-    k_attn_cascade<64><<<g_sms, NTH, sm, s>>>(q, pool, part_o, part_lse, D, layer, rows, reqs, pl);
-    k_attn_merge<64><<<(n * D.qh * 32 + 255) / 256, 256, 0, s>>>(part_o, part_lse, out, dbg, D, rows, reqs, pl, n);
-  }
+  if (D.hd == 128) launch_hd<128>(q, pool, out, dbg, part_o, part_lse, D, layer, rows, reqs, pl, n, s);
+  else launch_hd<64>(q, pool, out, dbg, part_o, part_lse, D, layer, rows, reqs, pl, n, s);
 }

@@ -98,15 +98,26 @@ struct Smem {
 
 // MODE: GEMM_STORE (C = AB^T + bias), GEMM_ACCUM (C += AB^T), GEMM_SWIGLU (columns of each
 // BN tile are [gate(BN/2) | up(BN/2)] of interleaved weights; writes bf16 act[m][F]).
+// Split-K: work unit u -> (m-tile = u % mt, split, n-tile); split s covers k-blocks
+// [s*kb/S, (s+1)*kb/S) and writes its fp32 partial tile to C + s*M*N.  The consumer kernel
+// (RMSNorm / RoPE) sums the S partials in split order, so the result is deterministic.
 template <int BN, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* C,
-              const float* __restrict__ bias, bf16* act, int M, int N, int K) {
+              const float* __restrict__ bias, bf16* act, int M, int N, int K, int S) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem<BN>& sm = *reinterpret_cast<Smem<BN>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN, ntiles = mt * nt;
-  const int kb_n = (K + BK - 1) / BK;
+  const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN, ntiles = mt * nt * S;
+  const int kb_all = (K + BK - 1) / BK;
+  auto unit_of = [&](int t, int& m0, int& n0, int& kb0, int& kb1, int& sp) {
+    m0 = (t % mt) * BM;
+    const int rest = t / mt;
+    sp = rest % S;
+    n0 = (rest / S) * BN;
+    kb0 = sp * kb_all / S;
+    kb1 = (sp + 1) * kb_all / S;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], 1); }
@@ -130,8 +141,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
-        for (int kb = 0; kb < kb_n; ++kb) {
+        int m0, n0, kb0, kb1, sp;
+        unit_of(t, m0, n0, kb0, kb1, sp);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&sm.empty[stage], phase ^ 1);
           mbar_expect_tx(&sm.full[stage], (BM + BN) * BK * 2);
           tma_load_2d(sm.a[stage], &tmA, &sm.full[stage], kb * BK, m0);
@@ -149,19 +161,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int as = it & 1;
       const uint32_t aph = (it >> 1) & 1;
+      int m0, n0, kb0, kb1, sp;
+      unit_of(t, m0, n0, kb0, kb1, sp);
       mbar_wait(&sm.tempty[as], aph ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t d = tmem + as * BN;
-      for (int kb = 0; kb < kb_n; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&sm.full[stage], phase);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (lane == 0) {
           const uint32_t a0 = smem_u32(sm.a[stage]), b0 = smem_u32(sm.b[stage]);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d, umma_desc(a0 + k * 32), umma_desc(b0 + k * 32), idesc, (kb | k) ? 1u : 0u);
+            umma_bf16(d, umma_desc(a0 + k * 32), umma_desc(b0 + k * 32), idesc, (kb > kb0 || k) ? 1u : 0u);
           umma_commit(&sm.empty[stage]);
-          if (kb == kb_n - 1) umma_commit(&sm.tfull[as]);
+          if (kb == kb1 - 1) umma_commit(&sm.tfull[as]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -175,14 +189,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int as = it & 1;
       const uint32_t aph = (it >> 1) & 1;
-      const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+      int m0, n0, kb0, kb1, sp;
+      unit_of(t, m0, n0, kb0, kb1, sp);
+      float* Cs = C + (size_t)sp * M * N;
       mbar_wait(&sm.tfull[as], aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const int gm = m0 + row;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + as * BN;
       if (MODE == GEMM_SWIGLU) {
         const int F = N / 2;   // N = 2F interleaved in BN-wide tiles
-        const int f0 = (t / mt) * (BN / 2);
+        const int f0 = n0 / 2;
 #pragma unroll 1
         for (int c = 0; c < BN / 2; c += 32) {
           float g[32], u[32];
@@ -211,7 +227,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tmem_ld32(tbase + c, v);
           const int gn = n0 + c;
           if (gm < M && gn < N) {
-            float* dst = C + (size_t)gm * N + gn;
+            float* dst = Cs + (size_t)gm * N + gn;
             if (gn + 32 <= N) {
 #pragma unroll
               for (int j = 0; j < 32; j += 4) {
@@ -291,7 +307,7 @@ MapCache g_maps;
 int g_num_sms = 0;
 
 template <int BN, int MODE>
-bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
+bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K, int S,
                cudaStream_t s) {
   const CUtensorMap* ma = g_maps.get(A, M, K, BM);
   const CUtensorMap* mb = g_maps.get(B, N, K, BN);
@@ -303,18 +319,45 @@ bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* 
     attr = true;
   }
   if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
-  const int ntiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int ntiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * S;
   const int grid = ntiles < g_num_sms ? ntiles : g_num_sms;
-  k_gemm_tc<BN, MODE><<<grid, NTHREADS, smem, s>>>(*ma, *mb, C, bias, act, M, N, K);
+  k_gemm_tc<BN, MODE><<<grid, NTHREADS, smem, s>>>(*ma, *mb, C, bias, act, M, N, K, S);
   return true;
 }
 }  // namespace
 
 bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
                     int mode, cudaStream_t s) {
+  return launch_gemm_tc_split(A, B, bias, C, act, M, N, K, mode, 1, 256, s);
+}
+
+bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
+                          int mode, int S, int BN, cudaStream_t s) {
   if (M <= 0 || N <= 0) return true;
   if (K % 8) return false;   // TMA row stride must be a multiple of 16 bytes
-  if (mode == GEMM_STORE) return launch_bn<256, GEMM_STORE>(A, B, bias, C, act, M, N, K, s);
-  if (mode == GEMM_ACCUM) return launch_bn<256, GEMM_ACCUM>(A, B, bias, C, act, M, N, K, s);
-  return launch_bn<256, GEMM_SWIGLU>(A, B, bias, C, act, M, N, K, s);
+  const int kb = (K + BK - 1) / BK;
+  if (S < 1 || S > kb || (mode == GEMM_SWIGLU && S != 1)) return false;
+  if (BN == 128) {
+    if (mode == GEMM_STORE) return launch_bn<128, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s);
+    if (mode == GEMM_ACCUM) return launch_bn<128, GEMM_ACCUM>(A, B, bias, C, act, M, N, K, S, s);
+    return false;
+  }
+  if (mode == GEMM_STORE) return launch_bn<256, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s);
+  if (mode == GEMM_ACCUM) return launch_bn<256, GEMM_ACCUM>(A, B, bias, C, act, M, N, K, S, s);
+  return launch_bn<256, GEMM_SWIGLU>(A, B, bias, C, act, M, N, K, S, s);
+}
+
+// Split choice for the decode GEMMs: enough (tile x split) units to cover the SMs.
+void choose_split(int M, int N, int K, int& S, int& BN) {
+  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
+  const int mt = (M + BM - 1) / BM;
+  const int t256 = mt * ((N + 255) / 256);
+  if (t256 >= g_num_sms * 3 / 4) { S = 1; BN = 256; return; }
+  BN = 128;
+  const int t128 = mt * ((N + 127) / 128);
+  const int kb = (K + BK - 1) / BK;
+  S = (g_num_sms + t128 / 2) / t128;
+  if (S < 1) S = 1;
+  if (S > 8) S = 8;
+  if (S > kb / 2) S = kb / 2 > 0 ? kb / 2 : 1;
 }

@@ -40,17 +40,25 @@ void launch_embed(const int* tok, const T* emb, float* h, int n, int d, cudaStre
   if (n > 0) k_embed<T><<<n, 256, 0, s>>>(tok, emb, h, d);
 }
 
-// ------------------------------------------------------------ RMSNorm
-// out = h * rsqrt(mean(h^2) + eps) * g ; rows with status != RUNNING are skipped when
-// status is given (the final norm keeps the z of finished rows for the PRM, O6).
+// ------------------------------------------------------------ RMSNorm (+ residual partials)
+// h[r] += sum_{s < np} parts[s][r]   (split-K partials of the previous projection, summed in
+// split order: deterministic), then out = h * rsqrt(mean(h^2) + eps) * g.  Rows with status
+// != RUNNING are skipped when status is given (the final norm keeps the z of finished rows
+// for the PRM, O6).
 template <typename T>
-__global__ void k_rmsnorm(const float* __restrict__ h, const T* __restrict__ g, T* __restrict__ out,
-                          float* __restrict__ out32, const int* __restrict__ status, int d, float eps) {
+__global__ void k_rmsnorm(float* __restrict__ h, const float* __restrict__ parts, int np, long long pstride,
+                          const T* __restrict__ g, T* __restrict__ out, float* __restrict__ out32,
+                          const int* __restrict__ status, int d, float eps) {
   int r = blockIdx.x;
   if (status && status[r] != RUNNING_ST) return;
-  const float* x = h + (long long)r * d;
+  float* x = h + (long long)r * d;
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += x[i] * x[i];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float v = x[i];
+    for (int sp = 0; sp < np; ++sp) v += parts[sp * pstride + (long long)r * d + i];
+    if (np) x[i] = v;
+    ss += v * v;
+  }
   __shared__ float red[32];
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
@@ -69,9 +77,9 @@ __global__ void k_rmsnorm(const float* __restrict__ h, const T* __restrict__ g, 
   }
 }
 template <typename T>
-void launch_rmsnorm(const float* h, const T* g, T* out, float* out32, const int* status, int n, int d,
-                    float eps, cudaStream_t s) {
-  if (n > 0) k_rmsnorm<T><<<n, 256, 0, s>>>(h, g, out, out32, status, d, eps);
+void launch_rmsnorm(float* h, const float* parts, int np, const T* g, T* out, float* out32, const int* status, int n,
+                    int d, float eps, cudaStream_t s) {
+  if (n > 0) k_rmsnorm<T><<<n, 256, 0, s>>>(h, parts, np, (long long)n * d, g, out, out32, status, d, eps);
 }
 
 // ------------------------------------------------------------ RoPE + KV append
@@ -79,7 +87,8 @@ void launch_rmsnorm(const float* h, const T* g, T* out, float* out32, const int*
 // paged pool.  Decode: suffix entry l of row r at table[r][l/bs], slot l%bs, position
 // P-1+l.  Prefill: prefix position p0+r at prefix[slot][p/bs], slot p%bs.
 template <typename T>
-__global__ void k_rope_append(const float* __restrict__ qkv, T* __restrict__ qout, T* __restrict__ pool,
+__global__ void k_rope_append(const float* __restrict__ parts, int np, long long pstride,
+                              const float* __restrict__ bias, T* __restrict__ qout, T* __restrict__ pool,
                               const float* __restrict__ rope_cs, Dims D, int layer, Rows rows, Reqs reqs,
                               RopeArgs a) {
   int r = blockIdx.x;
@@ -97,12 +106,14 @@ __global__ void k_rope_append(const float* __restrict__ qkv, T* __restrict__ qou
     slot_in_blk = l % D.bs;
   }
   const int half = D.hd / 2;
-  const float* x = qkv + (long long)r * D.qkv;
+  const float* x = parts + (long long)r * D.qkv;
   const float* cs = rope_cs + (long long)pos * D.hd;   // [cos(half) | sin(half)]
   int pairs = (D.qh + 2 * D.kvh) * half;
   for (int t = threadIdx.x; t < pairs; t += blockDim.x) {
     int head = t / half, i = t % half;
-    float x1 = x[head * D.hd + i], x2 = x[head * D.hd + i + half];
+    const int e1 = head * D.hd + i, e2 = e1 + half;
+    float x1 = bias[e1], x2 = bias[e2];
+    for (int sp = 0; sp < np; ++sp) { x1 += x[sp * pstride + e1]; x2 += x[sp * pstride + e2]; }   // split order
     if (head < D.qh + D.kvh) {                      // q or k: rotate-half
       float c = cs[i], sn = cs[half + i];
       float y1 = x1 * c - x2 * sn, y2 = x2 * c + x1 * sn;
@@ -122,9 +133,11 @@ __global__ void k_rope_append(const float* __restrict__ qkv, T* __restrict__ qou
   }
 }
 template <typename T>
-void launch_rope_append(const float* qkv, T* qout, T* pool, const float* rope_cs, Dims D, int layer, Rows rows,
-                        Reqs reqs, RopeArgs a, int n, cudaStream_t s) {
-  if (n > 0) k_rope_append<T><<<n, 256, 0, s>>>(qkv, qout, pool, rope_cs, D, layer, rows, reqs, a);
+void launch_rope_append(const float* parts, int np, const float* bias, T* qout, T* pool, const float* rope_cs, Dims D,
+                        int layer, Rows rows, Reqs reqs, RopeArgs a, int n, cudaStream_t s) {
+  if (n > 0)
+    k_rope_append<T><<<n, 256, 0, s>>>(parts, np, (long long)n * D.qkv, bias, qout, pool, rope_cs, D, layer, rows,
+                                       reqs, a);
 }
 
 // ------------------------------------------------------------ SwiGLU: act = SiLU(g) * u
@@ -195,10 +208,10 @@ void launch_to_f32(const T* in, float* out, long long n, cudaStream_t s) {
 #define INST(T)                                                                                        \
   template void launch_init_tensor<T>(T*, long long, int, int, float, unsigned long long, cudaStream_t); \
   template void launch_embed<T>(const int*, const T*, float*, int, int, cudaStream_t);                  \
-  template void launch_rmsnorm<T>(const float*, const T*, T*, float*, const int*, int, int, float,      \
-                                  cudaStream_t);                                                        \
-  template void launch_rope_append<T>(const float*, T*, T*, const float*, Dims, int, Rows, Reqs,        \
-                                      RopeArgs, int, cudaStream_t);                                     \
+  template void launch_rmsnorm<T>(float*, const float*, int, const T*, T*, float*, const int*, int, int, \
+                                  float, cudaStream_t);                                                 \
+  template void launch_rope_append<T>(const float*, int, const float*, T*, T*, const float*, Dims, int, \
+                                      Rows, Reqs, RopeArgs, int, cudaStream_t);                         \
   template void launch_swiglu<T>(const float*, T*, int, int, cudaStream_t);                             \
   template void launch_convert<T>(const float*, T*, long long, cudaStream_t);                           \
   template void launch_to_f32<T>(const T*, float*, long long, cudaStream_t);

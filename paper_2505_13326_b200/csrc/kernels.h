@@ -6,15 +6,17 @@
 template <typename T> void launch_init_tensor(T* p, long long n, int tensor_id, int is_norm, float std,
                                               unsigned long long seed, cudaStream_t s);
 template <typename T> void launch_embed(const int* tok, const T* emb, float* h, int n, int d, cudaStream_t s);
-template <typename T> void launch_rmsnorm(const float* h, const T* g, T* out, float* out32, const int* status,
-                                          int n, int d, float eps, cudaStream_t s);
+// h[r] += sum_{s<np} parts[s][r] (fixed order; np may be 0), then out = RMSNorm(h) * g
+template <typename T> void launch_rmsnorm(float* h, const float* parts, int np, const T* g, T* out, float* out32,
+                                          const int* status, int n, int d, float eps, cudaStream_t s);
 struct RopeArgs {
   // decode mode (slot == -1): per-row positions from Rows/Reqs; prefill mode: slot >= 0
   int prefill_slot, p0;
 };
-template <typename T> void launch_rope_append(const float* qkv, T* qout, T* pool, const float* rope_cs,
-                                              Dims D, int layer, Rows rows, Reqs reqs, RopeArgs a, int n,
-                                              cudaStream_t s);
+// qkv = sum_{s<np} parts[s] + bias (fixed order), then RoPE + paged KV append
+template <typename T> void launch_rope_append(const float* parts, int np, const float* bias, T* qout, T* pool,
+                                              const float* rope_cs, Dims D, int layer, Rows rows, Reqs reqs,
+                                              RopeArgs a, int n, cudaStream_t s);
 template <typename T> void launch_swiglu(const float* gu, T* act, int n, int F, cudaStream_t s);
 void launch_prm_head2(const float* hid, const float* w2, const float* b2, float* score, int n, int d,
                       cudaStream_t s);
@@ -32,6 +34,10 @@ template <typename T> void launch_gemm_simt(const T* A, const T* B, const float*
 bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
                     int mode, cudaStream_t s);
 void launch_interleave_gate_up(bf16* w, bf16* tmp, int F, int d, cudaStream_t s);
+// split-K variant: S partial products written to C + s*M*N (summed by the consumer kernel)
+bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
+                          int mode, int S, int BN, cudaStream_t s);
+void choose_split(int M, int N, int K, int& S, int& BN);
 
 // ---- attention (k_attn.cu)
 template <typename T> void launch_attn_decode_simple(const T* q, const T* pool, T* out, float* dbg, Dims D,
@@ -41,8 +47,9 @@ template <typename T> void launch_attn_prefill(const T* q, const T* pool, T* out
 
 // cascade attention (k_attn_cascade.cu).  Per-window plan of work units.
 struct AttnPlan {
-  int4* units;      // {type (1 prefix / 0 suffix), group or row, chunk, 0}
+  int4* units;      // tasks {type (1 prefix / 0 suffix), group or row, chunk, m-tile}
   int* n_units;
+  int* work;        // [L] dynamic work counters (reset by the merge kernel)
   int* grp_slot;    // [R]
   int* grp_n;       // [R]
   int* grp_rows;    // [R][qr_max]

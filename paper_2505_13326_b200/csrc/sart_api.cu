@@ -88,7 +88,7 @@ struct sart_ctx {
   int* free_stack = nullptr;
   DevResult* res = nullptr;
   int* slot_row = nullptr;
-  float *h = nullptr, *qkv = nullptr, *gu = nullptr, *z32 = nullptr, *logits = nullptr, *prm_hid = nullptr,
+  float *h = nullptr, *parts = nullptr, *gu = nullptr, *z32 = nullptr, *logits = nullptr, *prm_hid = nullptr,
         *prm_score = nullptr, *rope_cs = nullptr, *dbg_attn = nullptr;
   void *a = nullptr, *q = nullptr, *o = nullptr, *act = nullptr, *zT = nullptr;
   int* dbg_tok = nullptr;
@@ -233,6 +233,24 @@ void gemm(sart_ctx* ctx, const T* A, const T* B, const float* bias, float* C, in
   ctx->launches++;
 }
 
+// Projection whose consumer is a reduction kernel (RMSNorm residual add or RoPE): the bf16
+// path uses split-K so that small-N projections still cover all SMs; the S partials land in
+// ctx->parts and the consumer sums them in split order.  Returns S.
+template <typename T>
+int proj(sart_ctx* ctx, const T* A, const T* B, int M, int N, int K) {
+  int S = 1;
+  if constexpr (std::is_same<T, bf16>::value) {
+    int BN = 256;
+    choose_split(M, N, K, S, BN);
+    if (!launch_gemm_tc_split(A, B, nullptr, ctx->parts, nullptr, M, N, K, GEMM_STORE, S, BN, ctx->st))
+      ctx->gemm_failed = true;
+  } else {
+    launch_gemm_simt<T>(A, B, nullptr, ctx->parts, M, N, K, GEMM_STORE, ctx->st);
+  }
+  ctx->launches++;
+  return S;
+}
+
 // MLP up-projection + SwiGLU: fused tcgen05 epilogue on gate/up-interleaved weights (bf16),
 // or GEMM + elementwise kernel (fp32 mode).
 template <typename T>
@@ -283,21 +301,24 @@ void decode_step(sart_ctx* ctx, int n) {
     launch_attn_account(D, ctx->rows, ctx->reqs, ctx->plan, n, &ctx->ctr->attn_bytes, s);
     ctx->launches++;
   }
+  int np_res = 0;   // pending residual partials (previous layer's down projection)
   for (int l = 0; l < D.L; ++l) {
-    launch_rmsnorm<T>(ctx->h, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, n, D.d, D.eps, s);
-    gemm<T>(ctx, (T*)ctx->a, ctx->W_<T>(t_layer(l, 1)), ctx->fparams + ctx->f_bqkv + (size_t)l * D.qkv, ctx->qkv, n,
-            D.qkv, D.d, GEMM_STORE);
-    launch_rope_append<T>(ctx->qkv, (T*)ctx->q, (T*)ctx->pool, ctx->rope_cs, D, l, ctx->rows, ctx->reqs,
-                          RopeArgs{-1, 0}, n, s);
+    launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, n, D.d,
+                      D.eps, s);
+    int np = proj<T>(ctx, (T*)ctx->a, ctx->W_<T>(t_layer(l, 1)), n, D.qkv, D.d);
+    launch_rope_append<T>(ctx->parts, np, ctx->fparams + ctx->f_bqkv + (size_t)l * D.qkv, (T*)ctx->q, (T*)ctx->pool,
+                          ctx->rope_cs, D, l, ctx->rows, ctx->reqs, RopeArgs{-1, 0}, n, s);
     ctx->launches += 2;
     layer_attention<T>(ctx, l, n);
-    gemm<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), nullptr, ctx->h, n, D.d, D.qh * D.hd, GEMM_ACCUM);
-    launch_rmsnorm<T>(ctx->h, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, n, D.d, D.eps, s);
+    np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), n, D.d, D.qh * D.hd);
+    launch_rmsnorm<T>(ctx->h, ctx->parts, np, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, n, D.d, D.eps,
+                      s);
     mlp_up<T>(ctx, l, n);
-    gemm<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), nullptr, ctx->h, n, D.d, D.F, GEMM_ACCUM);
+    np_res = proj<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), n, D.d, D.F);
     ctx->launches += 1;
   }
-  launch_rmsnorm<T>(ctx->h, ctx->W_<T>(t_final(D)), (T*)ctx->zT, ctx->z32, ctx->rows.status, n, D.d, D.eps, s);
+  launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_final(D)), (T*)ctx->zT, ctx->z32, ctx->rows.status, n,
+                    D.d, D.eps, s);
   gemm<T>(ctx, (T*)ctx->zT, ctx->W_<T>(t_lm(D)), nullptr, ctx->logits, n, D.V, D.d, GEMM_STORE);
   launch_sample(ctx->logits, D, ctx->rows, ctx->reqs, ctx->ctr, n, ctx->dbg_tok, s);
   ctx->launches += 2;
@@ -312,19 +333,21 @@ void prefill(sart_ctx* ctx, int slot, int P) {
     const int c = std::min(ctx->PC, ntok - p0);
     launch_embed<T>(ctx->d_prompt + p0, ctx->W_<T>(t_embed()), ctx->h, c, D.d, s);
     ctx->launches++;
+    int np_res = 0;
     for (int l = 0; l < D.L; ++l) {
-      launch_rmsnorm<T>(ctx->h, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, c, D.d, D.eps, s);
-      gemm<T>(ctx, (T*)ctx->a, ctx->W_<T>(t_layer(l, 1)), ctx->fparams + ctx->f_bqkv + (size_t)l * D.qkv, ctx->qkv,
-              c, D.qkv, D.d, GEMM_STORE);
-      launch_rope_append<T>(ctx->qkv, (T*)ctx->q, (T*)ctx->pool, ctx->rope_cs, D, l, ctx->rows, ctx->reqs,
-                            RopeArgs{slot, p0}, c, s);
+      launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, c, D.d,
+                        D.eps, s);
+      int np = proj<T>(ctx, (T*)ctx->a, ctx->W_<T>(t_layer(l, 1)), c, D.qkv, D.d);
+      launch_rope_append<T>(ctx->parts, np, ctx->fparams + ctx->f_bqkv + (size_t)l * D.qkv, (T*)ctx->q,
+                            (T*)ctx->pool, ctx->rope_cs, D, l, ctx->rows, ctx->reqs, RopeArgs{slot, p0}, c, s);
       ctx->launches += 2;
       if (l == D.L - 1) break;  // the last layer's output is not part of the prefix KV
       launch_attn_prefill<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, D, l, ctx->reqs, slot, p0, c, s);
-      gemm<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), nullptr, ctx->h, c, D.d, D.qh * D.hd, GEMM_ACCUM);
-      launch_rmsnorm<T>(ctx->h, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, c, D.d, D.eps, s);
+      np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), c, D.d, D.qh * D.hd);
+      launch_rmsnorm<T>(ctx->h, ctx->parts, np, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, c, D.d,
+                        D.eps, s);
       mlp_up<T>(ctx, l, c);
-      gemm<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), nullptr, ctx->h, c, D.d, D.F, GEMM_ACCUM);
+      np_res = proj<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), c, D.d, D.F);
       ctx->launches += 2;
     }
   }
@@ -752,7 +775,7 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   // ---- workspaces
   const size_t W = ctx->W;
   IC(dalloc(ctx, &ctx->h, W * D.d * 4));
-  IC(dalloc(ctx, &ctx->qkv, W * D.qkv * 4));
+  IC(dalloc(ctx, &ctx->parts, W * std::max(D.qkv, D.d) * 8 * 4, false));   // split-K partials (S <= 8)
   IC(dalloc(ctx, &ctx->gu, W * 2 * D.F * 4));
   IC(dalloc(ctx, &ctx->z32, (size_t)D.R * D.d * 4));
   IC(dalloc(ctx, &ctx->logits, (size_t)D.R * D.V * 4));
@@ -777,9 +800,10 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     pl.npc_max = std::max(1, cdiv(cfg.max_prompt - 1, pl.CH));
     const int nsc_max = cdiv(D.cap, pl.CH);
     pl.nslot = pl.npc_max + nsc_max;
-    const size_t max_units = (size_t)D.R * (pl.npc_max + nsc_max);
+    const size_t max_units = (size_t)D.R * (4 * pl.npc_max + nsc_max);
     IC(dalloc(ctx, &pl.units, sizeof(int4) * max_units));
     IC(dalloc(ctx, &pl.n_units, sizeof(int)));
+    IC(dalloc(ctx, &pl.work, sizeof(int) * D.L));
     IC(dalloc(ctx, &pl.grp_slot, sizeof(int) * D.R));
     IC(dalloc(ctx, &pl.grp_n, sizeof(int) * D.R));
     IC(dalloc(ctx, &pl.grp_rows, sizeof(int) * (size_t)D.R * pl.qr_max));
@@ -1043,8 +1067,10 @@ int sart_debug_fetch(sart_ctx* ctx, int32_t what, int32_t layer, void* host_out,
 }
 
 int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const uint16_t* B, const float* bias,
-                    float* C, int32_t mode) {
-  if (M < 1 || N < 1 || K < 1 || !A || !B || !C || mode < 0 || mode > 2) return set_err(SART_EINVAL, "bad args");
+                    float* C, int32_t mode, int32_t splits, int32_t bn) {
+  if (M < 1 || N < 1 || K < 1 || !A || !B || !C || mode < 0 || mode > 2 || splits < 1 || splits > 8 ||
+      (bn != 128 && bn != 256))
+    return set_err(SART_EINVAL, "bad args");
   bf16 *dA = nullptr, *dB = nullptr, *dact = nullptr;
   float *dC = nullptr, *dbias = nullptr;
   const size_t outn = mode == GEMM_SWIGLU ? (size_t)M * (N / 2) : (size_t)M * N;
@@ -1052,7 +1078,7 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
   auto chk = [&](cudaError_t x) { if (x != cudaSuccess && e == cudaSuccess) e = x; };
   chk(cudaMalloc(&dA, 2 * (size_t)M * K));
   chk(cudaMalloc(&dB, 2 * (size_t)N * K));
-  chk(cudaMalloc(&dC, 4 * (size_t)M * N));
+  chk(cudaMalloc(&dC, 4 * (size_t)M * N * splits));
   chk(cudaMalloc(&dact, 2 * outn));
   if (bias) chk(cudaMalloc(&dbias, 4 * (size_t)N));
   if (e == cudaSuccess) {
@@ -1060,7 +1086,7 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
     chk(cudaMemcpy(dB, B, 2 * (size_t)N * K, cudaMemcpyHostToDevice));
     if (bias) chk(cudaMemcpy(dbias, bias, 4 * (size_t)N, cudaMemcpyHostToDevice));
     if (mode == GEMM_ACCUM) chk(cudaMemcpy(dC, C, 4 * (size_t)M * N, cudaMemcpyHostToDevice));
-    if (!launch_gemm_tc(dA, dB, dbias, dC, dact, M, N, K, mode, 0)) e = cudaErrorInvalidValue;
+    if (!launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, 0)) e = cudaErrorInvalidValue;
     chk(cudaGetLastError());
     chk(cudaDeviceSynchronize());
     if (mode == GEMM_SWIGLU) {
@@ -1071,7 +1097,7 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
         memcpy(&C[i], &u, 4);
       }
     } else {
-      chk(cudaMemcpy(C, dC, 4 * (size_t)M * N, cudaMemcpyDeviceToHost));
+      chk(cudaMemcpy(C, dC, 4 * (size_t)M * N * splits, cudaMemcpyDeviceToHost));
     }
   }
   cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dact); if (dbias) cudaFree(dbias);

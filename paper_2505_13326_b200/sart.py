@@ -121,7 +121,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.sart_get_profile.argtypes = [C.c_void_p, C.POINTER(SartProfile)]
     lib.sart_reset_profile.argtypes = [C.c_void_p]
     lib.sart_debug_gemm.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                    C.c_int32]
+                                    C.c_int32, C.c_int32, C.c_int32]
     for f in ("sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
               "sart_get_state", "sart_debug_fetch", "sart_get_profile", "sart_reset_profile", "sart_debug_gemm"):
         getattr(lib, f).restype = C.c_int
@@ -134,21 +134,26 @@ EXPORTED = ["sart_init", "sart_admit", "sart_step", "sart_export_counters", "sar
             "sart_reset_profile", "sart_debug_gemm"]
 
 
-def debug_gemm(A_bits: np.ndarray, B_bits: np.ndarray, bias=None, C=None, mode: int = 0) -> np.ndarray:
-    """sart_debug_gemm: A [M][K], B [N][K] as bf16 bit patterns (uint16)."""
+def debug_gemm(A_bits: np.ndarray, B_bits: np.ndarray, bias=None, C=None, mode: int = 0, splits: int = 1,
+               bn: int = 256) -> np.ndarray:
+    """sart_debug_gemm: A [M][K], B [N][K] as bf16 bit patterns (uint16).  With splits > 1 the
+    result has shape [splits, M, N] (partial products)."""
     lib = load_library()
     A = np.ascontiguousarray(A_bits, np.uint16)
     B = np.ascontiguousarray(B_bits, np.uint16)
     M, K = A.shape
     N = B.shape[0]
-    out = np.zeros((M, N // 2 if mode == 2 else N), np.float32) if C is None else np.ascontiguousarray(C, np.float32)
+    if splits > 1:
+        out = np.zeros((splits, M, N), np.float32)
+    else:
+        out = np.zeros((M, N // 2 if mode == 2 else N), np.float32) if C is None else np.ascontiguousarray(C, np.float32)
     if mode == 1 and C is None:
         raise ValueError("accumulate mode needs C")
     bptr = None
     if bias is not None:
         bias = np.ascontiguousarray(bias, np.float32)
         bptr = bias.ctypes.data
-    _check(lib.sart_debug_gemm(M, N, K, A.ctypes.data, B.ctypes.data, bptr, out.ctypes.data, mode))
+    _check(lib.sart_debug_gemm(M, N, K, A.ctypes.data, B.ctypes.data, bptr, out.ctypes.data, mode, splits, bn))
     return out
 
 

@@ -50,3 +50,16 @@ def test_gemm_swiglu_interleaved():
     u = a @ bits_to_f32(Wu).astype(np.float64).T
     ref = g / (1 + np.exp(-g)) * u
     assert np.max(np.abs(act - ref)) / np.max(np.abs(ref)) < 1e-2     # bf16 output rounding
+
+
+@pytest.mark.parametrize("M,N,K,S,BN", [(512, 1536, 8960, 6, 128), (512, 2048, 1536, 4, 128), (100, 1536, 1536, 6, 128),
+                                        (512, 1536, 1536, 3, 256), (1, 256, 512, 2, 128)])
+def test_gemm_split_k(M, N, K, S, BN):
+    """split-K partials (the RMSNorm/RoPE consumers sum them in split order)"""
+    rng = np.random.default_rng(M + N + K)
+    A, B = rnd(rng, (M, K)), rnd(rng, (N, K), 0.05)
+    from paper_2505_13326_b200.sart import debug_gemm
+    parts = debug_gemm(A, B, mode=0, splits=S, bn=BN)
+    C = parts.astype(np.float64).sum(axis=0)
+    ref = bits_to_f32(A).astype(np.float64) @ bits_to_f32(B).astype(np.float64).T
+    assert np.max(np.abs(C - ref)) / np.max(np.abs(ref)) < 1e-4
