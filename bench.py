@@ -120,10 +120,18 @@ def oracle_sample(steps: int, warmup: int, T: int):
     import numpy as np
     from oracle.engine import Engine as OEngine, EngineConfig, ModelSource
     from oracle.model import Model
-    from synth import SHAPES, gen_requests, gen_weights
+    from synth import SHAPES, gen_requests
     shape = SHAPES[C2["shape"]]
     t0 = time.time()
-    w = gen_weights(shape, "bf16")
+    # timing input only: plain fp32 normals (the values do not change the oracle's cost)
+    rng = np.random.default_rng(0)
+    w = {}
+    from synth import weight_names, weight_shapes
+    shp = weight_shapes(shape)
+    for name in weight_names(shape):
+        w[name] = (rng.standard_normal(shp[name], dtype=np.float32) * 0.02).astype(np.float32)
+        if name.endswith("norm"):
+            w[name] += 1.0
     gen_s = time.time() - t0
     cfg = EngineConfig(block_size=64, num_blocks=4096, T=1, cap=C2["cap"], eos_id=1)
     eng = OEngine(cfg, ModelSource(Model(shape, w), cfg, prm_scores=False))

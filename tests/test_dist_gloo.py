@@ -1,0 +1,112 @@
+"""world_size-2 gloo tests of the request-partitioned multi-GPU layer (paper_2505_13326_b200/dist.py)
+on CPU.  The per-rank engine is the oracle engine (test infrastructure) wrapped with the same
+duck-typed API as the CUDA engine; the union of the ranks' results must equal a
+single-process run (requests are independent), and both dispatch policies must be
+computed identically on every rank."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle.engine import Engine as OEngine, EngineConfig, ScriptedSource
+from synth import SHAPES, gen_requests
+
+KEYS = ["request_id", "answer_vote", "vote_count", "chosen_max_reward", "num_completed", "num_pruned",
+        "num_early_stopped", "branch_len", "branch_state", "branch_score", "finalize_reason"]
+
+
+class OracleRankEngine:
+    def __init__(self):
+        self.e = OEngine(EngineConfig(block_size=16, num_blocks=1 << 16, T=8, cap=48, eos_id=1), ScriptedSource(1))
+
+    def admit(self, r):
+        self.e.admit(r)
+
+    def step(self, n):
+        return self.e.step(n)
+
+    def collect(self):
+        return self.e.collect()
+
+    def counters(self):
+        s = self.e.stats()
+        c = [s["live_rows"], s["queued_branches"], s["queued_requests"], s["free_blocks"], s["committed_blocks"],
+             s["finalized_total"], s["windows"], s["steps"]] + [0] * 8
+        return torch.tensor(c, dtype=torch.int32)
+
+
+def workload():
+    shape = SHAPES["tiny"]
+    reqs = gen_requests(10, shape, 4, 2, 0.5, 2, 48, 8, eos_id=1, p_range=(2, 40), length="uniform",
+                        len_range=(1, 48), root_seed=5)
+    return [reqs[0:3], [], reqs[3:6], reqs[6:7], [], reqs[7:10]]
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, policy, q):
+    from paper_2505_13326_b200 import dist as sdist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    eng = OracleRankEngine()
+    owners = []
+    res = sdist.serve(eng, workload(), policy=policy)
+    allres = sdist.gather_results(res)
+    mine = sorted(r["request_id"] for r in res)
+    q.put((rank, mine, [{k: r[k] for k in KEYS} for r in allres]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("policy", ["round_robin", "least_loaded"])
+def test_two_rank_partition_equals_single_process(policy):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, policy, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(2):
+        rank, mine, allres = q.get(timeout=120)
+        out[rank] = (mine, allres)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # every request ran on exactly one rank
+    ids0, ids1 = out[0][0], out[1][0]
+    assert not set(ids0) & set(ids1) and len(ids0) + len(ids1) == 10
+    assert ids0 and ids1
+    if policy == "round_robin":
+        assert ids0 == [0, 2, 4, 6, 8] and ids1 == [1, 3, 5, 7, 9]
+    # rank 0 gathered everything; identical to one process running all requests
+    single = OracleRankEngine()
+    for batch in workload():
+        for r in batch:
+            single.admit(r)
+    single.step(1000)
+    ref = sorted(single.collect(), key=lambda r: r["request_id"])
+    got = out[0][1]
+    assert [r["request_id"] for r in got] == list(range(10))
+    for g, o in zip(got, ref):
+        for k in KEYS:
+            assert g[k] == o[k], (k, g["request_id"])
+    assert out[1][1] == []
+
+
+def test_least_loaded_is_deterministic():
+    from paper_2505_13326_b200.dist import LeastLoaded
+    c = torch.zeros((4, 16), dtype=torch.int32)
+    c[:, 2] = torch.tensor([3, 1, 1, 0])
+    c[:, 4] = torch.tensor([10, 5, 2, 7])
+    a = LeastLoaded(4).assign(c, 6)
+    b = LeastLoaded(4).assign(c.clone(), 6)
+    assert a == b == [3, 2, 1, 3, 2, 1]
