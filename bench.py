@@ -191,7 +191,7 @@ def main():
     eng = Engine(shape, "bf16", weight_seed=1234 + rank, block_size=cfg["block_size"], num_blocks=0,
                  max_rows=cfg["concurrent"] * cfg["N"], max_requests=256, max_prompt=cfg["p_range"][1] + 1,
                  T=cfg["T"], cap=cfg["cap"], eos_id=1, temperature=1.0, sampler_seed=7, device=local,
-                 stream=stream.cuda_stream, profile=True, attn_mode=args.attn_mode)
+                 stream=stream.cuda_stream, profile=False, attn_mode=args.attn_mode)
     windows_needed = args.warmup + args.steps
     # backlog: enough requests that 64 stay resident for every window (~12 finalize per window)
     n_backlog = cfg["concurrent"] + 24 * windows_needed
@@ -241,17 +241,32 @@ def main():
         t[0] = tmax[0]
     ms_max, tok_all, fin_all = float(t[0]), float(t[1]), float(t[2])
     value = tok_all / (ms_max / 1e3)
-    attn_ms = p1["attn_ms"] - p0["attn_ms"]
-    attn_bytes = p1["attn_bytes"] - p0["attn_bytes"]
     launches = p1["kernel_launches"] - p0["kernel_launches"]
+
+    # ---------------- roofline of the dominant kernel: one more window with per-launch CUDA
+    # events around every attention launch (eager launches on the same stream, same workload)
+    eng.set_profile(True)
+    q0 = eng.profile()
+    sp0 = eng.step(0)
+    eng.step(1)
+    torch.cuda.synchronize()
+    q1 = eng.profile()
+    sp1 = eng.step(0)
+    eng.set_profile(False)
+    attn_ms = q1["attn_ms"] - q0["attn_ms"]
+    attn_bytes = q1["attn_bytes"] - q0["attn_bytes"]
+    n_attn = max(1, q1["attn_launches"] - q0["attn_launches"])
     peaks = load_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     achieved = attn_bytes / (attn_ms / 1e3) / 1e9 if attn_ms > 0 else 0.0
-    roofline = {"bound": "hbm", "kernel": "cascade decode attention", "achieved": achieved, "peak": hbm_peak,
-                "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+    roofline = {"bound": "hbm", "kernel": "k_attn_cascade + k_attn_merge (cascade decode attention)",
+                "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s",
-                "attn_share_of_step": attn_ms / ms if ms > 0 else None,
-                "attn_launch_avg_ms": attn_ms / max(1, p1["attn_launches"] - p0["attn_launches"])}
+                "bytes_per_launch": attn_bytes / n_attn, "launch_avg_ms": attn_ms / n_attn,
+                "launches_measured": n_attn,
+                "measured_over": "1 eager window after the timed region (%d decode steps)" % (sp1["steps"] - sp0["steps"]),
+                "attn_ms_per_step": attn_ms / max(1, sp1["steps"] - sp0["steps"])}
 
     # ---------------- e2e: the public C-ABI path with host buffers, H2D/D2H inside the timed region
     e2e = None
@@ -278,6 +293,7 @@ def main():
             dist.all_reduce(e2e_v, op=dist.ReduceOp.SUM)
             e2e_v[0] = mx[0]
         e2e = {"value": float(e2e_v[1]) / float(e2e_v[0]), "unit": "branch-tokens/s",
+               "windows": args.steps,
                "h2d_bytes_per_step": h2d // max(1, args.steps), "d2h_bytes_per_step": d2h // max(1, args.steps),
                "includes": "admit (host prompts/scripts), prefill, decode windows, collect (D2H records+tokens)"}
     # C2: gather of result records to rank 0 (counts only here)
@@ -302,6 +318,7 @@ def main():
                            "parallelism": f"request-partitioned dp{world}",
                            "l2": "inputs larger than L2 (3.1 GB weights + multi-GB KV per step)"},
                 "requests_per_s": fin_all / (ms_max / 1e3), "decode_steps_timed": dec_steps,
+                "prefill_ms_timed": p1["prefill_ms"] - p0["prefill_ms"],
                 "branch_tokens_timed": tok_all, "gpu_launches": launches, "clocks": clocks,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e}
         print(json.dumps(line), flush=True)

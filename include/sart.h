@@ -265,6 +265,10 @@ typedef struct {
   double prefill_ms;       /* host-observed prefill time                         */
 } sart_profile;
 int sart_get_profile(sart_ctx* ctx, sart_profile* out);
+/* Turn per-launch attention timing on or off.  While on, decode steps are launched eagerly
+ * with CUDA events around each attention launch; while off, each window's decode step is
+ * captured once as a CUDA graph and replayed (the default serving mode). */
+int sart_set_profile(sart_ctx* ctx, int32_t enable);
 int sart_reset_profile(sart_ctx* ctx);
 
 #ifdef __cplusplus

@@ -422,16 +422,19 @@ __global__ void __launch_bounds__(1024) k_attn_plan(Dims D, Rows rows, Reqs reqs
 // running row, each running suffix once, plus q and o (profiling only)
 __global__ void __launch_bounds__(1024) k_attn_account(Dims D, Rows rows, Reqs reqs, int n, double* acc) {
   __shared__ double red[32];
+  __shared__ unsigned char live[1024];     // request slots with a running row (S <= 1024)
+  for (int i = threadIdx.x; i < D.S; i += 1024) live[i] = 0;
+  __syncthreads();
   double b = 0.0;
   const double kvtok = 2.0 * D.kvh * D.hd * 2.0;   // K+V bytes per token per layer (bf16)
   for (int r = threadIdx.x; r < n; r += 1024) {
     if (rows.status[r] != RUNNING_ST) continue;
     b += (rows.ell[r] + 1) * kvtok + 2.0 * D.qh * D.hd * 2.0;
-    bool first = true;
-    for (int r2 = 0; r2 < r; ++r2)
-      if (rows.slot[r2] == rows.slot[r] && rows.status[r2] == RUNNING_ST) { first = false; break; }
-    if (first) b += (reqs.P[rows.slot[r]] - 1) * kvtok;
+    live[rows.slot[r]] = 1;
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < D.S; i += 1024)    // prefix once per request
+    if (live[i]) b += (reqs.P[i] - 1) * kvtok;
   for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = b;
   __syncthreads();

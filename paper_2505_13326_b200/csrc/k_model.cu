@@ -45,41 +45,61 @@ void launch_embed(const int* tok, const T* emb, float* h, int n, int d, cudaStre
 // split order: deterministic), then out = h * rsqrt(mean(h^2) + eps) * g.  Rows with status
 // != RUNNING are skipped when status is given (the final norm keeps the z of finished rows
 // for the PRM, O6).
+template <typename T> __device__ __forceinline__ void store4(T* p, float4 v);
+template <> __device__ __forceinline__ void store4<float>(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+template <> __device__ __forceinline__ void store4<bf16>(bf16* p, float4 v) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+template <typename T> __device__ __forceinline__ float4 load4(const T* p);
+template <> __device__ __forceinline__ float4 load4<float>(const float* p) { return *reinterpret_cast<const float4*>(p); }
+template <> __device__ __forceinline__ float4 load4<bf16>(const bf16* p) {
+  uint2 u = *reinterpret_cast<const uint2*>(p);
+  __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&u.x), b = *reinterpret_cast<__nv_bfloat162*>(&u.y);
+  return make_float4(__low2float(a), __high2float(a), __low2float(b), __high2float(b));
+}
+
+// one 128-thread CTA per row, float4 vectorised (d % 4 == 0, checked at init)
 template <typename T>
-__global__ void k_rmsnorm(float* __restrict__ h, const float* __restrict__ parts, int np, long long pstride,
-                          const T* __restrict__ g, T* __restrict__ out, float* __restrict__ out32,
-                          const int* __restrict__ status, int d, float eps) {
-  int r = blockIdx.x;
+__global__ void __launch_bounds__(128) k_rmsnorm(float* __restrict__ h, const float* __restrict__ parts, int np,
+                                                  long long pstride, const T* __restrict__ g, T* __restrict__ out,
+                                                  float* __restrict__ out32, const int* __restrict__ status, int n,
+                                                  int d, float eps) {
+  const int r = blockIdx.x;
   if (status && status[r] != RUNNING_ST) return;
-  float* x = h + (long long)r * d;
+  float4* x = reinterpret_cast<float4*>(h + (long long)r * d);
+  const int d4 = d >> 2;
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    float v = x[i];
-    for (int sp = 0; sp < np; ++sp) v += parts[sp * pstride + (long long)r * d + i];
+  for (int i = threadIdx.x; i < d4; i += 128) {
+    float4 v = x[i];
+    for (int sp = 0; sp < np; ++sp) {   // split order: deterministic
+      const float4 p = reinterpret_cast<const float4*>(parts + sp * pstride + (long long)r * d)[i];
+      v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
+    }
     if (np) x[i] = v;
-    ss += v * v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
-  __shared__ float red[32];
+  __shared__ float red[4];
+#pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) red[0] = v;
-  }
-  __syncthreads();
-  float inv = rsqrtf(red[0] / d + eps);
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    float y = x[i] * inv * to_f(g[i]);
-    out[(long long)r * d + i] = from_f<T>(y);
-    if (out32) out32[(long long)r * d + i] = y;
+  const float inv = rsqrtf((red[0] + red[1] + red[2] + red[3]) / d + eps);
+  for (int i = threadIdx.x; i < d4; i += 128) {
+    const float4 v = x[i];
+    const float4 gg = load4<T>(g + 4 * i);
+    const float4 y = make_float4(v.x * inv * gg.x, v.y * inv * gg.y, v.z * inv * gg.z, v.w * inv * gg.w);
+    store4<T>(out + (long long)r * d + 4 * i, y);
+    if (out32) reinterpret_cast<float4*>(out32 + (long long)r * d)[i] = y;
   }
 }
 template <typename T>
 void launch_rmsnorm(float* h, const float* parts, int np, const T* g, T* out, float* out32, const int* status, int n,
                     int d, float eps, cudaStream_t s) {
-  if (n > 0) k_rmsnorm<T><<<n, 256, 0, s>>>(h, parts, np, (long long)n * d, g, out, out32, status, d, eps);
+  if (n > 0) k_rmsnorm<T><<<n, 128, 0, s>>>(h, parts, np, (long long)n * d, g, out, out32, status, n, d, eps);
 }
 
 // ------------------------------------------------------------ RoPE + KV append

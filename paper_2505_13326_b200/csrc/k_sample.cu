@@ -17,61 +17,87 @@ __device__ __forceinline__ void better(float& bk, int& bv, float k, int v) {
   if (k > bk || (k == bk && v < bv)) { bk = k; bv = v; }
 }
 
-__global__ void __launch_bounds__(512) k_sample(const float* __restrict__ logits, Dims D, Rows rows, Reqs reqs,
-                                                Ctr* ctr, int* dbg_tok) {
-  const int r = blockIdx.x;
+// Phase 1: one CTA per (row, vocab chunk of SCHUNK entries) -> the chunk's best (key, v).
+// Phase 2: one warp per row reduces the chunks (exact max with the lowest-v tie rule, so the
+// reduction order does not matter) and updates the row: history, EOS / cap, counters.
+constexpr int SCHUNK = 4096;
+
+__global__ void __launch_bounds__(256) k_sample_part(const float* __restrict__ logits, Dims D, Rows rows, Reqs reqs,
+                                                      float* __restrict__ pkey, int* __restrict__ pv, int nchunk) {
+  const int r = blockIdx.x, c = blockIdx.y;
   if (rows.status[r] != RUNNING_ST) return;
   const int slot = rows.slot[r], b = rows.b[r];
   const int s = rows.ell[r] + 1;
   const long long sb = (long long)slot * SART_MAXN + b;
   const int forced_len = reqs.sc_len[sb];   // 0 = no scripted EOS step
+  if (forced_len > 0 && s == forced_len) return;
+  const bool mask_eos = forced_len > 0;
   const float* lg = logits + (long long)r * D.V;
   const uint32_t rid = (uint32_t)reqs.id[slot];
   const uint32_t k0 = (uint32_t)D.seed, k1 = (uint32_t)(D.seed >> 32);
-  const bool mask_eos = forced_len > 0;
+  const bool unit_tau = D.tau == 1.0f;
+  float bk = -INFINITY;
+  int bv = 0x7fffffff;
+  const int g_lo = c * (SCHUNK / 4), g_hi = min((c + 1) * (SCHUNK / 4), (D.V + 3) >> 2);
+  for (int g4 = g_lo + threadIdx.x; g4 < g_hi; g4 += blockDim.x) {
+    const float4 l4 = (D.V % 4 == 0 && 4 * g4 + 3 < D.V) ? *reinterpret_cast<const float4*>(lg + 4 * g4)
+                                         : make_float4(lg[4 * g4], 4 * g4 + 1 < D.V ? lg[4 * g4 + 1] : 0.f,
+                                                       4 * g4 + 2 < D.V ? lg[4 * g4 + 2] : 0.f, 0.f);
+    const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+    u32x4 w{0, 0, 0, 0};
+    if (D.tau > 0.f) w = philox4x32_10(u32x4{(uint32_t)g4, (uint32_t)s, rid, (uint32_t)b}, k0, k1);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int v = 4 * g4 + j;
+      if (v >= D.V || (mask_eos && v == D.eos)) continue;
+      float key;
+      if (D.tau > 0.f) key = (unit_tau ? lv[j] : lv[j] / D.tau) + gumbel_from_word(ws[j]);
+      else key = lv[j];
+      better(bk, bv, key, v);
+    }
+  }
+  __shared__ float sk[8];
+  __shared__ int sv[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ok = __shfl_xor_sync(0xffffffffu, bk, o);
+    int ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    better(bk, bv, ok, ov);
+  }
+  if ((threadIdx.x & 31) == 0) { sk[threadIdx.x >> 5] = bk; sv[threadIdx.x >> 5] = bv; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w2 = 1; w2 < (int)(blockDim.x >> 5); ++w2) better(bk, bv, sk[w2], sv[w2]);
+    pkey[(long long)r * nchunk + c] = bk;
+    pv[(long long)r * nchunk + c] = bv;
+  }
+}
+
+__global__ void __launch_bounds__(32) k_sample_final(Dims D, Rows rows, Reqs reqs, Ctr* ctr, const float* pkey,
+                                                     const int* pv, int nchunk, int* dbg_tok) {
+  const int r = blockIdx.x, lane = threadIdx.x;
+  if (rows.status[r] != RUNNING_ST) return;
+  const int slot = rows.slot[r], b = rows.b[r];
+  const int s = rows.ell[r] + 1;
+  const long long sb = (long long)slot * SART_MAXN + b;
+  const int forced_len = reqs.sc_len[sb];
   int y;
-  __shared__ float sk[32];
-  __shared__ int sv[32];
   if (forced_len > 0 && s == forced_len) {
     y = D.eos;
   } else {
     float bk = -INFINITY;
     int bv = 0x7fffffff;
-    const int ngrp = (D.V + 3) >> 2;
-    for (int g4 = threadIdx.x; g4 < ngrp; g4 += blockDim.x) {
-      u32x4 w{0, 0, 0, 0};
-      if (D.tau > 0.f) w = philox4x32_10(u32x4{(uint32_t)g4, (uint32_t)s, rid, (uint32_t)b}, k0, k1);
-      uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        int v = 4 * g4 + j;
-        if (v >= D.V) break;
-        if (mask_eos && v == D.eos) continue;
-        float key = D.tau > 0.f ? lg[v] / D.tau + gumbel_from_word(ws[j]) : lg[v];
-        better(bk, bv, key, v);
-      }
-    }
+    for (int c = lane; c < nchunk; c += 32) better(bk, bv, pkey[(long long)r * nchunk + c], pv[(long long)r * nchunk + c]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       float ok = __shfl_xor_sync(0xffffffffu, bk, o);
       int ov = __shfl_xor_sync(0xffffffffu, bv, o);
       better(bk, bv, ok, ov);
     }
-    if ((threadIdx.x & 31) == 0) { sk[threadIdx.x >> 5] = bk; sv[threadIdx.x >> 5] = bv; }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      bk = threadIdx.x < (blockDim.x >> 5) ? sk[threadIdx.x] : -INFINITY;
-      bv = threadIdx.x < (blockDim.x >> 5) ? sv[threadIdx.x] : 0x7fffffff;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        float ok = __shfl_xor_sync(0xffffffffu, bk, o);
-        int ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        better(bk, bv, ok, ov);
-      }
-    }
     y = bv;
   }
-  if (threadIdx.x != 0) return;
+  if (lane != 0) return;
   if (dbg_tok) dbg_tok[r] = y;
   if (reqs.has_forced[slot]) y = reqs.forced[sb * D.cap + (s - 1)];   // teacher forcing
   reqs.hist[sb * D.cap + (s - 1)] = y;
@@ -90,9 +116,13 @@ __global__ void __launch_bounds__(512) k_sample(const float* __restrict__ logits
 }
 
 void launch_sample(const float* logits, Dims D, Rows rows, Reqs reqs, Ctr* ctr, int n, int* dbg_tok,
-                   cudaStream_t s) {
-  if (n > 0) k_sample<<<n, 512, 0, s>>>(logits, D, rows, reqs, ctr, dbg_tok);
+                   float* pkey, int* pv, cudaStream_t s) {
+  if (n <= 0) return;
+  const int nchunk = (D.V + SCHUNK - 1) / SCHUNK;
+  k_sample_part<<<dim3(n, nchunk), 256, 0, s>>>(logits, D, rows, reqs, pkey, pv, nchunk);
+  k_sample_final<<<n, 32, 0, s>>>(D, rows, reqs, ctr, pkey, pv, nchunk, dbg_tok);
 }
+int sample_chunks(int V) { return (V + SCHUNK - 1) / SCHUNK; }
 
 __global__ void k_step_begin(Ctr* ctr) {
   if (ctr->live > 0) { ctr->wstep += 1; ctr->steps += 1; }

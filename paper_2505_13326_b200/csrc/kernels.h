@@ -61,8 +61,9 @@ void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg,
                          Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s);
 
 // ---- sampler (k_sample.cu)
-void launch_sample(const float* logits, Dims D, Rows rows, Reqs reqs, Ctr* ctr, int n, int* dbg_tok,
-                   cudaStream_t s);
+void launch_sample(const float* logits, Dims D, Rows rows, Reqs reqs, Ctr* ctr, int n, int* dbg_tok, float* pkey,
+                   int* pv, cudaStream_t s);
+int sample_chunks(int V);
 void launch_step_begin(Ctr* ctr, cudaStream_t s);
 
 // ---- control (k_ctl.cu)

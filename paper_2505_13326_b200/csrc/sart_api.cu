@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -98,6 +99,8 @@ struct sart_ctx {
   int ev_cap = 0;
   AttnPlan plan{};
   float *part_o = nullptr, *part_lse = nullptr;
+  float* skey = nullptr;   // sampler per-chunk partial argmax
+  int* sv = nullptr;
 
   // host state
   std::deque<HostReq> request_queue;
@@ -112,7 +115,10 @@ struct sart_ctx {
   long long branch_tokens = 0;
   int last_n = 0;
   Ctr* h_ctr = nullptr;  // pinned
-  int* h_live = nullptr; // pinned
+  int* h_live = nullptr; // pinned [2]
+  cudaEvent_t poll_ev[2] = {nullptr, nullptr};
+  cudaGraphExec_t step_exec = nullptr;
+  bool use_graphs = true;
   std::vector<int64_t> last_slot_id;
 
   // profiling
@@ -320,7 +326,7 @@ void decode_step(sart_ctx* ctx, int n) {
   launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_final(D)), (T*)ctx->zT, ctx->z32, ctx->rows.status, n,
                     D.d, D.eps, s);
   gemm<T>(ctx, (T*)ctx->zT, ctx->W_<T>(t_lm(D)), nullptr, ctx->logits, n, D.V, D.d, GEMM_STORE);
-  launch_sample(ctx->logits, D, ctx->rows, ctx->reqs, ctx->ctr, n, ctx->dbg_tok, s);
+  launch_sample(ctx->logits, D, ctx->rows, ctx->reqs, ctx->ctr, n, ctx->dbg_tok, ctx->skey, ctx->sv, s);
   ctx->launches += 2;
 }
 
@@ -576,14 +582,55 @@ int run_window(sart_ctx* ctx) {
     launch_attn_plan(D, ctx->rows, ctx->reqs, ctx->plan, n, ctx->cfg.attn_mode == SART_ATTN_FLAT, ctx->st);
     ctx->launches++;
   }
-  for (int k = 1; k <= D.T; ++k) {
-    if (k > 1 && (k % 8) == 1) {
-      // live rows read back asynchronously; a window ends early when none is live (R31)
-      CK(cudaMemcpyAsync(ctx->h_live, &ctx->ctr->live, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
-      CK(cudaStreamSynchronize(ctx->st));
-      if (*ctx->h_live == 0) break;
-    }
+  // Decode steps.  Without profiling, the step (~260 kernels) is captured once per window as
+  // a CUDA graph and replayed T times (row count and pointers are fixed within a window; all
+  // per-step state is read from device memory).  A window ends early when no row is live
+  // (R31): the live count is copied back asynchronously every POLL steps and the host stops
+  // enqueuing once a completed copy shows 0; steps enqueued after that are no-ops.
+  const bool graph = !ctx->cfg.profile && ctx->use_graphs;
+  long long per_step = 0;
+  if (graph) {
+    const long long before = ctx->launches;
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
     decode_step<T>(ctx, n);
+    CK(cudaStreamEndCapture(ctx->st, &g));
+    per_step = ctx->launches - before;
+    ctx->launches = before;
+    bool updated = false;
+    if (ctx->step_exec) {
+      cudaGraphExecUpdateResultInfo info;
+      updated = cudaGraphExecUpdate(ctx->step_exec, g, &info) == cudaSuccess;
+      if (!updated) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(ctx->step_exec);
+        ctx->step_exec = nullptr;
+      }
+    }
+    if (!updated) CK(cudaGraphInstantiate(&ctx->step_exec, g, 0));
+    CK(cudaGraphDestroy(g));
+  }
+  constexpr int POLL = 16;
+  int polls = 0;
+  for (int k = 1; k <= D.T; ++k) {
+    if (k > 1 && (k % POLL) == 1) {
+      if (polls >= 2) {   // bound the run-ahead: wait for the poll two periods back
+        CK(cudaEventSynchronize(ctx->poll_ev[polls & 1]));
+        if (ctx->h_live[polls & 1] == 0) break;
+      }
+      CK(cudaMemcpyAsync(&ctx->h_live[polls & 1], &ctx->ctr->live, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+      CK(cudaEventRecord(ctx->poll_ev[polls & 1], ctx->st));
+      ++polls;
+      if (polls >= 2 && cudaEventQuery(ctx->poll_ev[(polls - 2) & 1]) == cudaSuccess &&
+          ctx->h_live[(polls - 2) & 1] == 0)
+        break;
+    }
+    if (graph) {
+      CK(cudaGraphLaunch(ctx->step_exec, ctx->st));
+      ctx->launches += per_step;
+    } else {
+      decode_step<T>(ctx, n);
+    }
   }
   CK(cudaGetLastError());
   if (ctx->gemm_failed) return set_err(SART_EINVAL, "GEMM shape unsupported by the tcgen05 kernel");
@@ -630,6 +677,9 @@ int sart_destroy(sart_ctx* ctx) {
   cudaSetDevice(ctx->cfg.device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (auto e : ctx->poll_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->step_exec) cudaGraphExecDestroy(ctx->step_exec);
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->wblob) cudaFree(ctx->wblob);
   if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
@@ -787,6 +837,8 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   IC(dalloc(ctx, &ctx->act, W * D.F * es));
   IC(dalloc(ctx, &ctx->zT, (size_t)D.R * D.d * es));
   IC(dalloc(ctx, &ctx->dbg_tok, (size_t)D.R * 4));
+  IC(dalloc(ctx, &ctx->skey, (size_t)D.R * sample_chunks(D.V) * 4));
+  IC(dalloc(ctx, &ctx->sv, (size_t)D.R * sample_chunks(D.V) * 4));
   IC(dalloc(ctx, &ctx->dbg_slot, (size_t)D.R * 4));
   IC(dalloc(ctx, &ctx->dbg_b, (size_t)D.R * 4));
   IC(dalloc(ctx, &ctx->d_prompt, (size_t)cfg.max_prompt * 4));
@@ -813,7 +865,10 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     }
   }
   IC(cudaMallocHost(&ctx->h_ctr, sizeof(Ctr) + sizeof(int) * D.S));
-  IC(cudaMallocHost(&ctx->h_live, sizeof(int)));
+  IC(cudaMallocHost(&ctx->h_live, 2 * sizeof(int)));
+  IC(cudaEventCreateWithFlags(&ctx->poll_ev[0], cudaEventDisableTiming));
+  IC(cudaEventCreateWithFlags(&ctx->poll_ev[1], cudaEventDisableTiming));
+  if (getenv("SART_NO_GRAPHS")) ctx->use_graphs = false;
   // ---- KV pool
   const size_t blk_bytes = (size_t)D.L * 2 * D.kvh * D.bs * D.hd * es;
   long long NB = cfg.num_blocks;
@@ -1114,6 +1169,17 @@ int sart_get_profile(sart_ctx* ctx, sart_profile* o) {
   o->prefill_ms = ctx->prefill_ms;
   return SART_OK;
 }
+int sart_set_profile(sart_ctx* ctx, int32_t enable) {
+  if (!ctx) return set_err(SART_EINVAL, "null argument");
+  if (enable && ctx->ev_pool.empty()) {
+    ctx->ev_pool.resize(2 * ctx->D.L * ctx->D.T + 2);
+    for (auto& ev : ctx->ev_pool)
+      if (cudaEventCreate(&ev) != cudaSuccess) return set_err(SART_ECUDA, "event create");
+  }
+  ctx->cfg.profile = enable ? 1 : 0;
+  return SART_OK;
+}
+
 int sart_reset_profile(sart_ctx* ctx) {
   if (!ctx) return set_err(SART_EINVAL, "null argument");
   ctx->attn_bytes_base += ctx->attn_bytes;

@@ -120,10 +120,11 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.sart_debug_fetch.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t, P32]
     lib.sart_get_profile.argtypes = [C.c_void_p, C.POINTER(SartProfile)]
     lib.sart_reset_profile.argtypes = [C.c_void_p]
+    lib.sart_set_profile.argtypes = [C.c_void_p, C.c_int32]
     lib.sart_debug_gemm.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_int32, C.c_int32, C.c_int32]
     for f in ("sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
-              "sart_get_state", "sart_debug_fetch", "sart_get_profile", "sart_reset_profile", "sart_debug_gemm"):
+              "sart_get_state", "sart_debug_fetch", "sart_get_profile", "sart_reset_profile", "sart_debug_gemm", "sart_set_profile"):
         getattr(lib, f).restype = C.c_int
     _lib = lib
     return lib
@@ -131,7 +132,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 
 EXPORTED = ["sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
             "sart_strerror", "sart_last_error", "sart_get_state", "sart_debug_fetch", "sart_get_profile",
-            "sart_reset_profile", "sart_debug_gemm"]
+            "sart_reset_profile", "sart_debug_gemm", "sart_set_profile"]
 
 
 def debug_gemm(A_bits: np.ndarray, B_bits: np.ndarray, bias=None, C=None, mode: int = 0, splits: int = 1,
@@ -339,3 +340,6 @@ class Engine:
 
     def reset_profile(self) -> None:
         _check(self.lib.sart_reset_profile(self.ctx))
+
+    def set_profile(self, enable: bool) -> None:
+        _check(self.lib.sart_set_profile(self.ctx, int(enable)))
