@@ -7,8 +7,9 @@
 // request and kv head: a "prefix task" multiplies a chunk of the shared prefix KV by up to
 // 16 query rows (branches x g heads) of the request, a "suffix task" covers one branch's
 // private KV.  Every task covers <= CH tokens and writes a normalised partial output and its
-// log-sum-exp; a merge kernel combines the partials of each (row, head) in a fixed order, so
-// the result does not depend on scheduling (deterministic, PP4).
+// log-sum-exp; a merge kernel combines the partials of each (row, kv head) in a fixed slot
+// order, so the result does not depend on scheduling (deterministic, PP4).  (Merging inside
+// the streaming kernel was measured slower: per-item fences and atomics stall the streams.)
 //
 // Kernel structure ("warp-autonomous" persistent kernel, one CTA per SM):
 //   * every warp takes items (task, kv head) from a work counter (dynamic load balance; an
@@ -21,12 +22,13 @@
 //   * no CTA-wide barriers and no cross-warp merges: warps never wait on each other.
 // Tensor cores are used because QK^T / PV are dense contractions, but the kernel is
 // HBM-bound (about g flop per byte): the design goal is bytes in flight per SM.
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace {
-constexpr int NW = 6;          // warps per CTA (all consumers)
-constexpr int NS = 2;          // stages per warp ring
-constexpr int SW = 32;         // tokens per stage
+// launch configurations <warps per CTA, stages per warp ring, tokens per stage>; the
+// default is chosen by measurement, SART_ATTN_CFG=<index> overrides it.
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
@@ -125,21 +127,32 @@ __device__ __forceinline__ bool q_of(const AttnPlan& pl, const Dims& D, const It
   return true;
 }
 
-template <int HD>
+// number of items that cover (row r, any kv head) this step
+__device__ __forceinline__ int items_for_row(const AttnPlan& pl, const Dims& D, const Rows& rows, const Reqs& reqs,
+                                             int r, int& npc, int& nsc) {
+  npc = (reqs.P[rows.slot[r]] - 1 + pl.CH - 1) / pl.CH;
+  nsc = (rows.ell[r] + 1 + pl.CH - 1) / pl.CH;
+  const int j = pl.row_pos[r];
+  const int tiles = (j * D.g + D.g - 1) / 16 - (j * D.g) / 16 + 1;   // prefix m-tiles holding this row
+  return nsc + npc * tiles;
+}
+
+template <int HD, int NS, int SW>
 struct WarpSmem {
   bf16 k[NS][SW * HD];
   bf16 v[NS][SW * HD];
   uint64_t full[NS];
-  uint64_t pad[8 - NS];
+  uint64_t pad[(NS & 1) ? 1 : 2];
 };
 
-template <int HD>
+template <int HD, int NW, int NS, int SW>
 __global__ void __launch_bounds__(NW * 32, 1)
     k_attn_cascade(const bf16* __restrict__ q, const bf16* __restrict__ pool, float* __restrict__ part_o,
-                   float* __restrict__ part_lse, Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl) {
+                   float* __restrict__ part_lse, bf16* __restrict__ out, float* __restrict__ dbg, Dims D, int layer,
+                   Rows rows, Reqs reqs, AttnPlan pl) {
   extern __shared__ __align__(128) uint8_t sraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpSmem<HD>& sm = reinterpret_cast<WarpSmem<HD>*>(sraw)[warp];
+  WarpSmem<HD, NS, SW>& sm = reinterpret_cast<WarpSmem<HD, NS, SW>*>(sraw)[warp];
   const int n_items = *pl.n_units * D.kvh;
   int* work = pl.work + layer;
   const float sl2 = 1.4426950408889634f * rsqrtf((float)HD);   // log2(e) / sqrt(hd)
@@ -162,6 +175,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
   int iss_idx = -1, iss_s0 = 0;    // ring index of the item being issued, next stage start
   uint32_t issued = 0, consumed = 0;
   bool exhausted = false;
+  // the next work index is grabbed one item ahead, so the atomic's latency is hidden
+  int next_grab = 0;
+  if (lane == 0) next_grab = atomicAdd(work, 1);
 
   auto refill = [&]() {
     while (issued - consumed < (uint32_t)NS) {
@@ -169,10 +185,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if (exhausted || r_cnt == NS + 1) return;
         Item nx{};
         for (;;) {
-          int v = 0;
-          if (lane == 0) v = atomicAdd(work, 1);
-          const int i = __shfl_sync(0xffffffffu, v, 0);
+          const int i = __shfl_sync(0xffffffffu, next_grab, 0);
           if (i >= n_items) { exhausted = true; return; }
+          if (lane == 0) next_grab = atomicAdd(work, 1);
           nx = decode_item(pl, D, rows, reqs, i);
           if (nx.valid) break;
         }
@@ -333,42 +348,62 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (r_cnt == 0) iss_idx = -1;
     refill();
   }
+  // the last CTA to finish resets this layer's counters for the next step
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(pl.done + layer, 1) == (int)gridDim.x - 1) {
+      pl.work[layer] = 0;
+      pl.done[layer] = 0;
+    }
+  }
 }
 
-// merge the partials of each (row, head) in fixed slot order; o (bf16) and optional fp32 debug.
-// Block 0 also resets this layer's work counter for the next step.
+// merge kernel: one warp per (row, q head); each lane owns HD/32 contiguous columns (one
+// vector load per slot), slots in fixed order (prefix chunks, then suffix chunks)
 template <int HD>
-__global__ void k_attn_merge(const float* __restrict__ part_o, const float* __restrict__ part_lse,
-                             bf16* __restrict__ out, float* __restrict__ dbg, Dims D, int layer, Rows rows,
-                             Reqs reqs, AttnPlan pl, int n) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) pl.work[layer] = 0;
+__global__ void __launch_bounds__(256) k_attn_merge(const float* __restrict__ part_o,
+                                                    const float* __restrict__ part_lse, bf16* __restrict__ out,
+                                                    float* __restrict__ dbg, Dims D, Rows rows, Reqs reqs,
+                                                    AttnPlan pl, int n) {
+  constexpr int C = HD / 32;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= n * D.qh) return;
   const int r = wid / D.qh, head = wid % D.qh;
   if (rows.status[r] != RUNNING_ST) return;
-  const int npc = (reqs.P[rows.slot[r]] - 1 + pl.CH - 1) / pl.CH;
-  const int nsc = (rows.ell[r] + 1 + pl.CH - 1) / pl.CH;
+  int npc, nsc;
+  items_for_row(pl, D, rows, reqs, r, npc, nsc);
   const long long base = ((long long)r * D.qh + head) * pl.nslot;
   float M = -INFINITY;
-  for (int c = 0; c < npc; ++c) M = fmaxf(M, part_lse[base + c]);
-  for (int c = 0; c < nsc; ++c) M = fmaxf(M, part_lse[base + pl.npc_max + c]);
-  float acc[HD / 32] = {};
+  for (int k = 0; k < npc + nsc; ++k) M = fmaxf(M, part_lse[base + (k < npc ? k : pl.npc_max + k - npc)]);
+  float acc[C] = {};
   float L = 0.f;
-  auto add = [&](int slot) {
-    const float w = exp2f(part_lse[base + slot] - M);
+#pragma unroll 4
+  for (int k = 0; k < npc + nsc; ++k) {
+    const long long pi = base + (k < npc ? k : pl.npc_max + k - npc);
+    const float w = exp2f(part_lse[pi] - M);
     L += w;
-#pragma unroll
-    for (int i = 0; i < HD / 32; ++i) acc[i] += w * part_o[(base + slot) * HD + lane + 32 * i];
-  };
-  for (int c = 0; c < npc; ++c) add(c);
-  for (int c = 0; c < nsc; ++c) add(pl.npc_max + c);
-#pragma unroll
-  for (int i = 0; i < HD / 32; ++i) {
-    const float v = acc[i] / L;
-    const long long oi = ((long long)r * D.qh + head) * HD + lane + 32 * i;
-    out[oi] = __float2bfloat16_rn(v);
-    if (dbg) dbg[oi] = v;
+    if constexpr (C == 4) {
+      const float4 v = *reinterpret_cast<const float4*>(part_o + pi * HD + lane * 4);
+      acc[0] += w * v.x; acc[1] += w * v.y; acc[2] += w * v.z; acc[3] += w * v.w;
+    } else {
+      const float2 v = *reinterpret_cast<const float2*>(part_o + pi * HD + lane * 2);
+      acc[0] += w * v.x; acc[1] += w * v.y;
+    }
   }
+  const long long oi = ((long long)r * D.qh + head) * HD + lane * C;
+  const float inv = 1.0f / L;
+  if constexpr (C == 4) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(acc[0] * inv, acc[1] * inv), b = __floats2bfloat162_rn(acc[2] * inv, acc[3] * inv);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(out + oi) = u;
+  } else {
+    *reinterpret_cast<__nv_bfloat162*>(out + oi) = __floats2bfloat162_rn(acc[0] * inv, acc[1] * inv);
+  }
+  if (dbg)
+    for (int c = 0; c < C; ++c) dbg[oi + c] = acc[c] * inv;
 }
 
 // ------------------------------------------------------------------ per-window plan
@@ -406,7 +441,11 @@ __global__ void __launch_bounds__(1024) k_attn_plan(Dims D, Rows rows, Reqs reqs
       }
       int k = 0;
       for (int r2 = r; r2 < n; ++r2)
-        if (rows.slot[r2] == slot) { pl.grp_rows[(ng + k / qr) * pl.qr_max + k % qr] = r2; ++k; }
+        if (rows.slot[r2] == slot) {
+          pl.grp_rows[(ng + k / qr) * pl.qr_max + k % qr] = r2;
+          pl.row_pos[r2] = k % qr;
+          ++k;
+        }
       ng += ngr;
     }
     for (int r = 0; r < n; ++r) {
@@ -455,18 +494,36 @@ void launch_attn_account(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, doubl
 }
 
 static int g_sms = 0;
+template <int HD, int NW, int NS, int SW>
+static void launch_cfg(const bf16* q, const bf16* pool, float* part_o, float* part_lse, bf16* out, float* dbg, Dims D,
+                       int layer, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s) {
+  const size_t sm = sizeof(WarpSmem<HD, NS, SW>) * NW;
+  static bool a = false;
+  if (!a) {
+    cudaFuncSetAttribute(k_attn_cascade<HD, NW, NS, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    a = true;
+  }
+  k_attn_cascade<HD, NW, NS, SW><<<g_sms, NW * 32, sm, s>>>(q, pool, part_o, part_lse, out, dbg, D, layer, rows,
+                                                             reqs, pl);
+}
+static int attn_cfg() {
+  static int c = -1;
+  if (c < 0) {
+    const char* e = getenv("SART_ATTN_CFG");
+    c = e ? atoi(e) : 0;
+  }
+  return c;
+}
 template <int HD>
 static void launch_hd(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse, Dims D,
                       int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s) {
-  const size_t sm = sizeof(WarpSmem<HD>) * NW;
-  static bool a = false;
-  if (!a) {
-    cudaFuncSetAttribute(k_attn_cascade<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    a = true;
+  switch (attn_cfg()) {
+    case 0: launch_cfg<HD, 6, 2, 32>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
+    case 2: launch_cfg<HD, 6, 4, 16>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
+    case 3: launch_cfg<HD, 7, 3, 16>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
+    default: launch_cfg<HD, 8, 3, 16>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
   }
-  k_attn_cascade<HD><<<g_sms, NW * 32, sm, s>>>(q, pool, part_o, part_lse, D, layer, rows, reqs, pl);
-  k_attn_merge<HD><<<(n * D.qh * 32 + 255) / 256, 256, 0, s>>>(part_o, part_lse, out, dbg, D, layer, rows, reqs, pl,
-                                                               n);
+  k_attn_merge<HD><<<(n * D.qh * 32 + 255) / 256, 256, 0, s>>>(part_o, part_lse, out, dbg, D, rows, reqs, pl, n);
 }
 void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse,
                          Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s) {

@@ -53,6 +53,8 @@ struct AttnPlan {
   int* grp_slot;    // [R]
   int* grp_n;       // [R]
   int* grp_rows;    // [R][qr_max]
+  int* row_pos;     // [R] position of the row inside its prefix group
+  int* done;        // [L] finished CTAs per layer launch
   int qr_max, CH, npc_max, nslot;
 };
 void launch_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat, cudaStream_t s);

@@ -856,6 +856,9 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     IC(dalloc(ctx, &pl.units, sizeof(int4) * max_units));
     IC(dalloc(ctx, &pl.n_units, sizeof(int)));
     IC(dalloc(ctx, &pl.work, sizeof(int) * D.L));
+    IC(dalloc(ctx, &pl.done, sizeof(int) * D.L));
+    IC(dalloc(ctx, &pl.row_pos, sizeof(int) * D.R));
+
     IC(dalloc(ctx, &pl.grp_slot, sizeof(int) * D.R));
     IC(dalloc(ctx, &pl.grp_n, sizeof(int) * D.R));
     IC(dalloc(ctx, &pl.grp_rows, sizeof(int) * (size_t)D.R * pl.qr_max));
