@@ -74,40 +74,26 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 
 // A decoded item: task (prefix/suffix chunk, m-tile) x kv head; token range for this step.
 struct Item {
-  int valid, task, h, t0, t1, nq, slot_idx;
+  int valid, task, h, t0, t1, nq, slot_idx, type, y, mt;
   const int* tab;
 };
 
 __device__ __forceinline__ Item decode_item(const AttnPlan& pl, const Dims& D, const Rows& rows, const Reqs& reqs,
                                             int item) {
-  Item it{};
-  it.task = item / D.kvh;
+  Item it;
+  it.task = item / D.kvh;            // index into the per-step packed list
   it.h = item % D.kvh;
-  const int4 u = pl.units[it.task];
-  const int c = u.z;
-  if (u.x == 0) {                                // suffix task: (row, chunk)
-    const int r = u.y;
-    if (rows.status[r] != RUNNING_ST) return it;
-    it.t0 = c * pl.CH;
-    it.t1 = min(it.t0 + pl.CH, rows.ell[r] + 1);
-    it.nq = D.g;
-    it.tab = rows.table + (long long)r * D.MBR;
-    it.slot_idx = pl.npc_max + c;
-  } else {                                       // prefix task: (group, chunk, m-tile)
-    const int gi = u.y, mt = u.w;
-    const int n = pl.grp_n[gi];
-    const int q0 = mt * 16, q1 = min(n * D.g, q0 + 16);
-    bool any = false;
-    for (int j = q0; j < q1; ++j) any |= rows.status[pl.grp_rows[gi * pl.qr_max + j / D.g]] == RUNNING_ST;
-    if (!any) return it;
-    const int slot = pl.grp_slot[gi];
-    it.t0 = c * pl.CH;
-    it.t1 = min(it.t0 + pl.CH, reqs.P[slot] - 1);
-    it.nq = q1 - q0;
-    it.tab = reqs.prefix + (long long)slot * D.MPB;
-    it.slot_idx = c;
-  }
-  it.valid = it.t0 < it.t1;
+  const int4 a = __ldcg(pl.items + 2 * it.task);
+  it.t0 = a.x;
+  it.t1 = a.y;
+  it.slot_idx = a.w;
+  const int4 b = __ldcg(pl.items + 2 * it.task + 1);
+  it.nq = b.w;
+  it.tab = (b.x == 0 ? rows.table : reqs.prefix) + a.z;
+  it.type = b.x;
+  it.y = b.y;
+  it.mt = b.z;
+  it.valid = 1;
   return it;
 }
 
@@ -115,13 +101,12 @@ __device__ __forceinline__ Item decode_item(const AttnPlan& pl, const Dims& D, c
 __device__ __forceinline__ bool q_of(const AttnPlan& pl, const Dims& D, const Item& it, int i, int& row,
                                      int& head) {
   if (i >= it.nq) return false;
-  const int4 u = pl.units[it.task];
-  if (u.x == 0) {
-    row = u.y;
+  if (it.type == 0) {
+    row = it.y;
     head = it.h * D.g + i;
   } else {
-    const int j = u.w * 16 + i;
-    row = pl.grp_rows[u.y * pl.qr_max + j / D.g];
+    const int j = it.mt * 16 + i;
+    row = pl.grp_rows[it.y * pl.qr_max + j / D.g];
     head = it.h * D.g + j % D.g;
   }
   return true;
@@ -153,7 +138,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   extern __shared__ __align__(128) uint8_t sraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpSmem<HD, NS, SW>& sm = reinterpret_cast<WarpSmem<HD, NS, SW>*>(sraw)[warp];
-  const int n_items = *pl.n_units * D.kvh;
+  const int n_items = *pl.n_items * D.kvh;
   int* work = pl.work + layer;
   const float sl2 = 1.4426950408889634f * rsqrtf((float)HD);   // log2(e) / sqrt(hd)
 
@@ -189,7 +174,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
           if (i >= n_items) { exhausted = true; return; }
           if (lane == 0) next_grab = atomicAdd(work, 1);
           nx = decode_item(pl, D, rows, reqs, i);
-          if (nx.valid) break;
+          break;
         }
         iss_idx = (r_head + r_cnt) % (NS + 1);
         ring[iss_idx] = nx;
@@ -406,6 +391,66 @@ __global__ void __launch_bounds__(256) k_attn_merge(const float* __restrict__ pa
     for (int c = 0; c < C; ++c) dbg[oi + c] = acc[c] * inv;
 }
 
+// ------------------------------------------------------------------ per-step item list
+// Valid tasks of this step (rows finished mid-window are skipped) with their token ranges,
+// ordered by size, largest first (counting sort on 16-token buckets), so that the dynamic
+// work queue ends with small items.  One launch per step serves all layers.
+__global__ void __launch_bounds__(1024) k_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl) {
+  constexpr int NB = 64;                       // size buckets
+  __shared__ int cnt[NB], base[NB];
+  const int tid = threadIdx.x;
+  const int nu = *pl.n_units;
+  const int bw = (pl.CH + NB - 1) / NB;        // tokens per bucket
+  if (tid < NB) cnt[tid] = 0;
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int t = tid; t < nu; t += 1024) {
+      const int4 u = pl.units[t];
+      int t0 = 0, t1 = 0, nq = 0, tabbase = 0, slot_idx = 0;
+      bool ok;
+      if (u.x == 0) {
+        const int r = u.y;
+        ok = rows.status[r] == RUNNING_ST;
+        t0 = u.z * pl.CH;
+        t1 = min(t0 + pl.CH, rows.ell[r] + 1);
+        nq = D.g;
+        tabbase = r * D.MBR;
+        slot_idx = pl.npc_max + u.z;
+      } else {
+        const int gi = u.y;
+        const int n = pl.grp_n[gi];
+        const int q0 = u.w * 16, q1 = min(n * D.g, q0 + 16);
+        ok = false;
+        for (int j = q0 / D.g; j <= (q1 - 1) / D.g; ++j)
+          ok |= rows.status[pl.grp_rows[gi * pl.qr_max + j]] == RUNNING_ST;
+        const int slot = pl.grp_slot[gi];
+        t0 = u.z * pl.CH;
+        t1 = min(t0 + pl.CH, reqs.P[slot] - 1);
+        nq = q1 - q0;
+        tabbase = slot * D.MPB;
+        slot_idx = u.z;
+      }
+      ok = ok && t0 < t1;
+      if (!ok) continue;
+      const int bkt = NB - 1 - min(NB - 1, (t1 - t0 - 1) / bw);   // larger first
+      if (pass == 0) {
+        atomicAdd(&cnt[bkt], 1);
+      } else {
+        const int pos = atomicAdd(&base[bkt], 1);
+        pl.items[2 * pos] = make_int4(t0, t1, tabbase, slot_idx);
+        pl.items[2 * pos + 1] = make_int4(u.x, u.y, u.w, nq);
+      }
+    }
+    __syncthreads();
+    if (pass == 0 && tid == 0) {
+      int acc = 0;
+      for (int b = 0; b < NB; ++b) { base[b] = acc; acc += cnt[b]; }
+      *pl.n_items = acc;
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------ per-window plan
 // Tasks: prefix tasks first (type 1: group, chunk, m-tile), then suffix tasks (type 0: row,
 // chunk).  Groups: the window's rows of one request in batch order, qr rows per group
@@ -487,6 +532,9 @@ __global__ void __launch_bounds__(1024) k_attn_account(Dims D, Rows rows, Reqs r
 
 void launch_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat, cudaStream_t s) {
   k_attn_plan<<<1, 1024, 0, s>>>(D, rows, reqs, pl, n, flat);
+}
+void launch_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s) {
+  k_attn_items<<<1, 1024, 0, s>>>(D, rows, reqs, pl);
 }
 void launch_attn_account(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, double* acc, cudaStream_t s) {
   (void)pl;

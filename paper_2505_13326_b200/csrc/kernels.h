@@ -55,9 +55,12 @@ struct AttnPlan {
   int* grp_rows;    // [R][qr_max]
   int* row_pos;     // [R] position of the row inside its prefix group
   int* done;        // [L] finished CTAs per layer launch
+  int4* items;      // [2 * max tasks] per-step packed items {t0, t1, table base, slot} {type, row|group, mtile, nq}
+  int* n_items;     // valid items this step
   int qr_max, CH, npc_max, nslot;
 };
 void launch_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat, cudaStream_t s);
+void launch_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s);
 void launch_attn_account(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, double* acc, cudaStream_t s);
 void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse,
                          Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s);

@@ -307,6 +307,10 @@ void decode_step(sart_ctx* ctx, int n) {
     launch_attn_account(D, ctx->rows, ctx->reqs, ctx->plan, n, &ctx->ctr->attn_bytes, s);
     ctx->launches++;
   }
+  if constexpr (std::is_same<T, bf16>::value) {   // this step's attention items (all layers)
+    launch_attn_items(D, ctx->rows, ctx->reqs, ctx->plan, s);
+    ctx->launches++;
+  }
   int np_res = 0;   // pending residual partials (previous layer's down projection)
   for (int l = 0; l < D.L; ++l) {
     launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, n, D.d,
@@ -857,6 +861,8 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     IC(dalloc(ctx, &pl.n_units, sizeof(int)));
     IC(dalloc(ctx, &pl.work, sizeof(int) * D.L));
     IC(dalloc(ctx, &pl.done, sizeof(int) * D.L));
+    IC(dalloc(ctx, &pl.items, sizeof(int4) * 2 * max_units));
+    IC(dalloc(ctx, &pl.n_items, sizeof(int)));
     IC(dalloc(ctx, &pl.row_pos, sizeof(int) * D.R));
 
     IC(dalloc(ctx, &pl.grp_slot, sizeof(int) * D.R));
