@@ -65,6 +65,18 @@ def attention(q: np.ndarray, K: np.ndarray, V: np.ndarray) -> np.ndarray:
     return p @ V
 
 
+def causal_attention(Q: np.ndarray, K: np.ndarray, V: np.ndarray) -> np.ndarray:
+    """Row t attends to keys 0..t: the same softmax as attention(), written as a masked
+    matrix (o_t = sum_{j<=t} softmax_j(q_t . k_j / sqrt(hd)) v_j)."""
+    n, hd = Q.shape
+    E = (Q @ K.T) / np.sqrt(hd)
+    E = np.where(np.tril(np.ones((n, n), dtype=bool)), E, -np.inf)
+    E = E - E.max(axis=1, keepdims=True)
+    Pm = np.exp(E)
+    Pm = Pm / Pm.sum(axis=1, keepdims=True)
+    return Pm @ V
+
+
 def silu(x: np.ndarray) -> np.ndarray:
     return x / (1.0 + np.exp(-x))
 
@@ -123,9 +135,8 @@ class Model:
         for l in range(s.n_layers):
             q, k, v = self._qkv(l, h, pos)
             o = np.zeros((n, s.n_heads, s.head_dim))
-            for t in range(n):
-                for i in range(s.n_heads):
-                    o[t, i] = attention(q[t, i], k[: t + 1, i // g], v[: t + 1, i // g])
+            for i in range(s.n_heads):
+                o[:, i] = causal_attention(q[:, i], k[:, i // g], v[:, i // g])
             out.append({"k": k, "v": v})
             h = self._post_attn(l, h, o)
         return out

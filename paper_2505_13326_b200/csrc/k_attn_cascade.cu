@@ -138,7 +138,6 @@ __global__ void __launch_bounds__(NW * 32, 1)
   extern __shared__ __align__(128) uint8_t sraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpSmem<HD, NS, SW>& sm = reinterpret_cast<WarpSmem<HD, NS, SW>*>(sraw)[warp];
-  const int n_items = *pl.n_items * D.kvh;
   int* work = pl.work + layer;
   const float sl2 = 1.4426950408889634f * rsqrtf((float)HD);   // log2(e) / sqrt(hd)
 
@@ -152,6 +151,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncwarp();
+  pdl_wait();                      // predecessor's q / KV writes are visible from here on
+  pdl_trigger();
+  const int n_items = *pl.n_items * D.kvh;
 
   // ---- issue side (warp-uniform state): ring of decoded items; the issue cursor runs up
   //      to NS stages ahead of the consume cursor, across item boundaries
@@ -351,6 +353,8 @@ __global__ void __launch_bounds__(256) k_attn_merge(const float* __restrict__ pa
                                                     const float* __restrict__ part_lse, bf16* __restrict__ out,
                                                     float* __restrict__ dbg, Dims D, Rows rows, Reqs reqs,
                                                     AttnPlan pl, int n) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int C = HD / 32;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= n * D.qh) return;
@@ -398,6 +402,8 @@ __global__ void __launch_bounds__(256) k_attn_merge(const float* __restrict__ pa
 __global__ void __launch_bounds__(1024) k_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl) {
   constexpr int NB = 64;                       // size buckets
   __shared__ int cnt[NB], base[NB];
+  pdl_wait();
+  pdl_trigger();
   const int tid = threadIdx.x;
   const int nu = *pl.n_units;
   const int bw = (pl.CH + NB - 1) / NB;        // tokens per bucket
@@ -506,6 +512,8 @@ __global__ void __launch_bounds__(1024) k_attn_plan(Dims D, Rows rows, Reqs reqs
 // running row, each running suffix once, plus q and o (profiling only)
 __global__ void __launch_bounds__(1024) k_attn_account(Dims D, Rows rows, Reqs reqs, int n, double* acc) {
   __shared__ double red[32];
+  pdl_wait();
+  pdl_trigger();
   __shared__ unsigned char live[1024];     // request slots with a running row (S <= 1024)
   for (int i = threadIdx.x; i < D.S; i += 1024) live[i] = 0;
   __syncthreads();
@@ -534,11 +542,11 @@ void launch_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat
   k_attn_plan<<<1, 1024, 0, s>>>(D, rows, reqs, pl, n, flat);
 }
 void launch_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s) {
-  k_attn_items<<<1, 1024, 0, s>>>(D, rows, reqs, pl);
+  launch_pdl(k_attn_items, dim3(1), dim3(1024), 0, s, D, rows, reqs, pl);
 }
 void launch_attn_account(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, double* acc, cudaStream_t s) {
   (void)pl;
-  k_attn_account<<<1, 1024, 0, s>>>(D, rows, reqs, n, acc);
+  launch_pdl(k_attn_account, dim3(1), dim3(1024), 0, s, D, rows, reqs, n, acc);
 }
 
 static int g_sms = 0;
@@ -551,8 +559,8 @@ static void launch_cfg(const bf16* q, const bf16* pool, float* part_o, float* pa
     cudaFuncSetAttribute(k_attn_cascade<HD, NW, NS, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     a = true;
   }
-  k_attn_cascade<HD, NW, NS, SW><<<g_sms, NW * 32, sm, s>>>(q, pool, part_o, part_lse, out, dbg, D, layer, rows,
-                                                             reqs, pl);
+  launch_pdl(k_attn_cascade<HD, NW, NS, SW>, dim3(g_sms), dim3(NW * 32), sm, s, q, pool, part_o, part_lse, out, dbg,
+             D, layer, rows, reqs, pl);
 }
 static int attn_cfg() {
   static int c = -1;
@@ -571,7 +579,8 @@ static void launch_hd(const bf16* q, const bf16* pool, bf16* out, float* dbg, fl
     case 3: launch_cfg<HD, 7, 3, 16>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
     default: launch_cfg<HD, 8, 3, 16>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
   }
-  k_attn_merge<HD><<<(n * D.qh * 32 + 255) / 256, 256, 0, s>>>(part_o, part_lse, out, dbg, D, rows, reqs, pl, n);
+  launch_pdl(k_attn_merge<HD>, dim3((n * D.qh * 32 + 255) / 256), dim3(256), 0, s, part_o, part_lse, out, dbg, D,
+             rows, reqs, pl, n);
 }
 void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse,
                          Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s) {

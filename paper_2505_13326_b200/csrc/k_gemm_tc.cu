@@ -21,7 +21,9 @@
 #include "kernels.h"
 
 namespace {
-constexpr int BM = 128, BK = 64, STAGES = 4;
+constexpr int BM = 128, BK = 64;
+// pipeline depth: ~192 KB of A+B stages in flight per SM whatever the tile width
+template <int BN> struct Stages { static constexpr int value = (192 * 1024) / ((BM + BN) * BK * 2); };
 constexpr int NTHREADS = 192;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -90,10 +92,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 
 template <int BN>
 struct Smem {
+  static constexpr int STAGES = Stages<BN>::value;
   alignas(1024) bf16 a[STAGES][BM * BK];
   alignas(1024) bf16 b[STAGES][BN * BK];
   uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   uint32_t tmem_base;
+  float slab[4][32][33];   // per epilogue warp: 32 rows x 32 cols, padded (coalesced stores)
 };
 
 // MODE: GEMM_STORE (C = AB^T + bias), GEMM_ACCUM (C += AB^T), GEMM_SWIGLU (columns of each
@@ -104,9 +108,10 @@ struct Smem {
 template <int BN, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* C,
-              const float* __restrict__ bias, bf16* act, int M, int N, int K, int S) {
+              const float* __restrict__ bias, bf16* act, int M, int N, int K, int S, const __grid_constant__ QkvEpi epi) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem<BN>& sm = *reinterpret_cast<Smem<BN>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int STAGES = Smem<BN>::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN, ntiles = mt * nt * S;
   const int kb_all = (K + BK - 1) / BK;
@@ -133,6 +138,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = sm.tmem_base;
+  if (threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -140,10 +146,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
       int stage = 0;
       uint32_t phase = 0;
+      bool first = true;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         int m0, n0, kb0, kb1, sp;
         unit_of(t, m0, n0, kb0, kb1, sp);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        int kb = kb0;
+        if (first) {
+          // PDL: the weight tiles of the first stages do not depend on the previous kernel;
+          // start them before waiting for it, then load the activations.
+          first = false;
+          const int pre = min(STAGES, kb1 - kb0);
+          for (int i = 0; i < pre; ++i) {
+            mbar_expect_tx(&sm.full[i], (BM + BN) * BK * 2);
+            tma_load_2d(sm.b[i], &tmB, &sm.full[i], (kb0 + i) * BK, n0);
+          }
+          pdl_wait();
+          for (int i = 0; i < pre; ++i) tma_load_2d(sm.a[i], &tmA, &sm.full[i], (kb0 + i) * BK, m0);
+          kb += pre;
+          stage = pre % STAGES;
+          phase = pre == STAGES ? 1 : 0;
+        }
+        for (; kb < kb1; ++kb) {
           mbar_wait(&sm.empty[stage], phase ^ 1);
           mbar_expect_tx(&sm.full[stage], (BM + BN) * BK * 2);
           tma_load_2d(sm.a[stage], &tmA, &sm.full[stage], kb * BK, m0);
@@ -151,6 +174,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
+      if (first) pdl_wait();
     }
   } else if (warp == 1) {
     // instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = 128
@@ -183,6 +207,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else {
     // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
+    pdl_wait();   // outputs may be read by the previous kernel; inputs (bias, rows) are visible
     const int q = warp & 3;
     const int row = q * 32 + lane;
     int it = 0;
@@ -196,7 +221,76 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       asm volatile("tcgen05.fence::after_thread_sync;");
       const int gm = m0 + row;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + as * BN;
-      if (MODE == GEMM_SWIGLU) {
+      if (MODE == GEMM_QKV) {
+        // tile = one head (BN == head_dim): q / k heads are rotated (pairs i, i + hd/2), k and v
+        // are appended to the paged pool at the row's slot (common.cuh layout and swizzle)
+        const Dims& D = epi.D;
+        const int head = n0 / BN;
+        constexpr int HALF = BN / 2;
+        int pos = 0;
+        bool kv_ok = false;
+        long long blk = 0;
+        int sib = 0;
+        if (gm < M) {
+          if (epi.a.prefill_slot >= 0) {
+            pos = epi.a.p0 + gm;
+            blk = epi.reqs.prefix[(long long)epi.a.prefill_slot * D.MPB + pos / D.bs];
+            sib = pos % D.bs;
+            kv_ok = true;
+          } else if (epi.rows.status[gm] == RUNNING_ST) {
+            const int l = epi.rows.ell[gm];
+            pos = epi.reqs.P[epi.rows.slot[gm]] - 1 + l;
+            blk = epi.rows.table[(long long)gm * D.MBR + l / D.bs];
+            sib = l % D.bs;
+            kv_ok = true;
+          }
+        }
+        const bool rot = head < D.qh + D.kvh;
+        const float* cs = epi.rope_cs + (long long)pos * BN;   // [cos(half) | sin(half)]
+#pragma unroll 1
+        for (int c = 0; c < HALF; c += 32) {
+          float x1[32], x2[32];
+          tmem_ld32(tbase + c, x1);
+          tmem_ld32(tbase + HALF + c, x2);
+          if (gm < M) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float a = x1[j] + epi.bias[n0 + c + j], b = x2[j] + epi.bias[n0 + HALF + c + j];
+              if (rot) {
+                const float co = cs[c + j], sn = cs[HALF + c + j];
+                const float y1 = a * co - b * sn, y2 = b * co + a * sn;
+                a = y1;
+                b = y2;
+              }
+              x1[j] = a;
+              x2[j] = b;
+            }
+            if (head < D.qh) {
+              bf16* qd = epi.qout + ((long long)gm * D.qh + head) * BN;
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                __align__(16) bf16 o1[8], o2[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) { o1[e] = __float2bfloat16_rn(x1[j + e]); o2[e] = __float2bfloat16_rn(x2[j + e]); }
+                *reinterpret_cast<uint4*>(qd + c + j) = *reinterpret_cast<uint4*>(o1);
+                *reinterpret_cast<uint4*>(qd + HALF + c + j) = *reinterpret_cast<uint4*>(o2);
+              }
+            } else if (kv_ok) {
+              const int kv = head < D.qh + D.kvh ? 0 : 1;
+              const int hh = kv == 0 ? head - D.qh : head - D.qh - D.kvh;
+              bf16* tile = epi.pool + kv_tile_off(D, epi.layer, blk, kv, hh);
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                __align__(16) bf16 o1[8], o2[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) { o1[e] = __float2bfloat16_rn(x1[j + e]); o2[e] = __float2bfloat16_rn(x2[j + e]); }
+                *reinterpret_cast<uint4*>(tile + kv_swz<bf16>(sib, c + j, BN)) = *reinterpret_cast<uint4*>(o1);
+                *reinterpret_cast<uint4*>(tile + kv_swz<bf16>(sib, HALF + c + j, BN)) = *reinterpret_cast<uint4*>(o2);
+              }
+            }
+          }
+        }
+      } else if (MODE == GEMM_SWIGLU) {
         const int F = N / 2;   // N = 2F interleaved in BN-wide tiles
         const int f0 = n0 / 2;
 #pragma unroll 1
@@ -221,34 +315,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
       } else {
+        // fp32 output: stage each 32 x 32 slab in shared memory, then store row by row so
+        // that every warp store instruction writes one full 128-byte line
+        float (*slab)[33] = sm.slab[q];
+        const int mrow0 = m0 + q * 32;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           float v[32];
           tmem_ld32(tbase + c, v);
-          const int gn = n0 + c;
-          if (gm < M && gn < N) {
-            float* dst = Cs + (size_t)gm * N + gn;
-            if (gn + 32 <= N) {
 #pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                if (bias) { x.x += bias[gn + j]; x.y += bias[gn + j + 1]; x.z += bias[gn + j + 2]; x.w += bias[gn + j + 3]; }
-                if (MODE == GEMM_ACCUM) {
-                  float4 y = *reinterpret_cast<float4*>(dst + j);
-                  x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
-                }
-                *reinterpret_cast<float4*>(dst + j) = x;
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                if (gn + j < N) {
-                  float x = v[j] + (bias ? bias[gn + j] : 0.f);
-                  dst[j] = MODE == GEMM_ACCUM ? dst[j] + x : x;
-                }
-              }
+          for (int j = 0; j < 32; ++j) slab[lane][j] = v[j];
+          __syncwarp();
+          const int gn = n0 + c + lane;
+          const float bv = (bias && gn < N) ? bias[gn] : 0.f;
+#pragma unroll 4
+          for (int rr = 0; rr < 32; ++rr) {
+            const int gm2 = mrow0 + rr;
+            if (gm2 < M && gn < N) {
+              float* dst = Cs + (size_t)gm2 * N + gn;
+              const float x = slab[rr][lane] + bv;
+              *dst = MODE == GEMM_ACCUM ? *dst + x : x;
             }
           }
+          __syncwarp();
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
@@ -308,7 +397,7 @@ int g_num_sms = 0;
 
 template <int BN, int MODE>
 bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K, int S,
-               cudaStream_t s) {
+               cudaStream_t s, const QkvEpi* epi = nullptr) {
   const CUtensorMap* ma = g_maps.get(A, M, K, BM);
   const CUtensorMap* mb = g_maps.get(B, N, K, BN);
   if (!ma || !mb) return false;
@@ -321,7 +410,9 @@ bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* 
   if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
   const int ntiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * S;
   const int grid = ntiles < g_num_sms ? ntiles : g_num_sms;
-  k_gemm_tc<BN, MODE><<<grid, NTHREADS, smem, s>>>(*ma, *mb, C, bias, act, M, N, K, S);
+  QkvEpi e{};
+  if (epi) e = *epi;
+  launch_pdl(k_gemm_tc<BN, MODE>, dim3(grid), dim3(NTHREADS), smem, s, *ma, *mb, C, bias, act, M, N, K, S, e);
   return true;
 }
 }  // namespace
@@ -345,6 +436,14 @@ bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float
   if (mode == GEMM_STORE) return launch_bn<256, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s);
   if (mode == GEMM_ACCUM) return launch_bn<256, GEMM_ACCUM>(A, B, bias, C, act, M, N, K, S, s);
   return launch_bn<256, GEMM_SWIGLU>(A, B, bias, C, act, M, N, K, S, s);
+}
+
+bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const QkvEpi& epi, cudaStream_t s) {
+  if (M <= 0) return true;
+  if (K % 8) return false;
+  if (epi.D.hd == 128) return launch_bn<128, GEMM_QKV>(A, B, nullptr, nullptr, nullptr, M, N, K, 1, s, &epi);
+  if (epi.D.hd == 64) return launch_bn<64, GEMM_QKV>(A, B, nullptr, nullptr, nullptr, M, N, K, 1, s, &epi);
+  return false;
 }
 
 // Split choice for the decode GEMMs: enough (tile x split) units to cover the SMs.

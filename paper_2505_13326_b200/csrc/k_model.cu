@@ -31,13 +31,15 @@ void launch_init_tensor(T* p, long long n, int tid, int is_norm, float std, unsi
 // ------------------------------------------------------------ embedding: h = E[tok]
 template <typename T>
 __global__ void k_embed(const int* __restrict__ tok, const T* __restrict__ emb, float* __restrict__ h, int d) {
+  pdl_wait();
+  pdl_trigger();
   int r = blockIdx.x;
   const T* e = emb + (long long)tok[r] * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) h[(long long)r * d + i] = to_f(e[i]);
 }
 template <typename T>
 void launch_embed(const int* tok, const T* emb, float* h, int n, int d, cudaStream_t s) {
-  if (n > 0) k_embed<T><<<n, 256, 0, s>>>(tok, emb, h, d);
+  if (n > 0) launch_pdl(k_embed<T>, dim3(n), dim3(256), 0, s, tok, emb, h, d);
 }
 
 // ------------------------------------------------------------ RMSNorm (+ residual partials)
@@ -68,6 +70,8 @@ __global__ void __launch_bounds__(128) k_rmsnorm(float* __restrict__ h, const fl
                                                   long long pstride, const T* __restrict__ g, T* __restrict__ out,
                                                   float* __restrict__ out32, const int* __restrict__ status, int n,
                                                   int d, float eps) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   if (status && status[r] != RUNNING_ST) return;
   float4* x = reinterpret_cast<float4*>(h + (long long)r * d);
@@ -99,7 +103,9 @@ __global__ void __launch_bounds__(128) k_rmsnorm(float* __restrict__ h, const fl
 template <typename T>
 void launch_rmsnorm(float* h, const float* parts, int np, const T* g, T* out, float* out32, const int* status, int n,
                     int d, float eps, cudaStream_t s) {
-  if (n > 0) k_rmsnorm<T><<<n, 128, 0, s>>>(h, parts, np, (long long)n * d, g, out, out32, status, n, d, eps);
+  if (n > 0)
+    launch_pdl(k_rmsnorm<T>, dim3(n), dim3(128), 0, s, h, parts, np, (long long)n * d, g, out, out32, status, n, d,
+               eps);
 }
 
 // ------------------------------------------------------------ RoPE + KV append

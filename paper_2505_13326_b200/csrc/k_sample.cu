@@ -24,6 +24,8 @@ constexpr int SCHUNK = 4096;
 
 __global__ void __launch_bounds__(256) k_sample_part(const float* __restrict__ logits, Dims D, Rows rows, Reqs reqs,
                                                       float* __restrict__ pkey, int* __restrict__ pv, int nchunk) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x, c = blockIdx.y;
   if (rows.status[r] != RUNNING_ST) return;
   const int slot = rows.slot[r], b = rows.b[r];
@@ -76,6 +78,8 @@ __global__ void __launch_bounds__(256) k_sample_part(const float* __restrict__ l
 
 __global__ void __launch_bounds__(32) k_sample_final(Dims D, Rows rows, Reqs reqs, Ctr* ctr, const float* pkey,
                                                      const int* pv, int nchunk, int* dbg_tok) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x, lane = threadIdx.x;
   if (rows.status[r] != RUNNING_ST) return;
   const int slot = rows.slot[r], b = rows.b[r];
@@ -119,12 +123,14 @@ void launch_sample(const float* logits, Dims D, Rows rows, Reqs reqs, Ctr* ctr, 
                    float* pkey, int* pv, cudaStream_t s) {
   if (n <= 0) return;
   const int nchunk = (D.V + SCHUNK - 1) / SCHUNK;
-  k_sample_part<<<dim3(n, nchunk), 256, 0, s>>>(logits, D, rows, reqs, pkey, pv, nchunk);
-  k_sample_final<<<n, 32, 0, s>>>(D, rows, reqs, ctr, pkey, pv, nchunk, dbg_tok);
+  launch_pdl(k_sample_part, dim3(n, nchunk), dim3(256), 0, s, logits, D, rows, reqs, pkey, pv, nchunk);
+  launch_pdl(k_sample_final, dim3(n), dim3(32), 0, s, D, rows, reqs, ctr, pkey, pv, nchunk, dbg_tok);
 }
 int sample_chunks(int V) { return (V + SCHUNK - 1) / SCHUNK; }
 
 __global__ void k_step_begin(Ctr* ctr) {
+  pdl_wait();
+  pdl_trigger();
   if (ctr->live > 0) { ctr->wstep += 1; ctr->steps += 1; }
 }
-void launch_step_begin(Ctr* ctr, cudaStream_t s) { k_step_begin<<<1, 1, 0, s>>>(ctr); }
+void launch_step_begin(Ctr* ctr, cudaStream_t s) { launch_pdl(k_step_begin, dim3(1), dim3(1), 0, s, ctr); }

@@ -2,6 +2,11 @@
 #pragma once
 #include "common.cuh"
 
+struct RopeArgs {
+  // decode mode (prefill_slot == -1): per-row positions from Rows/Reqs; prefill mode: slot >= 0
+  int prefill_slot, p0;
+};
+
 // ---- model (k_model.cu)
 template <typename T> void launch_init_tensor(T* p, long long n, int tensor_id, int is_norm, float std,
                                               unsigned long long seed, cudaStream_t s);
@@ -9,10 +14,6 @@ template <typename T> void launch_embed(const int* tok, const T* emb, float* h, 
 // h[r] += sum_{s<np} parts[s][r] (fixed order; np may be 0), then out = RMSNorm(h) * g
 template <typename T> void launch_rmsnorm(float* h, const float* parts, int np, const T* g, T* out, float* out32,
                                           const int* status, int n, int d, float eps, cudaStream_t s);
-struct RopeArgs {
-  // decode mode (slot == -1): per-row positions from Rows/Reqs; prefill mode: slot >= 0
-  int prefill_slot, p0;
-};
 // qkv = sum_{s<np} parts[s] + bias (fixed order), then RoPE + paged KV append
 template <typename T> void launch_rope_append(const float* parts, int np, const float* bias, T* qout, T* pool,
                                               const float* rope_cs, Dims D, int layer, Rows rows, Reqs reqs,
@@ -24,7 +25,20 @@ template <typename T> void launch_convert(const float* in, T* out, long long n, 
 template <typename T> void launch_to_f32(const T* in, float* out, long long n, cudaStream_t s);
 
 // ---- GEMM (k_gemm.cu): C[m][n] (+)= A[m][k] . B[n][k]^T (+ bias[n]); fp32 accumulate.
-enum { GEMM_STORE = 0, GEMM_ACCUM = 1, GEMM_SWIGLU = 2 };
+enum { GEMM_STORE = 0, GEMM_ACCUM = 1, GEMM_SWIGLU = 2, GEMM_QKV = 3 };
+// QKV epilogue: bias, rotate-half RoPE, q -> qout (bf16), k/v -> paged pool (decode: running
+// rows only; prefill: prefix positions p0 + row)
+struct QkvEpi {
+  const float* bias;
+  bf16* qout;
+  bf16* pool;
+  const float* rope_cs;
+  Dims D;
+  int layer;
+  Rows rows;
+  Reqs reqs;
+  RopeArgs a;
+};
 template <typename T> void launch_gemm_simt(const T* A, const T* B, const float* bias, float* C, int M, int N,
                                             int K, int mode, cudaStream_t s);
 
@@ -38,6 +52,8 @@ void launch_interleave_gate_up(bf16* w, bf16* tmp, int F, int d, cudaStream_t s)
 bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
                           int mode, int S, int BN, cudaStream_t s);
 void choose_split(int M, int N, int K, int& S, int& BN);
+// QKV projection with the bias + RoPE + paged KV append fused into the epilogue (tile = 1 head)
+bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const QkvEpi& epi, cudaStream_t s);
 
 // ---- attention (k_attn.cu)
 template <typename T> void launch_attn_decode_simple(const T* q, const T* pool, T* out, float* dbg, Dims D,

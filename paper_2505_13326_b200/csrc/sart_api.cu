@@ -257,6 +257,25 @@ int proj(sart_ctx* ctx, const T* A, const T* B, int M, int N, int K) {
   return S;
 }
 
+// QKV projection + bias + RoPE + paged KV append: one fused tcgen05 launch in bf16 (tile =
+// one head); fp32 mode: SIMT GEMM into the partial buffer + the RoPE/append kernel.
+template <typename T>
+void qkv_rope(sart_ctx* ctx, int l, int n, RopeArgs ra) {
+  const Dims& D = ctx->D;
+  const float* bias = ctx->fparams + ctx->f_bqkv + (size_t)l * D.qkv;
+  if constexpr (std::is_same<T, bf16>::value) {
+    QkvEpi e{bias, (bf16*)ctx->q, (bf16*)ctx->pool, ctx->rope_cs, D, l, ctx->rows, ctx->reqs, ra};
+    if (!launch_gemm_qkv((bf16*)ctx->a, ctx->W_<bf16>(t_layer(l, 1)), n, D.qkv, D.d, e, ctx->st))
+      ctx->gemm_failed = true;
+    ctx->launches++;
+  } else {
+    int np = proj<T>(ctx, (T*)ctx->a, ctx->W_<T>(t_layer(l, 1)), n, D.qkv, D.d);
+    launch_rope_append<T>(ctx->parts, np, bias, (T*)ctx->q, (T*)ctx->pool, ctx->rope_cs, D, l, ctx->rows, ctx->reqs,
+                          ra, n, ctx->st);
+    ctx->launches++;
+  }
+}
+
 // MLP up-projection + SwiGLU: fused tcgen05 epilogue on gate/up-interleaved weights (bf16),
 // or GEMM + elementwise kernel (fp32 mode).
 template <typename T>
@@ -315,12 +334,9 @@ void decode_step(sart_ctx* ctx, int n) {
   for (int l = 0; l < D.L; ++l) {
     launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, n, D.d,
                       D.eps, s);
-    int np = proj<T>(ctx, (T*)ctx->a, ctx->W_<T>(t_layer(l, 1)), n, D.qkv, D.d);
-    launch_rope_append<T>(ctx->parts, np, ctx->fparams + ctx->f_bqkv + (size_t)l * D.qkv, (T*)ctx->q, (T*)ctx->pool,
-                          ctx->rope_cs, D, l, ctx->rows, ctx->reqs, RopeArgs{-1, 0}, n, s);
-    ctx->launches += 2;
+    qkv_rope<T>(ctx, l, n, RopeArgs{-1, 0});
     layer_attention<T>(ctx, l, n);
-    np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), n, D.d, D.qh * D.hd);
+    int np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), n, D.d, D.qh * D.hd);
     launch_rmsnorm<T>(ctx->h, ctx->parts, np, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, n, D.d, D.eps,
                       s);
     mlp_up<T>(ctx, l, n);
@@ -347,13 +363,10 @@ void prefill(sart_ctx* ctx, int slot, int P) {
     for (int l = 0; l < D.L; ++l) {
       launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, c, D.d,
                         D.eps, s);
-      int np = proj<T>(ctx, (T*)ctx->a, ctx->W_<T>(t_layer(l, 1)), c, D.qkv, D.d);
-      launch_rope_append<T>(ctx->parts, np, ctx->fparams + ctx->f_bqkv + (size_t)l * D.qkv, (T*)ctx->q,
-                            (T*)ctx->pool, ctx->rope_cs, D, l, ctx->rows, ctx->reqs, RopeArgs{slot, p0}, c, s);
-      ctx->launches += 2;
+      qkv_rope<T>(ctx, l, c, RopeArgs{slot, p0});
       if (l == D.L - 1) break;  // the last layer's output is not part of the prefix KV
       launch_attn_prefill<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, D, l, ctx->reqs, slot, p0, c, s);
-      np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), c, D.d, D.qh * D.hd);
+      int np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), c, D.d, D.qh * D.hd);
       launch_rmsnorm<T>(ctx->h, ctx->parts, np, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, c, D.d,
                         D.eps, s);
       mlp_up<T>(ctx, l, c);

@@ -29,9 +29,9 @@ def forced_tokens(rng, N, cap, V):
     return t
 
 
-def oracle_teacher_forced(model, prompt, forced, steps, layers):
+def oracle_teacher_forced(model, prompt, forced, steps, layers, prefix=None):
     P = len(prompt)
-    prefix = model.prefill(prompt)
+    prefix = model.prefill(prompt) if prefix is None else prefix
     suffix = [{"k": [], "v": []} for _ in range(model.s.n_layers)]
     out = []
     for s in range(1, steps + 1):
@@ -56,7 +56,8 @@ def run_teacher_forced(shape, dtype, prompts, N, steps, bs, tol, std=0.08, seed=
         ft = forced_tokens(rng, N, steps, shape.vocab)
         forced[rid] = ft
         g.admit(Request(rid, prompt, N, N, -1.0, 0, None), forced_tokens=ft)
-    ref = {(rid, b): oracle_teacher_forced(model, prompts[rid], forced[rid][b], steps, layers)
+    prefixes = [model.prefill(p) for p in prompts]      # shared by the request's branches
+    ref = {(rid, b): oracle_teacher_forced(model, prompts[rid], forced[rid][b], steps, layers, prefixes[rid])
            for rid in range(len(prompts)) for b in range(N)}
     worst = dict(logits=0.0, prm=0.0, attn=0.0)
     step_of = {}
@@ -184,3 +185,30 @@ def test_model_mode_end_to_end_fp32():
     for a, b in zip(gres, ores):
         assert a["tokens"] == b["tokens"]
     g.close()
+
+
+def _slice(name, layers=1, vocab=4096):
+    """attention / GEMM geometry of a BASELINE shape with fewer layers and a small vocab
+    (the vocab only sizes the LM head, which the 1.5B-L2 test covers at full size)"""
+    import dataclasses
+    sh = SHAPES[name].with_layers(layers)
+    return dataclasses.replace(sh, name=f"{name}-L{layers}-V{vocab}", vocab=vocab)
+
+
+@pytest.mark.parametrize("name", ["7B", "14B"])
+def test_7b_14b_geometry_bf16_teacher_forced(name):
+    """g = 7 and g = 5: prefix m-tiles straddle rows (16 is not a multiple of g)."""
+    shape = _slice(name)
+    prompts = [gen_prompt(11, shape.vocab, EOS, 40, 40), gen_prompt(12, shape.vocab, EOS, 97, 97)]
+    w = run_teacher_forced(shape, "bf16", prompts, N=5, steps=10, bs=32, tol=2e-2, std=0.02)
+    print(name, "worst", w)
+
+
+@pytest.mark.parametrize("attn_mode", [0, 1])
+def test_long_prefix_many_branches(attn_mode):
+    """C5-like: one long shared prompt, 16 branches (two prefix groups of <= 12 rows at g=5,
+    several m-tiles per group, prefix chunks of 512) -- cascade and flat paths."""
+    shape = _slice("14B")
+    prompts = [gen_prompt(13, shape.vocab, EOS, 1300, 1300)]
+    w = run_teacher_forced(shape, "bf16", prompts, N=16, steps=4, bs=64, tol=2e-2, std=0.02, attn_mode=attn_mode)
+    print("long prefix worst", attn_mode, w)

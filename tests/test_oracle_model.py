@@ -147,3 +147,11 @@ def test_prm_head_closed_form():
     hdn = np.maximum(z @ w["prm_w1"].T.astype(np.float64) + w["prm_b1"], 0)
     lg = hdn @ w["prm_w2"].T.astype(np.float64) + w["prm_b2"]
     assert np.allclose(m.prm_score(z), 1.0 / (1.0 + np.exp(-(lg[:, 1] - lg[:, 0]))), atol=1e-14)
+
+
+def test_causal_attention_equals_per_position_attention():
+    rng = np.random.default_rng(9)
+    n, hd = 37, 64
+    Q, K, V = rng.standard_normal((n, hd)), rng.standard_normal((n, hd)) * 2, rng.standard_normal((n, hd))
+    ref = np.stack([om.attention(Q[t], K[: t + 1], V[: t + 1]) for t in range(n)])
+    assert np.allclose(om.causal_attention(Q, K, V), ref, atol=1e-12)
