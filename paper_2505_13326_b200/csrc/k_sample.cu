@@ -4,20 +4,12 @@
 // (readings R24, R25).  Ties go to the lowest v.  fp32 arithmetic; -ln u is evaluated as
 // log1p(-(2^24 - x - 0.5) 2^-24) in the upper half so u is represented exactly.
 #include "kernels.h"
-
-__device__ __forceinline__ float gumbel_from_word(uint32_t w) {
-  uint32_t x = w >> 8;
-  float lnu;
-  if (x < (1u << 23)) lnu = logf(((float)x + 0.5f) * (1.0f / 16777216.0f));
-  else lnu = log1pf(-(((float)((1u << 24) - x)) - 0.5f) * (1.0f / 16777216.0f));
-  return -logf(-lnu);
-}
-
-__device__ __forceinline__ void better(float& bk, int& bv, float k, int v) {
-  if (k > bk || (k == bk && v < bv)) { bk = k; bv = v; }
-}
+#include "sample_math.cuh"
 
 // Phase 1: one CTA per (row, vocab chunk of SCHUNK entries) -> the chunk's best (key, v).
+// (Fusing phase 1 into the LM-head GEMM epilogue was measured slower: 691 us vs 233 + 344 us
+// per C2 step -- the epilogue's 8 warps per SM cannot hide the Philox/log latency that the
+// stand-alone kernel hides with full occupancy.)
 // Phase 2: one warp per row reduces the chunks (exact max with the lowest-v tie rule, so the
 // reduction order does not matter) and updates the row: history, EOS / cap, counters.
 constexpr int SCHUNK = 4096;
@@ -37,7 +29,6 @@ __global__ void __launch_bounds__(256) k_sample_part(const float* __restrict__ l
   const float* lg = logits + (long long)r * D.V;
   const uint32_t rid = (uint32_t)reqs.id[slot];
   const uint32_t k0 = (uint32_t)D.seed, k1 = (uint32_t)(D.seed >> 32);
-  const bool unit_tau = D.tau == 1.0f;
   float bk = -INFINITY;
   int bv = 0x7fffffff;
   const int g_lo = c * (SCHUNK / 4), g_hi = min((c + 1) * (SCHUNK / 4), (D.V + 3) >> 2);
@@ -46,18 +37,7 @@ __global__ void __launch_bounds__(256) k_sample_part(const float* __restrict__ l
                                          : make_float4(lg[4 * g4], 4 * g4 + 1 < D.V ? lg[4 * g4 + 1] : 0.f,
                                                        4 * g4 + 2 < D.V ? lg[4 * g4 + 2] : 0.f, 0.f);
     const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-    u32x4 w{0, 0, 0, 0};
-    if (D.tau > 0.f) w = philox4x32_10(u32x4{(uint32_t)g4, (uint32_t)s, rid, (uint32_t)b}, k0, k1);
-    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int v = 4 * g4 + j;
-      if (v >= D.V || (mask_eos && v == D.eos)) continue;
-      float key;
-      if (D.tau > 0.f) key = (unit_tau ? lv[j] : lv[j] / D.tau) + gumbel_from_word(ws[j]);
-      else key = lv[j];
-      better(bk, bv, key, v);
-    }
+    sample_group4(bk, bv, lv, 4 * g4, D.V, s, rid, (uint32_t)b, k0, k1, D.tau, mask_eos, D.eos);
   }
   __shared__ float sk[8];
   __shared__ int sv[8];
@@ -127,6 +107,7 @@ void launch_sample(const float* logits, Dims D, Rows rows, Reqs reqs, Ctr* ctr, 
   launch_pdl(k_sample_final, dim3(n), dim3(32), 0, s, D, rows, reqs, ctr, pkey, pv, nchunk, dbg_tok);
 }
 int sample_chunks(int V) { return (V + SCHUNK - 1) / SCHUNK; }
+
 
 __global__ void k_step_begin(Ctr* ctr) {
   pdl_wait();

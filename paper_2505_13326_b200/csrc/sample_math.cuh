@@ -1,0 +1,38 @@
+// Per-element arithmetic of the Gumbel-max sampler (readings R24, R25), shared by the
+// stand-alone sampler (k_sample.cu) and the sampler fused into the LM-head GEMM epilogue.
+//   key_v = logit_v / tau + G_v,  G_v = -ln(-ln u_v),  u_v = ((w >> 8) + 0.5) 2^-24,
+//   w = Philox4x32-10((v >> 2, s, request_id, branch), seed)[v & 3];  ties -> lowest v.
+// fp32; -ln u is evaluated as log1p(-(2^24 - x - 0.5) 2^-24) in the upper half so that u
+// is represented exactly.
+#pragma once
+#include "common.cuh"
+
+__device__ __forceinline__ float gumbel_from_word(uint32_t w) {
+  uint32_t x = w >> 8;
+  float lnu;
+  if (x < (1u << 23)) lnu = logf(((float)x + 0.5f) * (1.0f / 16777216.0f));
+  else lnu = log1pf(-(((float)((1u << 24) - x)) - 0.5f) * (1.0f / 16777216.0f));
+  return -logf(-lnu);
+}
+
+__device__ __forceinline__ void better(float& bk, int& bv, float k, int v) {
+  if (k > bk || (k == bk && v < bv)) { bk = k; bv = v; }
+}
+
+// fold 4 consecutive vocab entries v0..v0+3 (v0 % 4 == 0) into (bk, bv)
+__device__ __forceinline__ void sample_group4(float& bk, int& bv, const float* lv, int v0, int V, int s, uint32_t rid,
+                                              uint32_t b, uint32_t k0, uint32_t k1, float tau, bool mask_eos,
+                                              int eos) {
+  u32x4 w{0, 0, 0, 0};
+  if (tau > 0.f) w = philox4x32_10(u32x4{(uint32_t)(v0 >> 2), (uint32_t)s, rid, b}, k0, k1);
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int v = v0 + j;
+    if (v >= V || (mask_eos && v == eos)) continue;
+    float key;
+    if (tau > 0.f) key = (tau == 1.0f ? lv[j] : lv[j] / tau) + gumbel_from_word(ws[j]);
+    else key = lv[j];
+    better(bk, bv, key, v);
+  }
+}

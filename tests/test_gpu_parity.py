@@ -131,7 +131,8 @@ def test_sampler_matches_oracle_on_gpu_logits():
     weights = gen_weights(shape, "bf16", std=0.08)
     seed = 0x1234_5678_9AB
     g = gpu_engine(shape, "bf16", weights, block_size=16, num_blocks=1024, max_rows=64, max_requests=8,
-                   max_prompt=64, T=1, cap=48, eos_id=EOS, temperature=0.7, sampler_seed=seed)
+                   max_prompt=64, T=1, cap=48, eos_id=EOS, temperature=0.7, sampler_seed=seed,
+                   debug_capture=True)   # logits are stored by the fused LM-head/sampler epilogue
     for rid in range(3):
         g.admit(Request(rid, gen_prompt(rid, shape.vocab, EOS, 10, 30), 4, 4, -1.0, 0, None))
     n_cmp = n_tie = 0
