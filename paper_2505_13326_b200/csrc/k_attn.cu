@@ -102,9 +102,10 @@ __global__ void __launch_bounds__(128) k_attn_decode_simple(const T* __restrict_
 
 template <typename T, int HD>
 __global__ void __launch_bounds__(128) k_attn_prefill(const T* __restrict__ q, const T* __restrict__ pool,
-                                                      T* __restrict__ out, Dims D, int layer, Reqs reqs, int slot,
-                                                      int p0) {
+                                                      T* __restrict__ out, Dims D, int layer, Reqs reqs,
+                                                      const int* __restrict__ pf_slot, const int* __restrict__ pf_pos) {
   const int i = blockIdx.x, head = blockIdx.y;
+  const int slot = pf_slot[i], p = pf_pos[i];
   __shared__ float qs[HD];
   for (int e = threadIdx.x; e < HD; e += blockDim.x) qs[e] = to_f(q[((long long)i * D.qh + head) * HD + e]);
   __syncthreads();
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(128) k_attn_prefill(const T* __restrict__ q, c
   const int bs = D.bs;
   KVSrc<T, HD> src{pool, D, layer, head / D.g};
   auto loc = [=] __device__(int j, long long& blk, int& t) { blk = ptab[j / bs]; t = j % bs; };
-  attend_one<T, HD>(qs, src, p0 + i + 1, loc, out + ((long long)i * D.qh + head) * HD, nullptr);
+  attend_one<T, HD>(qs, src, p + 1, loc, out + ((long long)i * D.qh + head) * HD, nullptr);
 }
 }  // namespace
 
@@ -125,18 +126,18 @@ void launch_attn_decode_simple(const T* q, const T* pool, T* out, float* dbg, Di
   else k_attn_decode_simple<T, 64><<<grid, 128, 0, s>>>(q, pool, out, dbg, D, layer, rows, reqs);
 }
 template <typename T>
-void launch_attn_prefill(const T* q, const T* pool, T* out, Dims D, int layer, Reqs reqs, int slot, int p0, int n,
-                         cudaStream_t s) {
+void launch_attn_prefill(const T* q, const T* pool, T* out, Dims D, int layer, Reqs reqs, const int* pf_slot,
+                         const int* pf_pos, int n, cudaStream_t s) {
   if (n <= 0) return;
   dim3 grid(n, D.qh);
-  if (D.hd == 128) k_attn_prefill<T, 128><<<grid, 128, 0, s>>>(q, pool, out, D, layer, reqs, slot, p0);
-  else k_attn_prefill<T, 64><<<grid, 128, 0, s>>>(q, pool, out, D, layer, reqs, slot, p0);
+  if (D.hd == 128) k_attn_prefill<T, 128><<<grid, 128, 0, s>>>(q, pool, out, D, layer, reqs, pf_slot, pf_pos);
+  else k_attn_prefill<T, 64><<<grid, 128, 0, s>>>(q, pool, out, D, layer, reqs, pf_slot, pf_pos);
 }
 template void launch_attn_decode_simple<float>(const float*, const float*, float*, float*, Dims, int, Rows, Reqs,
                                                int, cudaStream_t);
 template void launch_attn_decode_simple<bf16>(const bf16*, const bf16*, bf16*, float*, Dims, int, Rows, Reqs, int,
                                               cudaStream_t);
-template void launch_attn_prefill<float>(const float*, const float*, float*, Dims, int, Reqs, int, int, int,
-                                         cudaStream_t);
-template void launch_attn_prefill<bf16>(const bf16*, const bf16*, bf16*, Dims, int, Reqs, int, int, int,
+template void launch_attn_prefill<float>(const float*, const float*, float*, Dims, int, Reqs, const int*,
+                                         const int*, int, cudaStream_t);
+template void launch_attn_prefill<bf16>(const bf16*, const bf16*, bf16*, Dims, int, Reqs, const int*, const int*, int,
                                         cudaStream_t);

@@ -232,9 +232,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         long long blk = 0;
         int sib = 0;
         if (gm < M) {
-          if (epi.a.prefill_slot >= 0) {
-            pos = epi.a.p0 + gm;
-            blk = epi.reqs.prefix[(long long)epi.a.prefill_slot * D.MPB + pos / D.bs];
+          if (epi.a.pf_slot) {
+            pos = epi.a.pf_pos[gm];
+            blk = epi.reqs.prefix[(long long)epi.a.pf_slot[gm] * D.MPB + pos / D.bs];
             sib = pos % D.bs;
             kv_ok = true;
           } else if (epi.rows.status[gm] == RUNNING_ST) {

@@ -120,9 +120,9 @@ __global__ void k_rope_append(const float* __restrict__ parts, int np, long long
   int r = blockIdx.x;
   int pos, blk, slot_in_blk;
   bool write_kv = true;
-  if (a.prefill_slot >= 0) {
-    pos = a.p0 + r;
-    blk = reqs.prefix[(long long)a.prefill_slot * D.MPB + pos / D.bs];
+  if (a.pf_slot) {
+    pos = a.pf_pos[r];
+    blk = reqs.prefix[(long long)a.pf_slot[r] * D.MPB + pos / D.bs];
     slot_in_blk = pos % D.bs;
   } else {
     if (rows.status[r] != RUNNING_ST) return;

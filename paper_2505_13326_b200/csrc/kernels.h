@@ -3,8 +3,10 @@
 #include "common.cuh"
 
 struct RopeArgs {
-  // decode mode (prefill_slot == -1): per-row positions from Rows/Reqs; prefill mode: slot >= 0
-  int prefill_slot, p0;
+  // decode mode (pf_slot == nullptr): per-row positions from Rows/Reqs.  Prefill mode: row i
+  // of the batch is prompt position pf_pos[i] of request slot pf_slot[i] (batched prefill).
+  const int* pf_slot;
+  const int* pf_pos;
 };
 
 // ---- model (k_model.cu)
@@ -58,8 +60,10 @@ bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const Qk
 // ---- attention (k_attn.cu)
 template <typename T> void launch_attn_decode_simple(const T* q, const T* pool, T* out, float* dbg, Dims D,
                                                      int layer, Rows rows, Reqs reqs, int n, cudaStream_t s);
+// causal attention of a batch of prompt tokens (row i: slot pf_slot[i], position pf_pos[i])
+// over their requests' prefix blocks
 template <typename T> void launch_attn_prefill(const T* q, const T* pool, T* out, Dims D, int layer, Reqs reqs,
-                                               int slot, int p0, int n, cudaStream_t s);
+                                               const int* pf_slot, const int* pf_pos, int n, cudaStream_t s);
 
 // cascade attention (k_attn_cascade.cu).  Per-window plan of work units.
 struct AttnPlan {

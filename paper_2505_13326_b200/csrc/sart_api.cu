@@ -94,7 +94,12 @@ struct sart_ctx {
   void *a = nullptr, *q = nullptr, *o = nullptr, *act = nullptr, *zT = nullptr;
   int* dbg_tok = nullptr;
   int *dbg_slot = nullptr, *dbg_b = nullptr;
-  int* d_prompt = nullptr;
+  int* d_prompt = nullptr;     // batched prefill: tokens, request slots, positions
+  int *d_pf_slot = nullptr, *d_pf_pos = nullptr;
+  int pf_cap = 0;
+  std::vector<int> pf_tok, pf_slot, pf_pos;
+  cudaEvent_t pf_ev[2] = {nullptr, nullptr};
+  bool pf_pending = false;
   AdmitEvent* d_events = nullptr;
   int ev_cap = 0;
   AttnPlan plan{};
@@ -334,7 +339,7 @@ void decode_step(sart_ctx* ctx, int n) {
   for (int l = 0; l < D.L; ++l) {
     launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, n, D.d,
                       D.eps, s);
-    qkv_rope<T>(ctx, l, n, RopeArgs{-1, 0});
+    qkv_rope<T>(ctx, l, n, RopeArgs{nullptr, nullptr});
     layer_attention<T>(ctx, l, n);
     int np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), n, D.d, D.qh * D.hd);
     launch_rmsnorm<T>(ctx->h, ctx->parts, np, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, n, D.d, D.eps,
@@ -350,28 +355,32 @@ void decode_step(sart_ctx* ctx, int n) {
   ctx->launches += 2;
 }
 
+// Batched prefill (Alg. 1 L15): the prompts of every request admitted in this fill
+// loop are processed together, token i being position pf_pos[i] of request slot pf_slot[i];
+// chunks of up to PC tokens run all layers (a later chunk's tokens attend to the KV that
+// earlier chunks wrote).  The last layer only needs its K/V (the prefix has no output).
 template <typename T>
-void prefill(sart_ctx* ctx, int slot, int P) {
+void prefill_batch(sart_ctx* ctx, int ntok) {
   const Dims& D = ctx->D;
   cudaStream_t s = ctx->st;
-  const int ntok = P - 1;
-  for (int p0 = 0; p0 < ntok; p0 += ctx->PC) {
-    const int c = std::min(ctx->PC, ntok - p0);
-    launch_embed<T>(ctx->d_prompt + p0, ctx->W_<T>(t_embed()), ctx->h, c, D.d, s);
+  for (int t0 = 0; t0 < ntok; t0 += ctx->PC) {
+    const int c = std::min(ctx->PC, ntok - t0);
+    const RopeArgs ra{ctx->d_pf_slot + t0, ctx->d_pf_pos + t0};
+    launch_embed<T>(ctx->d_prompt + t0, ctx->W_<T>(t_embed()), ctx->h, c, D.d, s);
     ctx->launches++;
     int np_res = 0;
     for (int l = 0; l < D.L; ++l) {
       launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, c, D.d,
                         D.eps, s);
-      qkv_rope<T>(ctx, l, c, RopeArgs{slot, p0});
-      if (l == D.L - 1) break;  // the last layer's output is not part of the prefix KV
-      launch_attn_prefill<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, D, l, ctx->reqs, slot, p0, c, s);
+      qkv_rope<T>(ctx, l, c, ra);
+      if (l == D.L - 1) break;
+      launch_attn_prefill<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, D, l, ctx->reqs, ra.pf_slot, ra.pf_pos, c, s);
       int np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), c, D.d, D.qh * D.hd);
       launch_rmsnorm<T>(ctx->h, ctx->parts, np, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, c, D.d,
                         D.eps, s);
       mlp_up<T>(ctx, l, c);
       np_res = proj<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), c, D.d, D.F);
-      ctx->launches += 2;
+      ctx->launches += 3;
     }
   }
 }
@@ -424,7 +433,6 @@ int upload_request(sart_ctx* ctx, const HostReq& q, int slot) {
   if (!q.sc.forced_tokens.empty())
     CK(cudaMemcpyAsync(ctx->reqs.forced + sb * D.cap, q.sc.forced_tokens.data(), sizeof(int) * (size_t)q.N * D.cap,
                        cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(ctx->d_prompt, q.prompt.data(), sizeof(int) * q.prompt.size(), cudaMemcpyHostToDevice, s));
   return SART_OK;
 }
 
@@ -482,29 +490,45 @@ int fill(sart_ctx* ctx) {
       pop_off += npre;
       int rc = upload_request(ctx, q, slot);
       if (rc) return rc;
-      rc = flush_events(ctx, ev, pop_off, new_rows, commit_delta);
-      if (rc) return rc;
-      // L15: perform prefilling (prefix = prompt[0:P-1], R22)
-      int64_t t0 = now_ns();
-      if (ctx->bf16) prefill<bf16>(ctx, slot, P);
-      else prefill<float>(ctx, slot, P);
-      CK(cudaGetLastError());
+      // L15: the prompt joins this fill's prefill batch (prefix = prompt[0:P-1], R22)
+      for (int p = 0; p + 1 < P; ++p) {
+        ctx->pf_tok.push_back(q.prompt[p]);
+        ctx->pf_slot.push_back(slot);
+        ctx->pf_pos.push_back(p);
+      }
       SlotInfo& si = ctx->slots[slot];
       si.id = q.id;
       si.N = q.N;
       si.arrival_ns = q.arrival_ns;
-      si.prefill_ns = t0;
+      si.prefill_ns = now_ns();
       si.first_tok = q.prompt[P - 1];
       si.live = true;
       ctx->last_slot_id[slot] = q.id;
       for (int j = 0; j < q.N; ++j) ctx->branch_queue.emplace_back(slot, j);  // L17-19
-      ctx->prefill_ms += (now_ns() - t0) * 1e-6;
       ctx->request_queue.pop_front();
     } else {
       break;  // L8-9
     }
   }
-  return flush_events(ctx, ev, pop_off, new_rows, commit_delta);
+  int rc = flush_events(ctx, ev, pop_off, new_rows, commit_delta);   // all pops, in event order
+  if (rc) return rc;
+  const int ntok = (int)ctx->pf_tok.size();
+  if (ntok > 0) {
+    if (ntok > ctx->pf_cap) return set_err(SART_EINVAL, "prefill batch exceeds its buffer");
+    CK(cudaMemcpyAsync(ctx->d_prompt, ctx->pf_tok.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ctx->d_pf_slot, ctx->pf_slot.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ctx->d_pf_pos, ctx->pf_pos.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaEventRecord(ctx->pf_ev[0], ctx->st));
+    if (ctx->bf16) prefill_batch<bf16>(ctx, ntok);
+    else prefill_batch<float>(ctx, ntok);
+    CK(cudaEventRecord(ctx->pf_ev[1], ctx->st));
+    CK(cudaGetLastError());
+    ctx->pf_pending = true;
+    ctx->pf_tok.clear();
+    ctx->pf_slot.clear();
+    ctx->pf_pos.clear();
+  }
+  return SART_OK;
 }
 
 // ------------------------------------------------------------------ boundary read-back
@@ -513,6 +537,11 @@ int read_boundary(sart_ctx* ctx) {
   CK(cudaMemcpyAsync(ctx->h_ctr, ctx->ctr, sizeof(Ctr) + sizeof(int) * D.S, cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   Ctr& c = *ctx->h_ctr;
+  if (ctx->pf_pending) {   // GPU time of this window's batched prefill
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->pf_ev[0], ctx->pf_ev[1]) == cudaSuccess) ctx->prefill_ms += ms;
+    ctx->pf_pending = false;
+  }
   // the device applied the releases; the host mirror adopts its counters
   ctx->n_rows = c.n_rows;
   ctx->free_top = c.free_top;
@@ -696,6 +725,8 @@ int sart_destroy(sart_ctx* ctx) {
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (auto e : ctx->poll_ev)
     if (e) cudaEventDestroy(e);
+  for (auto e : ctx->pf_ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->step_exec) cudaGraphExecDestroy(ctx->step_exec);
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->wblob) cudaFree(ctx->wblob);
@@ -748,7 +779,7 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   D.max_pos = cfg.max_prompt + D.cap;
   D.theta = cfg.rope_theta; D.eps = cfg.rms_eps; D.tau = cfg.temperature; D.seed = cfg.sampler_seed;
   D.select_mode = cfg.select_mode;
-  ctx->PC = 256;
+  ctx->PC = 2048;   // prefill chunk (tokens)
   ctx->W = std::max(D.R, ctx->PC);
   const size_t es = ctx->bf16 ? 2 : 4;
 
@@ -858,7 +889,12 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   IC(dalloc(ctx, &ctx->sv, (size_t)D.R * sample_chunks(D.V) * 4));
   IC(dalloc(ctx, &ctx->dbg_slot, (size_t)D.R * 4));
   IC(dalloc(ctx, &ctx->dbg_b, (size_t)D.R * 4));
-  IC(dalloc(ctx, &ctx->d_prompt, (size_t)cfg.max_prompt * 4));
+  ctx->pf_cap = (int)std::min<long long>((long long)D.S * cfg.max_prompt, 1LL << 24);
+  IC(dalloc(ctx, &ctx->d_prompt, (size_t)ctx->pf_cap * 4));
+  IC(dalloc(ctx, &ctx->d_pf_slot, (size_t)ctx->pf_cap * 4));
+  IC(dalloc(ctx, &ctx->d_pf_pos, (size_t)ctx->pf_cap * 4));
+  IC(cudaEventCreate(&ctx->pf_ev[0]));
+  IC(cudaEventCreate(&ctx->pf_ev[1]));
   ctx->ev_cap = D.R + D.S + 64;
   IC(dalloc(ctx, &ctx->d_events, sizeof(AdmitEvent) * ctx->ev_cap));
   if (cfg.debug_capture) IC(dalloc(ctx, &ctx->dbg_attn, (size_t)D.L * D.R * D.qh * D.hd * 4));
