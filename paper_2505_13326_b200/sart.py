@@ -232,13 +232,16 @@ class Engine:
         if sc is not None or forced_tokens is not None:
             s = SartScript()
             if sc is not None:
-                if forced_len:
+                if forced_len and sc.forced_len is not None:
                     fl = _i32(sc.forced_len); keep.append(fl); s.forced_len = fl.ctypes.data_as(P32)
                 if use_script_scores:
-                    scores = np.ascontiguousarray(sc.scores, np.float32); keep.append(scores)
-                    fin = np.ascontiguousarray(sc.final_score, np.float32); keep.append(fin)
-                    s.scores, s.final_score = scores.ctypes.data_as(PF), fin.ctypes.data_as(PF)
-                    s.n_bnd = scores.shape[1]
+                    if sc.scores is not None:
+                        scores = np.ascontiguousarray(sc.scores, np.float32); keep.append(scores)
+                        s.scores = scores.ctypes.data_as(PF)
+                        s.n_bnd = scores.shape[1]
+                    if sc.final_score is not None:
+                        fin = np.ascontiguousarray(sc.final_score, np.float32); keep.append(fin)
+                        s.final_score = fin.ctypes.data_as(PF)
                 if use_answers and sc.answer is not None:
                     an = _i32(sc.answer); keep.append(an); s.answer = an.ctypes.data_as(P32)
             if forced_tokens is not None:
