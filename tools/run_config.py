@@ -1,0 +1,89 @@
+"""Run one BASELINE.json configuration on one GPU and print a JSON line.
+
+    python tools/run_config.py --config c3 --windows 4 --warmup 2
+
+c1: tiny decoder, 1 request, N=4, M=2, cap 64, T=16, alpha 0.5, beta 2 (BJ configs[0])
+c3: 7B shape, 32 requests/GPU (the per-GPU share of 256 on 8 GPUs), N=16, M=4, cap 8192,
+    T=400, alpha 0.5, beta 8, scripted rewards (BJ configs[2]); admission is commitment-limited
+c5: 14B shape, 8192-token shared prompt, N=32, M=16, alpha 0.5, beta 16, cap 16384, T=400,
+    1 request per GPU (BJ configs[4])
+Values: branch-tokens/s over the timed windows (CUDA events), attention roofline over one
+extra eager window (same method as bench.py).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+CONFIGS = {
+    "c1": dict(shape="tiny", n_req=1, N=4, M=2, alpha=0.5, beta=2, cap=64, T=16, p=(16, 16), B=64, bs=16),
+    "c3": dict(shape="7B", n_req=32, N=16, M=4, alpha=0.5, beta=8, cap=8192, T=400, p=(64, 1024), B=1024, bs=64),
+    "c5": dict(shape="14B", n_req=1, N=32, M=16, alpha=0.5, beta=16, cap=16384, T=400, p=(8193, 8193), B=64, bs=64),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--windows", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=2)
+    a = ap.parse_args()
+    import torch
+    from paper_2505_13326_b200 import Engine
+    from synth import SHAPES, gen_requests
+    c = CONFIGS[a.config]
+    shape = SHAPES[c["shape"]]
+    stream = torch.cuda.current_stream()
+    t0 = time.time()
+    eng = Engine(shape, "bf16", weight_seed=3, block_size=c["bs"], num_blocks=0, max_rows=c["B"], max_requests=256,
+                 max_prompt=c["p"][1] + 1, T=c["T"], cap=c["cap"], eos_id=1, temperature=1.0, sampler_seed=5,
+                 stream=stream.cuda_stream)
+    init_s = time.time() - t0
+    reqs = gen_requests(c["n_req"], shape, c["N"], c["M"], c["alpha"], c["beta"], c["cap"], c["T"], eos_id=1,
+                        p_range=c["p"])
+    for r in reqs:
+        eng.admit(r)
+    if a.config == "c1":      # latency config: time the whole request (no warm-up)
+        a.warmup, a.windows = 0, 1000
+    t0 = time.time()
+    eng.step(a.warmup)
+    torch.cuda.synchronize()
+    warm_s = time.time() - t0
+    s0, p0 = eng.step(0), eng.profile()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    eng.step(a.windows)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    s1, p1 = eng.step(0), eng.profile()
+    eng.set_profile(True)
+    q0 = eng.profile()
+    eng.step(1)
+    torch.cuda.synchronize()
+    q1 = eng.profile()
+    eng.set_profile(False)
+    att_ms, att_b = q1["attn_ms"] - q0["attn_ms"], q1["attn_bytes"] - q0["attn_bytes"]
+    st = eng.step(0)
+    out = {"config": a.config, "shape": c["shape"], "windows_timed": s1["windows"] - s0["windows"],
+           "decode_steps": s1["steps"] - s0["steps"],
+           "branch_tokens_per_s": (s1["branch_tokens"] - s0["branch_tokens"]) / (ms / 1e3),
+           "requests_finalized": s1["finalized_total"] - s0["finalized_total"], "ms_timed": ms,
+           "ms_per_decode_step": ms / max(1, s1["steps"] - s0["steps"]),
+           "us_per_decode_step": 1e3 * ms / max(1, s1["steps"] - s0["steps"]),
+           "prefill_ms_timed": p1["prefill_ms"] - p0["prefill_ms"],
+           "live_rows_end": st["live_rows"], "queued_requests_end": st["queued_requests"],
+           "free_blocks": st["free_blocks"], "committed_blocks": st["committed_blocks"],
+           "attn_GBps": att_b / (att_ms / 1e3) / 1e9 if att_ms else None,
+           "attn_frac_of_6455": att_b / (att_ms / 1e3) / 1e9 / 6455.3 if att_ms else None,
+           "attn_ms_per_launch": att_ms / max(1, q1["attn_launches"] - q0["attn_launches"]),
+           "init_s": init_s, "warmup_s": warm_s}
+    print(json.dumps(out), flush=True)
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()
