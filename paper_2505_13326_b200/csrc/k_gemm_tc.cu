@@ -448,14 +448,16 @@ bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const Qk
 
 // Split choice for the decode GEMMs: enough (tile x split) units to cover the SMs.
 void choose_split(int M, int N, int K, int& S, int& BN) {
+  // measured on B200 at M = 512 (tools/gemm_sweep.py): long-K projections prefer 256-wide
+  // tiles with more splits, short-K ones 128-wide tiles; aim for ~one unit per SM
   if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
   const int mt = (M + BM - 1) / BM;
+  const int kb = (K + BK - 1) / BK;
   const int t256 = mt * ((N + 255) / 256);
   if (t256 >= g_num_sms * 3 / 4) { S = 1; BN = 256; return; }
-  BN = 128;
-  const int t128 = mt * ((N + 127) / 128);
-  const int kb = (K + BK - 1) / BK;
-  S = (g_num_sms + t128 / 2) / t128;
+  BN = K >= 4096 ? 256 : 128;
+  const int t = mt * ((N + BN - 1) / BN);
+  S = (g_num_sms + t / 2) / t;
   if (S < 1) S = 1;
   if (S > 8) S = 8;
   if (S > kb / 2) S = kb / 2 > 0 ? kb / 2 : 1;

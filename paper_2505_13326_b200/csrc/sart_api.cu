@@ -1202,6 +1202,22 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
     if (!launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, 0)) e = cudaErrorInvalidValue;
     chk(cudaGetLastError());
     chk(cudaDeviceSynchronize());
+    if (const char* reps_s = getenv("SART_GEMM_BENCH_REPS")) {   // micro-benchmark (tools/gemm_sweep.py)
+      const int reps = atoi(reps_s);
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, 0);
+      for (int i = 0; i < reps; ++i) launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, 0);
+      cudaEventRecord(b, 0);
+      cudaEventSynchronize(b);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, a, b);
+      fprintf(stderr, "GEMMBENCH M=%d N=%d K=%d mode=%d S=%d BN=%d us=%.2f TFLOPs=%.1f\n", M, N, K, mode, splits, bn,
+              1e3 * ms / reps, 2.0 * M * N * K / (ms / reps * 1e-3) / 1e12);
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
     if (mode == GEMM_SWIGLU) {
       std::vector<uint16_t> h(outn);
       chk(cudaMemcpy(h.data(), dact, 2 * outn, cudaMemcpyDeviceToHost));

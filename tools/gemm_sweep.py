@@ -1,0 +1,24 @@
+"""Sweep split-K / tile width of the tcgen05 GEMM on the C2 decode shapes (M = 512 rows)."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("SART_GEMM_BENCH_REPS", "200")
+from paper_2505_13326_b200.sart import debug_gemm  # noqa: E402
+
+rng = np.random.default_rng(0)
+shapes = {"o": (512, 1536, 1536), "down": (512, 1536, 8960), "qkv": (512, 2048, 1536), "gateup": (512, 17920, 1536)}
+for name, (M, N, K) in shapes.items():
+    A = rng.integers(0, 1 << 14, size=(M, K), dtype=np.uint16)
+    B = rng.integers(0, 1 << 14, size=(N, K), dtype=np.uint16)
+    for bn in (128, 256):
+        for S in (1, 2, 3, 4, 6, 8):
+            if name == "gateup" and S > 1:
+                continue
+            print(name, flush=True)
+            try:
+                debug_gemm(A, B, mode=0, splits=S, bn=bn)
+            except Exception as e:
+                print("fail", e)
