@@ -395,6 +395,159 @@ __global__ void __launch_bounds__(256) k_attn_merge(const float* __restrict__ pa
     for (int c = 0; c < C; ++c) dbg[oi + c] = acc[c] * inv;
 }
 
+// ------------------------------------------------------------------ causal prefill (f1)
+// Prompt positions of a batched prefill (Alg. 1 L15): CTA = (64-position query block of one
+// request, q head); 4 warps x 16 query rows; K/V of key positions [64 kb, 64 kb + 64) staged
+// through a 2-stage bulk-copy ring; the last key block is masked causally.
+template <int HD>
+__global__ void __launch_bounds__(128) k_attn_prefill_tc(const bf16* __restrict__ q, const bf16* __restrict__ pool,
+                                                         bf16* __restrict__ out, Dims D, int layer, Reqs reqs,
+                                                         const int4* __restrict__ blocks) {
+  constexpr int KT = 64;                                   // key tokens per stage
+  extern __shared__ __align__(128) uint8_t praw[];
+  bf16 (*ks)[KT * HD] = reinterpret_cast<bf16 (*)[KT * HD]>(praw);
+  bf16 (*vs)[KT * HD] = reinterpret_cast<bf16 (*)[KT * HD]>(praw + 2 * KT * HD * sizeof(bf16));
+  uint64_t* full = reinterpret_cast<uint64_t*>(praw + 4 * KT * HD * sizeof(bf16));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4 blk = blocks[blockIdx.x];                     // {first batch row, rows, slot, first position}
+  const int head = blockIdx.y, h = head / D.g;
+  const int r0 = blk.x, nr = blk.y, slot = blk.z, p0 = blk.w;
+  const int nkey = p0 + nr;                                // keys 0 .. p0 + nr - 1
+  const int nkb = (nkey + KT - 1) / KT;
+  const int* ptab = reqs.prefix + (long long)slot * D.MPB;
+  const float sl2 = 1.4426950408889634f * rsqrtf((float)HD);
+  if (threadIdx.x == 0) {
+    mb_init(&full[0], 1);
+    mb_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int kb) {
+    const int st = kb & 1;
+    const int t0 = kb * KT, ntok = min(KT, nkey - t0);
+    const int tpb = min(D.bs, KT);
+    const int pieces = (ntok + tpb - 1) / tpb;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mb_expect(&full[st], 2u * pieces * tpb * HD * 2);
+    for (int pc = 0; pc < pieces; ++pc) {
+      const int tok = t0 + pc * tpb;
+      const long long b = ptab[tok / D.bs];
+      const int inb = tok % D.bs;
+      bulk_g2s(s_u32(ks[st] + pc * tpb * HD), pool + kv_tile_off(D, layer, b, 0, h) + (long long)inb * HD,
+               tpb * HD * 2, &full[st]);
+      bulk_g2s(s_u32(vs[st] + pc * tpb * HD), pool + kv_tile_off(D, layer, b, 1, h) + (long long)inb * HD,
+               tpb * HD * 2, &full[st]);
+    }
+  };
+  // stale smem of a partial stage is multiplied by P = 0: keep it finite
+  for (int e = threadIdx.x; e < 4 * KT * HD / 8; e += 128) reinterpret_cast<uint4*>(praw)[e] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    issue(0);
+    if (nkb > 1) issue(1);
+  }
+  // Q fragments of this warp's 16 rows (zero beyond nr)
+  const int qr0 = warp * 16 + (lane >> 2), qr1 = qr0 + 8, cc = 2 * (lane & 3);
+  const bf16* q0 = qr0 < nr ? q + ((long long)(r0 + qr0) * D.qh + head) * HD : nullptr;
+  const bf16* q1 = qr1 < nr ? q + ((long long)(r0 + qr1) * D.qh + head) * HD : nullptr;
+  uint32_t qa[HD / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < HD / 16; ++kk) {
+    qa[kk][0] = q0 ? *reinterpret_cast<const uint32_t*>(q0 + 16 * kk + cc) : 0u;
+    qa[kk][1] = q1 ? *reinterpret_cast<const uint32_t*>(q1 + 16 * kk + cc) : 0u;
+    qa[kk][2] = q0 ? *reinterpret_cast<const uint32_t*>(q0 + 16 * kk + 8 + cc) : 0u;
+    qa[kk][3] = q1 ? *reinterpret_cast<const uint32_t*>(q1 + 16 * kk + 8 + cc) : 0u;
+  }
+  const int pos0 = p0 + qr0, pos1 = p0 + qr1;              // query positions (causal limits)
+  float o[HD / 8][4];
+#pragma unroll
+  for (int nt = 0; nt < HD / 8; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int st = kb & 1;
+    mb_wait(&full[st], (kb >> 1) & 1);
+    const uint32_t kbase = s_u32(ks[st]), vbase = s_u32(vs[st]);
+    const int t0 = kb * KT;
+    if (t0 <= p0 + warp * 16 + 15) {                       // some key of this block is visible to the warp
+#pragma unroll 1
+      for (int sub = 0; sub < KT; sub += 16) {
+        if (t0 + sub > p0 + warp * 16 + 15) break;
+        float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const int mi = lane >> 3;
+          const int tok = sub + (lane & 7) + 8 * (mi >> 1);
+          const int ch = 2 * kk + (mi & 1);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(kbase + tok * (HD * 2) + ((ch ^ (tok & 7)) << 4), b0, b1, b2, b3);
+          mma16816(s[0], qa[kk], b0, b1);
+          mma16816(s[1], qa[kk], b2, b3);
+        }
+        const int kpos = t0 + sub + 2 * (lane & 3);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int kp = kpos + nt * 8 + (e & 1);
+            if (kp > (e < 2 ? pos0 : pos1)) s[nt][e] = -INFINITY;      // causal (also beyond nkey)
+          }
+        float mx0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
+        float mx1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+        const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
+        const float u0 = n0 == -INFINITY ? 0.f : n0, u1 = n1 == -INFINITY ? 0.f : n1;
+        const float c0 = exp2f((m0 - u0) * sl2), c1 = exp2f((m1 - u1) * sl2);
+        m0 = n0;
+        m1 = n1;
+        float pr[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          pr[nt][0] = exp2f((s[nt][0] - u0) * sl2);
+          pr[nt][1] = exp2f((s[nt][1] - u0) * sl2);
+          pr[nt][2] = exp2f((s[nt][2] - u1) * sl2);
+          pr[nt][3] = exp2f((s[nt][3] - u1) * sl2);
+        }
+        l0 = l0 * c0 + pr[0][0] + pr[0][1] + pr[1][0] + pr[1][1];
+        l1 = l1 * c1 + pr[0][2] + pr[0][3] + pr[1][2] + pr[1][3];
+#pragma unroll
+        for (int nt = 0; nt < HD / 8; ++nt) { o[nt][0] *= c0; o[nt][1] *= c0; o[nt][2] *= c1; o[nt][3] *= c1; }
+        uint32_t pa[4] = {pack_bf16(pr[0][0], pr[0][1]), pack_bf16(pr[0][2], pr[0][3]), pack_bf16(pr[1][0], pr[1][1]),
+                          pack_bf16(pr[1][2], pr[1][3])};
+#pragma unroll
+        for (int dp = 0; dp < HD / 16; ++dp) {
+          const int mi = lane >> 3;
+          const int tok = sub + (lane & 7) + 8 * (mi & 1);
+          const int ch = 2 * dp + (mi >> 1);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(vbase + tok * (HD * 2) + ((ch ^ (tok & 7)) << 4), b0, b1, b2, b3);
+          mma16816(o[2 * dp], pa, b0, b1);
+          mma16816(o[2 * dp + 1], pa, b2, b3);
+        }
+      }
+    }
+    __syncthreads();                                       // every warp is done with this stage
+    if (threadIdx.x == 0 && kb + 2 < nkb) issue(kb + 2);
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int qr = half ? qr1 : qr0;
+    if (qr >= nr) continue;
+    const float inv = 1.0f / (half ? l1 : l0);
+    bf16* dst = out + ((long long)(r0 + qr) * D.qh + head) * HD;
+#pragma unroll
+    for (int nt = 0; nt < HD / 8; ++nt)
+      *reinterpret_cast<__nv_bfloat162*>(dst + nt * 8 + cc) =
+          __floats2bfloat162_rn(o[nt][2 * half] * inv, o[nt][2 * half + 1] * inv);
+  }
+}
+
 // ------------------------------------------------------------------ per-step item list
 // Valid tasks of this step (rows finished mid-window are skipped) with their token ranges,
 // ordered by size, largest first (counting sort on 16-token buckets), so that the dynamic
@@ -540,6 +693,26 @@ __global__ void __launch_bounds__(1024) k_attn_account(Dims D, Rows rows, Reqs r
 
 void launch_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat, cudaStream_t s) {
   k_attn_plan<<<1, 1024, 0, s>>>(D, rows, reqs, pl, n, flat);
+}
+void launch_attn_prefill_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Reqs reqs,
+                            const int4* blocks, int nblocks, cudaStream_t s) {
+  if (nblocks <= 0) return;
+  dim3 grid(nblocks, D.qh);
+  const size_t sm = 4 * 64 * (size_t)D.hd * sizeof(bf16) + 64;
+  static bool a128 = false, a64 = false;
+  if (D.hd == 128) {
+    if (!a128) {
+      cudaFuncSetAttribute(k_attn_prefill_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      a128 = true;
+    }
+    k_attn_prefill_tc<128><<<grid, 128, sm, s>>>(q, pool, out, D, layer, reqs, blocks);
+  } else {
+    if (!a64) {
+      cudaFuncSetAttribute(k_attn_prefill_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      a64 = true;
+    }
+    k_attn_prefill_tc<64><<<grid, 128, sm, s>>>(q, pool, out, D, layer, reqs, blocks);
+  }
 }
 void launch_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s) {
   launch_pdl(k_attn_items, dim3(1), dim3(1024), 0, s, D, rows, reqs, pl);

@@ -98,6 +98,8 @@ struct sart_ctx {
   int *d_pf_slot = nullptr, *d_pf_pos = nullptr;
   int pf_cap = 0;
   std::vector<int> pf_tok, pf_slot, pf_pos;
+  std::vector<int> pf_slot_h, pf_pos_h;   // host copies used to build the query blocks
+  int4* d_pf_blocks = nullptr;
   cudaEvent_t pf_ev[2] = {nullptr, nullptr};
   bool pf_pending = false;
   AdmitEvent* d_events = nullptr;
@@ -366,6 +368,20 @@ void prefill_batch(sart_ctx* ctx, int ntok) {
   for (int t0 = 0; t0 < ntok; t0 += ctx->PC) {
     const int c = std::min(ctx->PC, ntok - t0);
     const RopeArgs ra{ctx->d_pf_slot + t0, ctx->d_pf_pos + t0};
+    // 64-position query blocks of each request segment of this chunk (tensor-core prefill)
+    int nqb = 0;
+    if constexpr (std::is_same<T, bf16>::value) {
+      std::vector<int4> qb;
+      for (int i = 0; i < c;) {
+        const int slot = ctx->pf_slot_h[t0 + i];
+        int j = i;
+        while (j < c && ctx->pf_slot_h[t0 + j] == slot && j - i < 64) ++j;
+        qb.push_back(make_int4(i, j - i, slot, ctx->pf_pos_h[t0 + i]));
+        i = j;
+      }
+      nqb = (int)qb.size();
+      cudaMemcpyAsync(ctx->d_pf_blocks, qb.data(), sizeof(int4) * qb.size(), cudaMemcpyHostToDevice, s);
+    }
     launch_embed<T>(ctx->d_prompt + t0, ctx->W_<T>(t_embed()), ctx->h, c, D.d, s);
     ctx->launches++;
     int np_res = 0;
@@ -374,7 +390,11 @@ void prefill_batch(sart_ctx* ctx, int ntok) {
                         D.eps, s);
       qkv_rope<T>(ctx, l, c, ra);
       if (l == D.L - 1) break;
-      launch_attn_prefill<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, D, l, ctx->reqs, ra.pf_slot, ra.pf_pos, c, s);
+      if constexpr (std::is_same<T, bf16>::value)
+        launch_attn_prefill_tc((bf16*)ctx->q, (bf16*)ctx->pool, (bf16*)ctx->o, D, l, ctx->reqs, ctx->d_pf_blocks, nqb,
+                               s);
+      else
+        launch_attn_prefill<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, D, l, ctx->reqs, ra.pf_slot, ra.pf_pos, c, s);
       int np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), c, D.d, D.qh * D.hd);
       launch_rmsnorm<T>(ctx->h, ctx->parts, np, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, c, D.d,
                         D.eps, s);
@@ -519,6 +539,8 @@ int fill(sart_ctx* ctx) {
     CK(cudaMemcpyAsync(ctx->d_pf_slot, ctx->pf_slot.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
     CK(cudaMemcpyAsync(ctx->d_pf_pos, ctx->pf_pos.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
     CK(cudaEventRecord(ctx->pf_ev[0], ctx->st));
+    ctx->pf_slot_h.swap(ctx->pf_slot);
+    ctx->pf_pos_h.swap(ctx->pf_pos);
     if (ctx->bf16) prefill_batch<bf16>(ctx, ntok);
     else prefill_batch<float>(ctx, ntok);
     CK(cudaEventRecord(ctx->pf_ev[1], ctx->st));
@@ -893,6 +915,7 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   IC(dalloc(ctx, &ctx->d_prompt, (size_t)ctx->pf_cap * 4));
   IC(dalloc(ctx, &ctx->d_pf_slot, (size_t)ctx->pf_cap * 4));
   IC(dalloc(ctx, &ctx->d_pf_pos, (size_t)ctx->pf_cap * 4));
+  IC(dalloc(ctx, &ctx->d_pf_blocks, sizeof(int4) * (size_t)(ctx->PC / 64 + D.S + 8)));
   IC(cudaEventCreate(&ctx->pf_ev[0]));
   IC(cudaEventCreate(&ctx->pf_ev[1]));
   ctx->ev_cap = D.R + D.S + 64;
