@@ -428,6 +428,10 @@ bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float
   if (K % 8) return false;   // TMA row stride must be a multiple of 16 bytes
   const int kb = (K + BK - 1) / BK;
   if (S < 1 || S > kb || (mode == GEMM_SWIGLU && S != 1)) return false;
+  if (BN == 64) {
+    if (mode == GEMM_STORE) return launch_bn<64, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s);
+    return false;
+  }
   if (BN == 128) {
     if (mode == GEMM_STORE) return launch_bn<128, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s);
     if (mode == GEMM_ACCUM) return launch_bn<128, GEMM_ACCUM>(A, B, bias, C, act, M, N, K, S, s);

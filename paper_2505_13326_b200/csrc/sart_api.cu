@@ -923,7 +923,8 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   if (cfg.debug_capture) IC(dalloc(ctx, &ctx->dbg_attn, (size_t)D.L * D.R * D.qh * D.hd * 4));
   {  // cascade attention plan and partial outputs
     AttnPlan& pl = ctx->plan;
-    pl.CH = 512;
+    pl.CH = 512;   // tokens per attention chunk (SART_ATTN_CH overrides; multiple of 64)
+    if (const char* e = getenv("SART_ATTN_CH")) pl.CH = std::max(64, atoi(e) / 64 * 64);
     pl.qr_max = std::max(1, std::min(SART_MAXN, 64 / D.g));
     pl.npc_max = std::max(1, cdiv(cfg.max_prompt - 1, pl.CH));
     const int nsc_max = cdiv(D.cap, pl.CH);
@@ -1205,7 +1206,7 @@ int sart_debug_fetch(sart_ctx* ctx, int32_t what, int32_t layer, void* host_out,
 int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const uint16_t* B, const float* bias,
                     float* C, int32_t mode, int32_t splits, int32_t bn) {
   if (M < 1 || N < 1 || K < 1 || !A || !B || !C || mode < 0 || mode > 2 || splits < 1 || splits > 8 ||
-      (bn != 128 && bn != 256))
+      (bn != 64 && bn != 128 && bn != 256))
     return set_err(SART_EINVAL, "bad args");
   bf16 *dA = nullptr, *dB = nullptr, *dact = nullptr;
   float *dC = nullptr, *dbias = nullptr;

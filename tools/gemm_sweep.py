@@ -9,12 +9,18 @@ os.environ.setdefault("SART_GEMM_BENCH_REPS", "200")
 from paper_2505_13326_b200.sart import debug_gemm  # noqa: E402
 
 rng = np.random.default_rng(0)
-shapes = {"o": (512, 1536, 1536), "down": (512, 1536, 8960), "qkv": (512, 2048, 1536), "gateup": (512, 17920, 1536)}
+shapes = {"empty1": (128, 128, 64), "empty148": (512, 4736, 64), "o": (512, 1536, 1536), "down": (512, 1536, 8960),
+          "qkv": (512, 2048, 1536), "gateup": (512, 17920, 1536)}
+only = sys.argv[1:] or list(shapes)
 for name, (M, N, K) in shapes.items():
+    if name not in only:
+        continue
     A = rng.integers(0, 1 << 14, size=(M, K), dtype=np.uint16)
     B = rng.integers(0, 1 << 14, size=(N, K), dtype=np.uint16)
-    for bn in (128, 256):
+    for bn in (64, 128, 256):
         for S in (1, 2, 3, 4, 6, 8):
+            if S > max(1, K // 128):
+                continue
             if name == "gateup" and S > 1:
                 continue
             print(name, flush=True)
