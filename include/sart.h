@@ -253,9 +253,11 @@ int sart_debug_fetch(sart_ctx* ctx, int32_t what, int32_t layer, void* host_out,
  * buffers.  mode 0: store, 1: accumulate into C (C is read), 2: SwiGLU on gate/up rows
  * interleaved in 256-row tiles; C receives M x N/2 values (bf16 rounded).
  * splits (1..8): split-K, C receives splits x M x N partial products (caller sums);
- * bn: output tile width 128 or 256 (SwiGLU needs 256 and splits = 1). */
+ * bn: output tile width 64, 128 or 256 (SwiGLU needs 256 and splits = 1; 64: store only);
+ * bm: output tile height 128 or 256 (256: two 128-row tensor-core tiles share each weight
+ * stage; store with bn 128/256, SwiGLU with bn 256).  Unsupported combinations: SART_EINVAL. */
 int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const uint16_t* B, const float* bias,
-                    float* C, int32_t mode, int32_t splits, int32_t bn);
+                    float* C, int32_t mode, int32_t splits, int32_t bn, int32_t bm);
 
 typedef struct {
   double attn_ms;          /* sum of attention-kernel durations (CUDA events)    */

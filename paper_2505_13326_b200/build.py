@@ -12,7 +12,7 @@ LIB = os.path.join(HERE, "libsart.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--extended-lambda", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
-         "-cudart", "static"]
+         "-cudart", "static"] + os.environ.get("SART_NVCC_EXTRA", "").split()
 
 
 def sources():

@@ -22,8 +22,13 @@
 
 namespace {
 constexpr int BM = 128, BK = 64;
-// pipeline depth: ~192 KB of A+B stages in flight per SM whatever the tile width
-template <int BN> struct Stages { static constexpr int value = (192 * 1024) / ((BM + BN) * BK * 2); };
+// pipeline depth: ~192 KB of A+B stages in flight per SM whatever the tile shape
+template <int BN, int MS> struct Stages { static constexpr int value = (192 * 1024) / ((MS * BM + BN) * BK * 2); };
+// TMEM accumulators: MS m-subtiles x BN columns, double-buffered when that fits in 512 columns
+template <int BN, int MS> struct Tmem {
+  static constexpr int NBUF = 2 * MS * BN <= 512 ? 2 : 1;
+  static constexpr int COLS = NBUF * MS * BN;
+};
 constexpr int NTHREADS = 192;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -90,33 +95,51 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int BN>
+template <int BN, int MS>
 struct Smem {
-  static constexpr int STAGES = Stages<BN>::value;
-  alignas(1024) bf16 a[STAGES][BM * BK];
+  static constexpr int STAGES = Stages<BN, MS>::value;
+  alignas(1024) bf16 a[STAGES][MS * BM * BK];
   alignas(1024) bf16 b[STAGES][BN * BK];
   uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   uint32_t tmem_base;
-  float slab[4][32][33];   // per epilogue warp: 32 rows x 32 cols, padded (coalesced stores)
 };
 
+// MS m-subtiles of 128 rows share each B stage (tile = MS*128 x BN): per-SM operand traffic
+// per flop falls from (128 + BN) / (128 BN) to (MS 128 + BN) / (MS 128 BN) -- the decode GEMMs are
+// bound by L2 -> SM operand delivery, not by the tensor pipe (profiles/r1_gemm_ncu.txt).
 // MODE: GEMM_STORE (C = AB^T + bias), GEMM_ACCUM (C += AB^T), GEMM_SWIGLU (columns of each
 // BN tile are [gate(BN/2) | up(BN/2)] of interleaved weights; writes bf16 act[m][F]).
 // Split-K: work unit u -> (m-tile = u % mt, split, n-tile); split s covers k-blocks
 // [s*kb/S, (s+1)*kb/S) and writes its fp32 partial tile to C + s*M*N.  The consumer kernel
 // (RMSNorm / RoPE) sums the S partials in split order, so the result is deterministic.
-template <int BN, int MODE>
+}  // namespace
+__device__ unsigned long long g_gemm_ts[4][10];
+__device__ int g_gemm_ts_idx;
+namespace {
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+template <int BN, int MODE, int MS>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* C,
               const float* __restrict__ bias, bf16* act, int M, int N, int K, int S, const __grid_constant__ QkvEpi epi) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  Smem<BN>& sm = *reinterpret_cast<Smem<BN>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int STAGES = Smem<BN>::STAGES;
+  // epilogue staging, per epilogue warp 32 rows x 32 cols padded: a static __shared__ array so
+  // that the compiler emits STS/LDS (a pointer into the aligned dynamic buffer decays to
+  // generic LD/ST, which it cannot reorder around the global stores)
+  __shared__ __align__(16) float slab_s[4][32 * 32];
+  Smem<BN, MS>& sm =
+      *reinterpret_cast<Smem<BN, MS>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int STAGES = Smem<BN, MS>::STAGES;
+  constexpr int NBUF = Tmem<BN, MS>::NBUF, TCOLS = Tmem<BN, MS>::COLS;
+  constexpr uint32_t STAGE_TX = (MS * BM + BN) * BK * 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN, ntiles = mt * nt * S;
+  const int mt = (M + MS * BM - 1) / (MS * BM), nt = (N + BN - 1) / BN, ntiles = mt * nt * S;
   const int kb_all = (K + BK - 1) / BK;
   auto unit_of = [&](int t, int& m0, int& n0, int& kb0, int& kb1, int& sp) {
-    m0 = (t % mt) * BM;
+    m0 = (t % mt) * (MS * BM);
     const int rest = t / mt;
     sp = rest % S;
     n0 = (rest / S) * BN;
@@ -124,20 +147,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     kb1 = (sp + 1) * kb_all / S;
   };
 
+#ifdef SART_GEMM_TS   // phase timestamps of CTA 0 (build with -DSART_GEMM_TS; SART_GEMM_TS=1 prints them)
+  __shared__ int ts_slot;
+  const bool tsb = blockIdx.x == 0;
+  if (threadIdx.x == 0 && tsb) { ts_slot = atomicAdd(&g_gemm_ts_idx, 1) & 3; g_gemm_ts[ts_slot][0] = gtime(); }
+#define TS(i) if (tsb) g_gemm_ts[ts_slot][i] = gtime()
+#else
+#define TS(i) do {} while (0)
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&sm.tfull[s], 1); mbar_init(&sm.tempty[s], 4); }
+    for (int s = 0; s < NBUF; ++s) { mbar_init(&sm.tfull[s], 1); mbar_init(&sm.tempty[s], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
-                 "r"(2 * BN));
+                 "r"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = sm.tmem_base;
+  if (threadIdx.x == 0) { TS(1); }
   if (threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0) {
@@ -157,19 +189,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           first = false;
           const int pre = min(STAGES, kb1 - kb0);
           for (int i = 0; i < pre; ++i) {
-            mbar_expect_tx(&sm.full[i], (BM + BN) * BK * 2);
+            mbar_expect_tx(&sm.full[i], STAGE_TX);
             tma_load_2d(sm.b[i], &tmB, &sm.full[i], (kb0 + i) * BK, n0);
           }
           pdl_wait();
-          for (int i = 0; i < pre; ++i) tma_load_2d(sm.a[i], &tmA, &sm.full[i], (kb0 + i) * BK, m0);
+          TS(2);
+          for (int i = 0; i < pre; ++i)
+#pragma unroll
+            for (int j = 0; j < MS; ++j)
+              tma_load_2d(sm.a[i] + j * BM * BK, &tmA, &sm.full[i], (kb0 + i) * BK, m0 + j * BM);
           kb += pre;
           stage = pre % STAGES;
           phase = pre == STAGES ? 1 : 0;
         }
         for (; kb < kb1; ++kb) {
           mbar_wait(&sm.empty[stage], phase ^ 1);
-          mbar_expect_tx(&sm.full[stage], (BM + BN) * BK * 2);
-          tma_load_2d(sm.a[stage], &tmA, &sm.full[stage], kb * BK, m0);
+          mbar_expect_tx(&sm.full[stage], STAGE_TX);
+#pragma unroll
+          for (int j = 0; j < MS; ++j) tma_load_2d(sm.a[stage] + j * BM * BK, &tmA, &sm.full[stage], kb * BK, m0 + j * BM);
           tma_load_2d(sm.b[stage], &tmB, &sm.full[stage], kb * BK, n0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -183,23 +220,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint32_t phase = 0;
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const int as = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
+      const int as = it % NBUF;
+      const uint32_t aph = (it / NBUF) & 1;
       int m0, n0, kb0, kb1, sp;
       unit_of(t, m0, n0, kb0, kb1, sp);
       mbar_wait(&sm.tempty[as], aph ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t d = tmem + as * BN;
+      const uint32_t d = tmem + as * MS * BN;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&sm.full[stage], phase);
         asm volatile("tcgen05.fence::after_thread_sync;");
+        if (lane == 0 && it == 0 && kb == kb0) { TS(3); }
         if (lane == 0) {
           const uint32_t a0 = smem_u32(sm.a[stage]), b0 = smem_u32(sm.b[stage]);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d, umma_desc(a0 + k * 32), umma_desc(b0 + k * 32), idesc, (kb > kb0 || k) ? 1u : 0u);
+#pragma unroll
+            for (int j = 0; j < MS; ++j)
+              umma_bf16(d + j * BN, umma_desc(a0 + j * BM * BK * 2 + k * 32), umma_desc(b0 + k * 32), idesc,
+                        (kb > kb0 || k) ? 1u : 0u);
           umma_commit(&sm.empty[stage]);
           if (kb == kb1 - 1) umma_commit(&sm.tfull[as]);
+          if (kb == kb1 - 1 && it == 0) { TS(4); }
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -212,15 +254,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int row = q * 32 + lane;
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const int as = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
-      int m0, n0, kb0, kb1, sp;
-      unit_of(t, m0, n0, kb0, kb1, sp);
+      const int as = it % NBUF;
+      const uint32_t aph = (it / NBUF) & 1;
+      int m0_, n0, kb0, kb1, sp;
+      unit_of(t, m0_, n0, kb0, kb1, sp);
       float* Cs = C + (size_t)sp * M * N;
       mbar_wait(&sm.tfull[as], aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
+      if (warp == 2 && lane == 0 && it == 0) { TS(5); }
+#pragma unroll 1
+      for (int ms = 0; ms < MS; ++ms) {
+      const int m0 = m0_ + ms * BM;
       const int gm = m0 + row;
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + as * BN;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (as * MS + ms) * BN;
       if (MODE == GEMM_QKV) {
         // tile = one head (BN == head_dim): q / k heads are rotated (pairs i, i + hd/2), k and v
         // are appended to the paged pool at the row's slot (common.cuh layout and swizzle)
@@ -254,16 +300,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tmem_ld32(tbase + HALF + c, x2);
           if (gm < M) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              float a = x1[j] + epi.bias[n0 + c + j], b = x2[j] + epi.bias[n0 + HALF + c + j];
-              if (rot) {
-                const float co = cs[c + j], sn = cs[HALF + c + j];
-                const float y1 = a * co - b * sn, y2 = b * co + a * sn;
-                a = y1;
-                b = y2;
+            for (int j = 0; j < 32; ++j) { x1[j] += epi.bias[n0 + c + j]; x2[j] += epi.bias[n0 + HALF + c + j]; }
+            if (rot) {
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                const float4 co = *reinterpret_cast<const float4*>(cs + c + 4 * j4);
+                const float4 sn = *reinterpret_cast<const float4*>(cs + HALF + c + 4 * j4);
+                const float cv[4] = {co.x, co.y, co.z, co.w}, sv[4] = {sn.x, sn.y, sn.z, sn.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int j = 4 * j4 + e;
+                  const float a = x1[j], b = x2[j];
+                  x1[j] = a * cv[e] - b * sv[e];
+                  x2[j] = b * cv[e] + a * sv[e];
+                }
               }
-              x1[j] = a;
-              x2[j] = b;
             }
             if (head < D.qh) {
               bf16* qd = epi.qout + ((long long)gm * D.qh + head) * BN;
@@ -307,7 +358,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                   float x = g[j + e];
-                  o[e] = __float2bfloat16_rn(x / (1.0f + __expf(-x)) * u[j + e]);
+                  o[e] = __float2bfloat16_rn(__fdividef(x, 1.0f + __expf(-x)) * u[j + e]);
                 }
                 *reinterpret_cast<uint4*>(dst + j) = *reinterpret_cast<uint4*>(o);
               }
@@ -315,43 +366,88 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
       } else {
-        // fp32 output: stage each 32 x 32 slab in shared memory, then store row by row so
-        // that every warp store instruction writes one full 128-byte line
-        float (*slab)[33] = sm.slab[q];
+        // fp32 output: each lane holds one row of a 32 x 32 chunk; transpose it through a
+        // 16-byte-swizzled shared slab (chunk k of row r at k ^ (r & 7): conflict-free both ways)
+        // so that each 16-byte store instruction writes 4 full 128-byte lines
+        float* slab = slab_s[q];
         const int mrow0 = m0 + q * 32;
+        const int kk = lane & 7, r4 = lane >> 3;
+        const bool vec = (N & 3) == 0;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           float v[32];
           tmem_ld32(tbase + c, v);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) slab[lane][j] = v[j];
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<float4*>(slab + lane * 32 + ((k ^ (lane & 7)) << 2)) =
+                make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
           __syncwarp();
-          const int gn = n0 + c + lane;
-          const float bv = (bias && gn < N) ? bias[gn] : 0.f;
-#pragma unroll 4
-          for (int rr = 0; rr < 32; ++rr) {
-            const int gm2 = mrow0 + rr;
-            if (gm2 < M && gn < N) {
-              float* dst = Cs + (size_t)gm2 * N + gn;
-              const float x = slab[rr][lane] + bv;
-              *dst = MODE == GEMM_ACCUM ? *dst + x : x;
+          const int gn = n0 + c + kk * 4;
+          float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (bias) {
+            if (vec && gn + 4 <= N) bv = *reinterpret_cast<const float4*>(bias + gn);
+            else {
+              if (gn < N) bv.x = bias[gn];
+              if (gn + 1 < N) bv.y = bias[gn + 1];
+              if (gn + 2 < N) bv.z = bias[gn + 2];
+              if (gn + 3 < N) bv.w = bias[gn + 3];
             }
           }
+          float4 x[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = i * 4 + r4;
+            x[i] = *reinterpret_cast<const float4*>(slab + rr * 32 + ((kk ^ (rr & 7)) << 2));
+            x[i].x += bv.x; x[i].y += bv.y; x[i].z += bv.z; x[i].w += bv.w;
+          }
           __syncwarp();
+          float* dst = Cs + (size_t)(mrow0 + r4) * N + gn;
+          if (vec && gn + 4 <= N) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (mrow0 + i * 4 + r4 < M) {
+                float4* d4 = reinterpret_cast<float4*>(dst + (size_t)i * 4 * N);
+                if (MODE == GEMM_ACCUM) {
+                  const float4 o = *d4;
+                  x[i].x += o.x; x[i].y += o.y; x[i].z += o.z; x[i].w += o.w;
+                }
+                *d4 = x[i];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (mrow0 + i * 4 + r4 < M) {
+                float* d = dst + (size_t)i * 4 * N;
+                const float xs[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (gn + e < N) d[e] = MODE == GEMM_ACCUM ? d[e] + xs[e] : xs[e];
+              }
+            }
+          }
         }
       }
+      }  // m-subtile
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
+      if (warp == 2 && lane == 0 && it == 0) { TS(6); }
       if (lane == 0) mbar_arrive(&sm.tempty[as]);
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) { TS(7); }
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+    if (lane == 0) { TS(8); }
   }
 }
 
+}  // namespace
+void gemm_ts_reset() { int z = 0; cudaMemcpyToSymbol(g_gemm_ts_idx, &z, 4); }
+void gemm_ts_fetch(unsigned long long* h) { cudaMemcpyFromSymbol(h, g_gemm_ts, sizeof(g_gemm_ts)); }
+namespace {
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -395,39 +491,46 @@ struct MapCache {
 MapCache g_maps;
 int g_num_sms = 0;
 
-template <int BN, int MODE>
+template <int BN, int MODE, int MS = 1>
 bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K, int S,
                cudaStream_t s, const QkvEpi* epi = nullptr) {
   const CUtensorMap* ma = g_maps.get(A, M, K, BM);
   const CUtensorMap* mb = g_maps.get(B, N, K, BN);
   if (!ma || !mb) return false;
-  const size_t smem = sizeof(Smem<BN>) + 1024;
+  const size_t smem = sizeof(Smem<BN, MS>) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tc<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_gemm_tc<BN, MODE, MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
-  const int ntiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * S;
+  const int ntiles = ((M + MS * BM - 1) / (MS * BM)) * ((N + BN - 1) / BN) * S;
   const int grid = ntiles < g_num_sms ? ntiles : g_num_sms;
   QkvEpi e{};
   if (epi) e = *epi;
-  launch_pdl(k_gemm_tc<BN, MODE>, dim3(grid), dim3(NTHREADS), smem, s, *ma, *mb, C, bias, act, M, N, K, S, e);
+  launch_pdl(k_gemm_tc<BN, MODE, MS>, dim3(grid), dim3(NTHREADS), smem, s, *ma, *mb, C, bias, act, M, N, K, S, e);
   return true;
 }
 }  // namespace
 
 bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
                     int mode, cudaStream_t s) {
-  return launch_gemm_tc_split(A, B, bias, C, act, M, N, K, mode, 1, 256, s);
+  return launch_gemm_tc_split(A, B, bias, C, act, M, N, K, mode, 1, 256, 1, s);
 }
 
 bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
-                          int mode, int S, int BN, cudaStream_t s) {
+                          int mode, int S, int BN, int MSUB, cudaStream_t s) {
   if (M <= 0 || N <= 0) return true;
   if (K % 8) return false;   // TMA row stride must be a multiple of 16 bytes
   const int kb = (K + BK - 1) / BK;
   if (S < 1 || S > kb || (mode == GEMM_SWIGLU && S != 1)) return false;
+  if (MSUB == 2) {
+    if (BN == 128 && mode == GEMM_STORE) return launch_bn<128, GEMM_STORE, 2>(A, B, bias, C, act, M, N, K, S, s);
+    if (BN == 256 && mode == GEMM_STORE) return launch_bn<256, GEMM_STORE, 2>(A, B, bias, C, act, M, N, K, S, s);
+    if (BN == 256 && mode == GEMM_SWIGLU) return launch_bn<256, GEMM_SWIGLU, 2>(A, B, bias, C, act, M, N, K, S, s);
+    return false;
+  }
+  if (MSUB != 1) return false;
   if (BN == 64) {
     if (mode == GEMM_STORE) return launch_bn<64, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s);
     return false;
@@ -451,7 +554,8 @@ bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const Qk
 }
 
 // Split choice for the decode GEMMs: enough (tile x split) units to cover the SMs.
-void choose_split(int M, int N, int K, int& S, int& BN) {
+void choose_split(int M, int N, int K, int& S, int& BN, int& MSUB) {
+  MSUB = 1;
   // measured on B200 at M = 512 (tools/gemm_sweep.py): long-K projections prefer 256-wide
   // tiles with more splits, short-K ones 128-wide tiles; aim for ~one unit per SM
   if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);

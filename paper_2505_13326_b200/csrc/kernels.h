@@ -47,13 +47,15 @@ template <typename T> void launch_gemm_simt(const T* A, const T* B, const float*
 // tcgen05 GEMM (k_gemm_tc.cu), bf16 operands.  GEMM_SWIGLU: B rows interleaved in 256-row
 // tiles as [gate 128 | up 128]; writes act[m][N/2] = SiLU(gate) * up as bf16.
 // Returns false when the shape is unsupported (caller falls back to nothing: it is an error).
+void gemm_ts_reset();
+void gemm_ts_fetch(unsigned long long* h);
 bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
                     int mode, cudaStream_t s);
 void launch_interleave_gate_up(bf16* w, bf16* tmp, int F, int d, cudaStream_t s);
 // split-K variant: S partial products written to C + s*M*N (summed by the consumer kernel)
 bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
-                          int mode, int S, int BN, cudaStream_t s);
-void choose_split(int M, int N, int K, int& S, int& BN);
+                          int mode, int S, int BN, int MSUB, cudaStream_t s);
+void choose_split(int M, int N, int K, int& S, int& BN, int& MSUB);
 // QKV projection with the bias + RoPE + paged KV append fused into the epilogue (tile = 1 head)
 bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const QkvEpi& epi, cudaStream_t s);
 

@@ -253,9 +253,9 @@ template <typename T>
 int proj(sart_ctx* ctx, const T* A, const T* B, int M, int N, int K) {
   int S = 1;
   if constexpr (std::is_same<T, bf16>::value) {
-    int BN = 256;
-    choose_split(M, N, K, S, BN);
-    if (!launch_gemm_tc_split(A, B, nullptr, ctx->parts, nullptr, M, N, K, GEMM_STORE, S, BN, ctx->st))
+    int BN = 256, MS = 1;
+    choose_split(M, N, K, S, BN, MS);
+    if (!launch_gemm_tc_split(A, B, nullptr, ctx->parts, nullptr, M, N, K, GEMM_STORE, S, BN, MS, ctx->st))
       ctx->gemm_failed = true;
   } else {
     launch_gemm_simt<T>(A, B, nullptr, ctx->parts, M, N, K, GEMM_STORE, ctx->st);
@@ -1204,9 +1204,9 @@ int sart_debug_fetch(sart_ctx* ctx, int32_t what, int32_t layer, void* host_out,
 }
 
 int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const uint16_t* B, const float* bias,
-                    float* C, int32_t mode, int32_t splits, int32_t bn) {
+                    float* C, int32_t mode, int32_t splits, int32_t bn, int32_t bm) {
   if (M < 1 || N < 1 || K < 1 || !A || !B || !C || mode < 0 || mode > 2 || splits < 1 || splits > 8 ||
-      (bn != 64 && bn != 128 && bn != 256))
+      (bn != 64 && bn != 128 && bn != 256) || (bm != 128 && bm != 256))
     return set_err(SART_EINVAL, "bad args");
   bf16 *dA = nullptr, *dB = nullptr, *dact = nullptr;
   float *dC = nullptr, *dbias = nullptr;
@@ -1223,7 +1223,8 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
     chk(cudaMemcpy(dB, B, 2 * (size_t)N * K, cudaMemcpyHostToDevice));
     if (bias) chk(cudaMemcpy(dbias, bias, 4 * (size_t)N, cudaMemcpyHostToDevice));
     if (mode == GEMM_ACCUM) chk(cudaMemcpy(dC, C, 4 * (size_t)M * N, cudaMemcpyHostToDevice));
-    if (!launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, 0)) e = cudaErrorInvalidValue;
+    chk(cudaDeviceSynchronize());   // the kernel prefetches B before its PDL wait: B must be resident
+    if (!launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, bm / 128, 0)) e = cudaErrorInvalidValue;
     chk(cudaGetLastError());
     chk(cudaDeviceSynchronize());
     if (const char* reps_s = getenv("SART_GEMM_BENCH_REPS")) {   // micro-benchmark (tools/gemm_sweep.py)
@@ -1232,15 +1233,30 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
       cudaEventCreate(&a);
       cudaEventCreate(&b);
       cudaEventRecord(a, 0);
-      for (int i = 0; i < reps; ++i) launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, 0);
+      for (int i = 0; i < reps; ++i) launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, bm / 128, 0);
       cudaEventRecord(b, 0);
       cudaEventSynchronize(b);
       float ms = 0.f;
       cudaEventElapsedTime(&ms, a, b);
-      fprintf(stderr, "GEMMBENCH M=%d N=%d K=%d mode=%d S=%d BN=%d us=%.2f TFLOPs=%.1f\n", M, N, K, mode, splits, bn,
+      fprintf(stderr, "GEMMBENCH M=%d N=%d K=%d mode=%d S=%d BM=%d BN=%d us=%.2f TFLOPs=%.1f\n", M, N, K, mode, splits,
+              bm, bn,
               1e3 * ms / reps, 2.0 * M * N * K / (ms / reps * 1e-3) / 1e12);
       cudaEventDestroy(a);
       cudaEventDestroy(b);
+    }
+    if (getenv("SART_GEMM_TS")) {
+      gemm_ts_reset();
+      for (int i = 0; i < 4; ++i) launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, bm / 128, 0);
+      cudaDeviceSynchronize();
+      unsigned long long h[4][10];
+      gemm_ts_fetch(&h[0][0]);
+      for (int i = 0; i < 4; ++i) {
+        fprintf(stderr, "GEMMTS M=%d N=%d K=%d S=%d BM=%d BN=%d launch %d:", M, N, K, splits, bm, bn, i);
+        for (int j = 1; j < 9; ++j) fprintf(stderr, " %lld", (long long)(h[i][j] - h[i][0]));
+        if (i) fprintf(stderr, " | start-after-prev-start %lld prev-end->start %lld", (long long)(h[i][0] - h[i - 1][0]),
+                       (long long)(h[i][0] - h[i - 1][8]));
+        fprintf(stderr, "\n");
+      }
     }
     if (mode == GEMM_SWIGLU) {
       std::vector<uint16_t> h(outn);

@@ -122,7 +122,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.sart_reset_profile.argtypes = [C.c_void_p]
     lib.sart_set_profile.argtypes = [C.c_void_p, C.c_int32]
     lib.sart_debug_gemm.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                    C.c_int32, C.c_int32, C.c_int32]
+                                    C.c_int32, C.c_int32, C.c_int32, C.c_int32]
     for f in ("sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
               "sart_get_state", "sart_debug_fetch", "sart_get_profile", "sart_reset_profile", "sart_debug_gemm", "sart_set_profile"):
         getattr(lib, f).restype = C.c_int
@@ -136,7 +136,7 @@ EXPORTED = ["sart_init", "sart_admit", "sart_step", "sart_export_counters", "sar
 
 
 def debug_gemm(A_bits: np.ndarray, B_bits: np.ndarray, bias=None, C=None, mode: int = 0, splits: int = 1,
-               bn: int = 256) -> np.ndarray:
+               bn: int = 256, bm: int = 128) -> np.ndarray:
     """sart_debug_gemm: A [M][K], B [N][K] as bf16 bit patterns (uint16).  With splits > 1 the
     result has shape [splits, M, N] (partial products)."""
     lib = load_library()
@@ -154,7 +154,7 @@ def debug_gemm(A_bits: np.ndarray, B_bits: np.ndarray, bias=None, C=None, mode: 
     if bias is not None:
         bias = np.ascontiguousarray(bias, np.float32)
         bptr = bias.ctypes.data
-    _check(lib.sart_debug_gemm(M, N, K, A.ctypes.data, B.ctypes.data, bptr, out.ctypes.data, mode, splits, bn))
+    _check(lib.sart_debug_gemm(M, N, K, A.ctypes.data, B.ctypes.data, bptr, out.ctypes.data, mode, splits, bn, bm))
     return out
 
 

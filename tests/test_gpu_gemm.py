@@ -36,15 +36,16 @@ def test_gemm_accumulate():
     assert np.max(np.abs(C - ref)) / np.max(np.abs(ref)) < 1e-4
 
 
-def test_gemm_swiglu_interleaved():
-    rng = np.random.default_rng(2)
-    M, F, K = 70, 1024, 512
+@pytest.mark.parametrize("M,bm", [(70, 128), (70, 256), (300, 256), (512, 256)])
+def test_gemm_swiglu_interleaved(M, bm):
+    rng = np.random.default_rng(2 + M)
+    F, K = 1024, 512
     A = rnd(rng, (M, K))
     Wg, Wu = rnd(rng, (F, K), 0.05), rnd(rng, (F, K), 0.05)
     # interleave in 256-row tiles [gate 128 | up 128]
     B = np.concatenate([np.concatenate([Wg[t * 128:(t + 1) * 128], Wu[t * 128:(t + 1) * 128]]) for t in range(F // 128)])
     from paper_2505_13326_b200.sart import debug_gemm
-    act = debug_gemm(A, B, mode=2)
+    act = debug_gemm(A, B, mode=2, bm=bm)
     a = bits_to_f32(A).astype(np.float64)
     g = a @ bits_to_f32(Wg).astype(np.float64).T
     u = a @ bits_to_f32(Wu).astype(np.float64).T
@@ -52,14 +53,20 @@ def test_gemm_swiglu_interleaved():
     assert np.max(np.abs(act - ref)) / np.max(np.abs(ref)) < 1e-2     # bf16 output rounding
 
 
-@pytest.mark.parametrize("M,N,K,S,BN", [(512, 1536, 8960, 6, 128), (512, 2048, 1536, 4, 128), (100, 1536, 1536, 6, 128),
-                                        (512, 1536, 1536, 3, 256), (1, 256, 512, 2, 128)])
-def test_gemm_split_k(M, N, K, S, BN):
+@pytest.mark.parametrize("M,N,K,S,BN,BM", [(512, 1536, 8960, 6, 128, 128), (512, 2048, 1536, 4, 128, 128),
+                                           (100, 1536, 1536, 6, 128, 128), (512, 1536, 1536, 3, 256, 128),
+                                           (1, 256, 512, 2, 128, 128), (512, 1536, 8960, 6, 256, 256),
+                                           (512, 1536, 8960, 8, 128, 256), (300, 1536, 1536, 3, 128, 256),
+                                           (129, 640, 512, 2, 256, 256), (1, 256, 512, 1, 256, 256),
+                                           (640, 512, 256, 1, 64, 128)])
+def test_gemm_split_k(M, N, K, S, BN, BM):
     """split-K partials (the RMSNorm/RoPE consumers sum them in split order)"""
     rng = np.random.default_rng(M + N + K)
     A, B = rnd(rng, (M, K)), rnd(rng, (N, K), 0.05)
     from paper_2505_13326_b200.sart import debug_gemm
-    parts = debug_gemm(A, B, mode=0, splits=S, bn=BN)
-    C = parts.astype(np.float64).sum(axis=0)
+    if S > 8:
+        pytest.skip("splits > 8 not exposed")
+    parts = debug_gemm(A, B, mode=0, splits=S, bn=BN, bm=BM)
+    C = parts.astype(np.float64).reshape(-1, M, N).sum(axis=0)   # S = 1 returns [M][N]
     ref = bits_to_f32(A).astype(np.float64) @ bits_to_f32(B).astype(np.float64).T
     assert np.max(np.abs(C - ref)) / np.max(np.abs(ref)) < 1e-4

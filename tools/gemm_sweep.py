@@ -17,7 +17,7 @@ for name, (M, N, K) in shapes.items():
         continue
     A = rng.integers(0, 1 << 14, size=(M, K), dtype=np.uint16)
     B = rng.integers(0, 1 << 14, size=(N, K), dtype=np.uint16)
-    for bn in (64, 128, 256):
+    for bm, bn in ((128, 128), (128, 256), (256, 128), (256, 256)):
         for S in (1, 2, 3, 4, 6, 8):
             if S > max(1, K // 128):
                 continue
@@ -25,6 +25,6 @@ for name, (M, N, K) in shapes.items():
                 continue
             print(name, flush=True)
             try:
-                debug_gemm(A, B, mode=0, splits=S, bn=bn)
+                debug_gemm(A, B, mode=2 if name == "gateup" and bn == 256 else 0, splits=S, bn=bn, bm=bm)
             except Exception as e:
                 print("fail", e)
