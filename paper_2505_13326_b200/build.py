@@ -8,7 +8,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libsart.so")
+LIB = os.environ.get("SART_LIB_OUT", os.path.join(HERE, "libsart.so"))   # SART_LIB_OUT: A/B variants
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--extended-lambda", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
@@ -19,8 +19,14 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+OBJDIR = os.path.join(HERE, "build") if "SART_LIB_OUT" not in os.environ else LIB + ".objs"
+STAMP = os.path.join(OBJDIR, "flags.txt")
+
+
 def up_to_date() -> bool:
     if not os.path.exists(LIB):
+        return False
+    if not os.path.exists(STAMP) or open(STAMP).read() != " ".join(FLAGS):
         return False
     t = os.path.getmtime(LIB)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
@@ -31,7 +37,7 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = True, jobs: int = 8) -> str:
     if not force and up_to_date():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = OBJDIR
     os.makedirs(objdir, exist_ok=True)
     procs = []
     objs = []
@@ -57,6 +63,8 @@ def build(force: bool = False, verbose: bool = True, jobs: int = 8) -> str:
            "-o", tmp, "-lcuda"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(" ".join(FLAGS))
     return LIB
 
 

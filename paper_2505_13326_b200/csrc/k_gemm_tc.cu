@@ -29,7 +29,14 @@ template <int BN, int MS> struct Tmem {
   static constexpr int NBUF = 2 * MS * BN <= 512 ? 2 : 1;
   static constexpr int COLS = NBUF * MS * BN;
 };
-constexpr int NTHREADS = 192;
+// warp 0 TMA producer, warp 1 MMA issuer, then NEPI epilogue warps: NEPI / 4 per TMEM lane
+// quarter (warp % 4), splitting the 32-column chunks between them
+#ifndef SART_GEMM_NEPI
+#define SART_GEMM_NEPI 4   // 8 (two warps per lane quarter) measured 1.3% slower per C2 step
+#endif
+constexpr int NEPI = SART_GEMM_NEPI;
+constexpr int NTHREADS = 64 + 32 * NEPI;
+constexpr int CSTEP = 32 * (NEPI / 4);   // chunk stride of one epilogue warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -58,6 +65,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
           smem_u32(dst)),
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+// 1-D bulk copy global -> shared (contiguous bytes, multiple of 16) completing on an mbarrier
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 // K-major operand tile [rows][64 bf16] with 128-byte swizzle: SBO = 8 rows x 128 B.
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
@@ -95,6 +109,75 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// fp32 output of one 32-row TMEM lane quarter (BN columns): each lane holds one row of a
+// 32 x 32 chunk; transpose it through a 16-byte-swizzled shared slab (chunk k of row r at
+// k ^ (r & 7): conflict-free both ways) so that each 16-byte store instruction writes 4 full
+// 128-byte lines.  MODE == GEMM_ACCUM adds into C.
+template <int BN, int MODE>
+__device__ __forceinline__ void store_tile_f32(uint32_t tbase, float* Cs, int mrow0, int n0, int M, int N,
+                                               const float* bias, uint32_t slab, int lane, int c_begin, int c_step) {
+  const int kk = lane & 7, r4 = lane >> 3;
+  const bool vec = (N & 3) == 0;
+#pragma unroll 1
+  for (int c = c_begin; c < BN; c += c_step) {
+    float v[32];
+    tmem_ld32(tbase + c, v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(slab + (uint32_t)(lane * 32 + ((k ^ (lane & 7)) << 2)) * 4),
+                   "f"(v[4 * k]), "f"(v[4 * k + 1]), "f"(v[4 * k + 2]), "f"(v[4 * k + 3])
+                   : "memory");
+    __syncwarp();
+    const int gn = n0 + c + kk * 4;
+    float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (bias) {
+      if (vec && gn + 4 <= N) bv = *reinterpret_cast<const float4*>(bias + gn);
+      else {
+        if (gn < N) bv.x = bias[gn];
+        if (gn + 1 < N) bv.y = bias[gn + 1];
+        if (gn + 2 < N) bv.z = bias[gn + 2];
+        if (gn + 3 < N) bv.w = bias[gn + 3];
+      }
+    }
+    float4 x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int rr = i * 4 + r4;
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(x[i].x), "=f"(x[i].y), "=f"(x[i].z), "=f"(x[i].w)
+                   : "r"(slab + (uint32_t)(rr * 32 + ((kk ^ (rr & 7)) << 2)) * 4)
+                   : "memory");
+      x[i].x += bv.x; x[i].y += bv.y; x[i].z += bv.z; x[i].w += bv.w;
+    }
+    __syncwarp();
+    float* dst = Cs + (size_t)(mrow0 + r4) * N + gn;
+    if (vec && gn + 4 <= N) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (mrow0 + i * 4 + r4 < M) {
+          float4* d4 = reinterpret_cast<float4*>(dst + (size_t)i * 4 * N);
+          if (MODE == GEMM_ACCUM) {
+            const float4 o = *d4;
+            x[i].x += o.x; x[i].y += o.y; x[i].z += o.z; x[i].w += o.w;
+          }
+          *d4 = x[i];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (mrow0 + i * 4 + r4 < M) {
+          float* d = dst + (size_t)i * 4 * N;
+          const float xs[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (gn + e < N) d[e] = MODE == GEMM_ACCUM ? d[e] + xs[e] : xs[e];
+        }
+      }
+    }
+  }
+}
+
 template <int BN, int MS>
 struct Smem {
   static constexpr int STAGES = Stages<BN, MS>::value;
@@ -102,6 +185,7 @@ struct Smem {
   alignas(1024) bf16 b[STAGES][BN * BK];
   uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   uint32_t tmem_base;
+  alignas(16) float slab[NEPI][32 * 32];   // epilogue transpose staging (explicit st/ld.shared)
 };
 
 // MS m-subtiles of 128 rows share each B stage (tile = MS*128 x BN): per-SM operand traffic
@@ -115,6 +199,7 @@ struct Smem {
 }  // namespace
 __device__ unsigned long long g_gemm_ts[4][10];
 __device__ int g_gemm_ts_idx;
+__device__ unsigned long long g_gemm_trace[2][64];   // CTA 0, first tile: [0] load issue, [1] stage landed
 namespace {
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -123,13 +208,10 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 template <int BN, int MODE, int MS>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* C,
-              const float* __restrict__ bias, bf16* act, int M, int N, int K, int S, const __grid_constant__ QkvEpi epi) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // epilogue staging, per epilogue warp 32 rows x 32 cols padded: a static __shared__ array so
-  // that the compiler emits STS/LDS (a pointer into the aligned dynamic buffer decays to
-  // generic LD/ST, which it cannot reorder around the global stores)
-  __shared__ __align__(16) float slab_s[4][32 * 32];
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const bf16* __restrict__ Bt,
+              float* C, const float* __restrict__ bias, bf16* act, int M, int N, int K, int S,
+              const __grid_constant__ QkvEpi epi) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];   // 1024-aligned below (+1024 B slack)
   Smem<BN, MS>& sm =
       *reinterpret_cast<Smem<BN, MS>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int STAGES = Smem<BN, MS>::STAGES;
@@ -157,7 +239,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], 1); }
-    for (int s = 0; s < NBUF; ++s) { mbar_init(&sm.tfull[s], 1); mbar_init(&sm.tempty[s], 4); }
+    for (int s = 0; s < NBUF; ++s) { mbar_init(&sm.tfull[s], 1); mbar_init(&sm.tempty[s], NEPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -175,7 +257,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+      if (!Bt) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+      // weights: pre-tiled (Bt: [n-tile][k-block] images of the swizzled shared tile, one
+      // contiguous bulk copy each) or row-major through the 2-D tensor map
+      auto load_b = [&](int st, int kbi, int n0_) {
+        if (Bt) bulk_load(sm.b[st], Bt + ((size_t)(n0_ / BN) * kb_all + kbi) * (BN * BK), BN * BK * 2, &sm.full[st]);
+        else tma_load_2d(sm.b[st], &tmB, &sm.full[st], kbi * BK, n0_);
+      };
+      auto load_a = [&](int st, int j, int kbi, int m0_) {
+        tma_load_2d(sm.a[st] + j * BM * BK, &tmA, &sm.full[st], kbi * BK, m0_ + j * BM);
+      };
       int stage = 0;
       uint32_t phase = 0;
       bool first = true;
@@ -190,14 +281,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int pre = min(STAGES, kb1 - kb0);
           for (int i = 0; i < pre; ++i) {
             mbar_expect_tx(&sm.full[i], STAGE_TX);
-            tma_load_2d(sm.b[i], &tmB, &sm.full[i], (kb0 + i) * BK, n0);
+            load_b(i, kb0 + i, n0);
           }
           pdl_wait();
           TS(2);
-          for (int i = 0; i < pre; ++i)
+          for (int i = 0; i < pre; ++i) {
 #pragma unroll
             for (int j = 0; j < MS; ++j)
-              tma_load_2d(sm.a[i] + j * BM * BK, &tmA, &sm.full[i], (kb0 + i) * BK, m0 + j * BM);
+              load_a(i, j, kb0 + i, m0);
+#ifdef SART_GEMM_TS
+            if (blockIdx.x == 0 && i < 64) g_gemm_trace[0][i] = gtime();
+#endif
+          }
           kb += pre;
           stage = pre % STAGES;
           phase = pre == STAGES ? 1 : 0;
@@ -206,8 +301,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mbar_wait(&sm.empty[stage], phase ^ 1);
           mbar_expect_tx(&sm.full[stage], STAGE_TX);
 #pragma unroll
-          for (int j = 0; j < MS; ++j) tma_load_2d(sm.a[stage] + j * BM * BK, &tmA, &sm.full[stage], kb * BK, m0 + j * BM);
-          tma_load_2d(sm.b[stage], &tmB, &sm.full[stage], kb * BK, n0);
+          for (int j = 0; j < MS; ++j) load_a(stage, j, kb, m0);
+          load_b(stage, kb, n0);
+#ifdef SART_GEMM_TS
+          if (blockIdx.x == 0 && t == blockIdx.x && kb - kb0 < 64) g_gemm_trace[0][kb - kb0] = gtime();
+#endif
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -231,6 +329,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_wait(&sm.full[stage], phase);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (lane == 0 && it == 0 && kb == kb0) { TS(3); }
+#ifdef SART_GEMM_TS
+        if (lane == 0 && blockIdx.x == 0 && it == 0 && kb - kb0 < 64) g_gemm_trace[1][kb - kb0] = gtime();
+#endif
         if (lane == 0) {
           const uint32_t a0 = smem_u32(sm.a[stage]), b0 = smem_u32(sm.b[stage]);
 #pragma unroll
@@ -250,7 +351,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else {
     // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
     pdl_wait();   // outputs may be read by the previous kernel; inputs (bias, rows) are visible
-    const int q = warp & 3;
+    const int q = warp & 3;            // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;  // which 32-column chunks of the tile it handles
     const int row = q * 32 + lane;
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -269,10 +371,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (as * MS + ms) * BN;
       if (MODE == GEMM_QKV) {
         // tile = one head (BN == head_dim): q / k heads are rotated (pairs i, i + hd/2), k and v
-        // are appended to the paged pool at the row's slot (common.cuh layout and swizzle)
+        // are appended to the paged pool at the row's slot (common.cuh layout and swizzle).
+        // Split-K (S > 1): every unit publishes its fp32 partial tile (C + split * M * N); the
+        // last of the S units of a (m-tile, head, lane quarter) -- an atomic arrival count --
+        // sums the S partials in split order (deterministic) and runs the epilogue.
         const Dims& D = epi.D;
         const int head = n0 / BN;
         constexpr int HALF = BN / 2;
+        if (S > 1) {
+          store_tile_f32<BN, GEMM_STORE>(tbase, Cs, m0 + q * 32, n0, M, N, nullptr, smem_u32(sm.slab[warp - 2]), lane, half * 32, CSTEP);
+          __threadfence();
+          __syncwarp();
+          int old = 0;
+          if (lane == 0) {
+            int* cnt = epi.cnt + (((size_t)head * mt + m0_ / BM) * 4 + q) * 2 + half;
+            old = atomicAdd(cnt, 1);
+            if (old == S - 1) *cnt = 0;   // reset for the next launch (stream-ordered)
+          }
+          old = __shfl_sync(0xffffffffu, old, 0);
+          if (old != S - 1) continue;
+          __threadfence();
+        }
         int pos = 0;
         bool kv_ok = false;
         long long blk = 0;
@@ -294,10 +413,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const bool rot = head < D.qh + D.kvh;
         const float* cs = epi.rope_cs + (long long)pos * BN;   // [cos(half) | sin(half)]
 #pragma unroll 1
-        for (int c = 0; c < HALF; c += 32) {
+        for (int c = half * 32; c < HALF; c += CSTEP) {
           float x1[32], x2[32];
-          tmem_ld32(tbase + c, x1);
-          tmem_ld32(tbase + HALF + c, x2);
+          if (S == 1) {
+            tmem_ld32(tbase + c, x1);
+            tmem_ld32(tbase + HALF + c, x2);
+          } else if (gm < M) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x1[j] = x2[j] = 0.f;
+            for (int sp2 = 0; sp2 < S; ++sp2) {   // split order
+              const float* p = C + (size_t)sp2 * M * N + (size_t)gm * N + n0 + c;
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                const float4 a = __ldcg(reinterpret_cast<const float4*>(p + 4 * j4));
+                const float4 b = __ldcg(reinterpret_cast<const float4*>(p + HALF + 4 * j4));
+                x1[4 * j4] += a.x; x1[4 * j4 + 1] += a.y; x1[4 * j4 + 2] += a.z; x1[4 * j4 + 3] += a.w;
+                x2[4 * j4] += b.x; x2[4 * j4 + 1] += b.y; x2[4 * j4 + 2] += b.z; x2[4 * j4 + 3] += b.w;
+              }
+            }
+          }
           if (gm < M) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) { x1[j] += epi.bias[n0 + c + j]; x2[j] += epi.bias[n0 + HALF + c + j]; }
@@ -345,7 +479,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int F = N / 2;   // N = 2F interleaved in BN-wide tiles
         const int f0 = n0 / 2;
 #pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
+        for (int c = half * 32; c < BN / 2; c += CSTEP) {
           float g[32], u[32];
           tmem_ld32(tbase + c, g);
           tmem_ld32(tbase + BN / 2 + c, u);
@@ -366,67 +500,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
       } else {
-        // fp32 output: each lane holds one row of a 32 x 32 chunk; transpose it through a
-        // 16-byte-swizzled shared slab (chunk k of row r at k ^ (r & 7): conflict-free both ways)
-        // so that each 16-byte store instruction writes 4 full 128-byte lines
-        float* slab = slab_s[q];
-        const int mrow0 = m0 + q * 32;
-        const int kk = lane & 7, r4 = lane >> 3;
-        const bool vec = (N & 3) == 0;
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          float v[32];
-          tmem_ld32(tbase + c, v);
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            *reinterpret_cast<float4*>(slab + lane * 32 + ((k ^ (lane & 7)) << 2)) =
-                make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-          __syncwarp();
-          const int gn = n0 + c + kk * 4;
-          float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (bias) {
-            if (vec && gn + 4 <= N) bv = *reinterpret_cast<const float4*>(bias + gn);
-            else {
-              if (gn < N) bv.x = bias[gn];
-              if (gn + 1 < N) bv.y = bias[gn + 1];
-              if (gn + 2 < N) bv.z = bias[gn + 2];
-              if (gn + 3 < N) bv.w = bias[gn + 3];
-            }
-          }
-          float4 x[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int rr = i * 4 + r4;
-            x[i] = *reinterpret_cast<const float4*>(slab + rr * 32 + ((kk ^ (rr & 7)) << 2));
-            x[i].x += bv.x; x[i].y += bv.y; x[i].z += bv.z; x[i].w += bv.w;
-          }
-          __syncwarp();
-          float* dst = Cs + (size_t)(mrow0 + r4) * N + gn;
-          if (vec && gn + 4 <= N) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              if (mrow0 + i * 4 + r4 < M) {
-                float4* d4 = reinterpret_cast<float4*>(dst + (size_t)i * 4 * N);
-                if (MODE == GEMM_ACCUM) {
-                  const float4 o = *d4;
-                  x[i].x += o.x; x[i].y += o.y; x[i].z += o.z; x[i].w += o.w;
-                }
-                *d4 = x[i];
-              }
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              if (mrow0 + i * 4 + r4 < M) {
-                float* d = dst + (size_t)i * 4 * N;
-                const float xs[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  if (gn + e < N) d[e] = MODE == GEMM_ACCUM ? d[e] + xs[e] : xs[e];
-              }
-            }
-          }
-        }
+        store_tile_f32<BN, MODE>(tbase, Cs, m0 + q * 32, n0, M, N, bias, smem_u32(sm.slab[warp - 2]), lane, half * 32, CSTEP);
       }
       }  // m-subtile
       asm volatile("tcgen05.fence::before_thread_sync;");
@@ -447,6 +521,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }  // namespace
 void gemm_ts_reset() { int z = 0; cudaMemcpyToSymbol(g_gemm_ts_idx, &z, 4); }
 void gemm_ts_fetch(unsigned long long* h) { cudaMemcpyFromSymbol(h, g_gemm_ts, sizeof(g_gemm_ts)); }
+void gemm_trace_fetch(unsigned long long* h) { cudaMemcpyFromSymbol(h, g_gemm_trace, sizeof(g_gemm_trace)); }
 namespace {
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -493,9 +568,9 @@ int g_num_sms = 0;
 
 template <int BN, int MODE, int MS = 1>
 bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K, int S,
-               cudaStream_t s, const QkvEpi* epi = nullptr) {
+               cudaStream_t s, const QkvEpi* epi = nullptr, const bf16* Bt = nullptr) {
   const CUtensorMap* ma = g_maps.get(A, M, K, BM);
-  const CUtensorMap* mb = g_maps.get(B, N, K, BN);
+  const CUtensorMap* mb = Bt ? ma : g_maps.get(B, N, K, BN);
   if (!ma || !mb) return false;
   const size_t smem = sizeof(Smem<BN, MS>) + 1024;
   static bool attr = false;
@@ -508,48 +583,67 @@ bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* 
   const int grid = ntiles < g_num_sms ? ntiles : g_num_sms;
   QkvEpi e{};
   if (epi) e = *epi;
-  launch_pdl(k_gemm_tc<BN, MODE, MS>, dim3(grid), dim3(NTHREADS), smem, s, *ma, *mb, C, bias, act, M, N, K, S, e);
+  launch_pdl(k_gemm_tc<BN, MODE, MS>, dim3(grid), dim3(NTHREADS), smem, s, *ma, *mb, Bt, C, bias, act, M, N, K, S, e);
   return true;
 }
 }  // namespace
 
 bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
-                    int mode, cudaStream_t s) {
-  return launch_gemm_tc_split(A, B, bias, C, act, M, N, K, mode, 1, 256, 1, s);
+                    int mode, cudaStream_t s, const bf16* Bt) {
+  // 256-row tiles (two MMA tiles per weight stage) once they still fill ~3/4 of the SMs:
+  // measured 7% faster on the C2 gate/up projection (profiles/r1_gemm_bm256_sweep.txt)
+  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
+  const int ms = (mode == GEMM_SWIGLU && M > BM && ((M + 2 * BM - 1) / (2 * BM)) * ((N + 255) / 256) >= g_num_sms * 3 / 4)
+                     ? 2 : 1;
+  return launch_gemm_tc_split(A, B, bias, C, act, M, N, K, mode, 1, 256, ms, s, Bt);
 }
 
 bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
-                          int mode, int S, int BN, int MSUB, cudaStream_t s) {
+                          int mode, int S, int BN, int MSUB, cudaStream_t s, const bf16* Bt) {
   if (M <= 0 || N <= 0) return true;
   if (K % 8) return false;   // TMA row stride must be a multiple of 16 bytes
   const int kb = (K + BK - 1) / BK;
   if (S < 1 || S > kb || (mode == GEMM_SWIGLU && S != 1)) return false;
   if (MSUB == 2) {
-    if (BN == 128 && mode == GEMM_STORE) return launch_bn<128, GEMM_STORE, 2>(A, B, bias, C, act, M, N, K, S, s);
-    if (BN == 256 && mode == GEMM_STORE) return launch_bn<256, GEMM_STORE, 2>(A, B, bias, C, act, M, N, K, S, s);
-    if (BN == 256 && mode == GEMM_SWIGLU) return launch_bn<256, GEMM_SWIGLU, 2>(A, B, bias, C, act, M, N, K, S, s);
+    if (BN == 128 && mode == GEMM_STORE) return launch_bn<128, GEMM_STORE, 2>(A, B, bias, C, act, M, N, K, S, s, nullptr, Bt);
+    if (BN == 256 && mode == GEMM_STORE) return launch_bn<256, GEMM_STORE, 2>(A, B, bias, C, act, M, N, K, S, s, nullptr, Bt);
+    if (BN == 256 && mode == GEMM_SWIGLU) return launch_bn<256, GEMM_SWIGLU, 2>(A, B, bias, C, act, M, N, K, S, s, nullptr, Bt);
     return false;
   }
   if (MSUB != 1) return false;
   if (BN == 64) {
-    if (mode == GEMM_STORE) return launch_bn<64, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s);
+    if (mode == GEMM_STORE) return launch_bn<64, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s, nullptr, Bt);
     return false;
   }
   if (BN == 128) {
-    if (mode == GEMM_STORE) return launch_bn<128, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s);
-    if (mode == GEMM_ACCUM) return launch_bn<128, GEMM_ACCUM>(A, B, bias, C, act, M, N, K, S, s);
+    if (mode == GEMM_STORE) return launch_bn<128, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s, nullptr, Bt);
+    if (mode == GEMM_ACCUM) return launch_bn<128, GEMM_ACCUM>(A, B, bias, C, act, M, N, K, S, s, nullptr, Bt);
     return false;
   }
-  if (mode == GEMM_STORE) return launch_bn<256, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s);
-  if (mode == GEMM_ACCUM) return launch_bn<256, GEMM_ACCUM>(A, B, bias, C, act, M, N, K, S, s);
-  return launch_bn<256, GEMM_SWIGLU>(A, B, bias, C, act, M, N, K, S, s);
+  if (mode == GEMM_STORE) return launch_bn<256, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s, nullptr, Bt);
+  if (mode == GEMM_ACCUM) return launch_bn<256, GEMM_ACCUM>(A, B, bias, C, act, M, N, K, S, s, nullptr, Bt);
+  return launch_bn<256, GEMM_SWIGLU>(A, B, bias, C, act, M, N, K, S, s, nullptr, Bt);
 }
 
-bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const QkvEpi& epi, cudaStream_t s) {
+bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const QkvEpi& epi, cudaStream_t s,
+                     const bf16* Bt) {
   if (M <= 0) return true;
   if (K % 8) return false;
-  if (epi.D.hd == 128) return launch_bn<128, GEMM_QKV>(A, B, nullptr, nullptr, nullptr, M, N, K, 1, s, &epi);
-  if (epi.D.hd == 64) return launch_bn<64, GEMM_QKV>(A, B, nullptr, nullptr, nullptr, M, N, K, 1, s, &epi);
+  // split-K so that (m-tiles x heads x splits) covers the SMs; the last split of each tile
+  // runs the fused bias + RoPE + KV-append epilogue
+  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
+  const int mt = (M + BM - 1) / BM, heads = N / epi.D.hd, kb = (K + BK - 1) / BK;
+  int S = 1;
+  if (epi.parts && epi.cnt && heads * mt * 8 <= epi.cnt_cap && epi.D.hd >= 128) {
+    S = (g_num_sms + heads * mt / 2) / (heads * mt);
+    S = std::max(1, std::min(S, std::min(8, kb / 2)));
+    // measured on C2: the fused single-pass kernel is 3% faster per step than S = 2 with the
+    // partial round trip, so split-K is opt-in (SART_QKV_SPLIT=max splits) for other shapes
+    static const int smax = getenv("SART_QKV_SPLIT") ? atoi(getenv("SART_QKV_SPLIT")) : 1;
+    S = std::max(1, std::min(S, smax));
+  }
+  if (epi.D.hd == 128) return launch_bn<128, GEMM_QKV>(A, B, nullptr, epi.parts, nullptr, M, N, K, S, s, &epi, Bt);
+  if (epi.D.hd == 64) return launch_bn<64, GEMM_QKV>(A, B, nullptr, epi.parts, nullptr, M, N, K, S, s, &epi, Bt);
   return false;
 }
 
@@ -569,4 +663,41 @@ void choose_split(int M, int N, int K, int& S, int& BN, int& MSUB) {
   if (S < 1) S = 1;
   if (S > 8) S = 8;
   if (S > kb / 2) S = kb / 2 > 0 ? kb / 2 : 1;
+}
+
+// ------------------------------------------------------------------ pre-tiled weights
+// Wt[n-tile][k-block] = the exact shared-memory image of the (BN x 64) K-major tile with the
+// 128-byte swizzle (16-byte chunk c of row r stored at c ^ (r & 7)); rows >= N and columns >= K
+// are zero.  One contiguous BN*128-byte bulk copy per stage replaces BN strided 128-byte rows.
+__global__ void k_tile_b(const bf16* __restrict__ W, bf16* __restrict__ Wt, int N, int K, int BN, int KB,
+                         long long chunks) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < chunks; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i & 7);                 // source 16-byte chunk within the row's 64 columns
+    const long long rowid = i >> 3;             // (n-tile, k-block, r)
+    const int r = (int)(rowid % BN);
+    const long long tk = rowid / BN;
+    const int kb = (int)(tk % KB);
+    const int nt = (int)(tk / KB);
+    const int n = nt * BN + r, k = kb * BK + c * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (n < N) {
+      if (k + 8 <= K && (K & 7) == 0) v = *reinterpret_cast<const uint4*>(W + (size_t)n * K + k);
+      else {
+        __align__(16) bf16 t[8];
+        for (int e = 0; e < 8; ++e) t[e] = (k + e < K) ? W[(size_t)n * K + k + e] : __float2bfloat16_rn(0.f);
+        v = *reinterpret_cast<uint4*>(t);
+      }
+    }
+    *reinterpret_cast<uint4*>(Wt + rowid * BK + ((c ^ (r & 7)) << 3)) = v;
+  }
+}
+
+size_t tiled_b_elems(int N, int K, int BN) {
+  return (size_t)((N + BN - 1) / BN) * BN * (size_t)((K + BK - 1) / BK) * BK;
+}
+void launch_tile_b(const bf16* W, bf16* Wt, int N, int K, int BN, cudaStream_t s) {
+  const int KB = (K + BK - 1) / BK;
+  const long long chunks = (long long)tiled_b_elems(N, K, BN) / 8;
+  const int blocks = (int)std::min<long long>((chunks + 255) / 256, 148LL * 16);
+  k_tile_b<<<blocks, 256, 0, s>>>(W, Wt, N, K, BN, KB, chunks);
 }

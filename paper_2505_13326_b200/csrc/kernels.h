@@ -40,6 +40,9 @@ struct QkvEpi {
   Rows rows;
   Reqs reqs;
   RopeArgs a;
+  float* parts;   // split-K partials [S][M][N] (S > 1)
+  int* cnt;       // per (head, m-tile, lane quarter) arrival counters, zero between launches
+  int cnt_cap;    // entries in cnt (split-K is used only when heads x m-tiles x 4 fits)
 };
 template <typename T> void launch_gemm_simt(const T* A, const T* B, const float* bias, float* C, int M, int N,
                                             int K, int mode, cudaStream_t s);
@@ -49,15 +52,19 @@ template <typename T> void launch_gemm_simt(const T* A, const T* B, const float*
 // Returns false when the shape is unsupported (caller falls back to nothing: it is an error).
 void gemm_ts_reset();
 void gemm_ts_fetch(unsigned long long* h);
+void gemm_trace_fetch(unsigned long long* h);
 bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
-                    int mode, cudaStream_t s);
+                    int mode, cudaStream_t s, const bf16* Bt = nullptr);
 void launch_interleave_gate_up(bf16* w, bf16* tmp, int F, int d, cudaStream_t s);
 // split-K variant: S partial products written to C + s*M*N (summed by the consumer kernel)
 bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
-                          int mode, int S, int BN, int MSUB, cudaStream_t s);
+                          int mode, int S, int BN, int MSUB, cudaStream_t s, const bf16* Bt = nullptr);
+// pre-tiled weight layout for the tcgen05 GEMM (k_gemm_tc.cu)
+size_t tiled_b_elems(int N, int K, int BN);
+void launch_tile_b(const bf16* W, bf16* Wt, int N, int K, int BN, cudaStream_t s);
 void choose_split(int M, int N, int K, int& S, int& BN, int& MSUB);
 // QKV projection with the bias + RoPE + paged KV append fused into the epilogue (tile = 1 head)
-bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const QkvEpi& epi, cudaStream_t s);
+bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const QkvEpi& epi, cudaStream_t s, const bf16* Bt = nullptr);
 
 // ---- attention (k_attn.cu)
 template <typename T> void launch_attn_decode_simple(const T* q, const T* pool, T* out, float* dbg, Dims D,

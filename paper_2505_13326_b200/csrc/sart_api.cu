@@ -97,6 +97,8 @@ struct sart_ctx {
   int* d_prompt = nullptr;     // batched prefill: tokens, request slots, positions
   int *d_pf_slot = nullptr, *d_pf_pos = nullptr;
   int pf_cap = 0;
+  int* qkv_cnt = nullptr;   // split-K QKV arrival counters
+  int qkv_cnt_cap = 0;
   std::vector<int> pf_tok, pf_slot, pf_pos;
   std::vector<int> pf_slot_h, pf_pos_h;   // host copies used to build the query blocks
   int4* d_pf_blocks = nullptr;
@@ -271,7 +273,8 @@ void qkv_rope(sart_ctx* ctx, int l, int n, RopeArgs ra) {
   const Dims& D = ctx->D;
   const float* bias = ctx->fparams + ctx->f_bqkv + (size_t)l * D.qkv;
   if constexpr (std::is_same<T, bf16>::value) {
-    QkvEpi e{bias, (bf16*)ctx->q, (bf16*)ctx->pool, ctx->rope_cs, D, l, ctx->rows, ctx->reqs, ra};
+    QkvEpi e{bias,       (bf16*)ctx->q, (bf16*)ctx->pool, ctx->rope_cs, D,           l,
+             ctx->rows, ctx->reqs,    ra,               ctx->parts,    ctx->qkv_cnt, ctx->qkv_cnt_cap};
     if (!launch_gemm_qkv((bf16*)ctx->a, ctx->W_<bf16>(t_layer(l, 1)), n, D.qkv, D.d, e, ctx->st))
       ctx->gemm_failed = true;
     ctx->launches++;
@@ -896,6 +899,8 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   const size_t W = ctx->W;
   IC(dalloc(ctx, &ctx->h, W * D.d * 4));
   IC(dalloc(ctx, &ctx->parts, W * std::max(D.qkv, D.d) * 8 * 4, false));   // split-K partials (S <= 8)
+  ctx->qkv_cnt_cap = (D.qkv / D.hd) * ((int)((W + 127) / 128)) * 8;
+  IC(dalloc(ctx, &ctx->qkv_cnt, sizeof(int) * (size_t)ctx->qkv_cnt_cap));   // QKV split-K arrivals (zeroed)
   IC(dalloc(ctx, &ctx->gu, W * 2 * D.F * 4));
   IC(dalloc(ctx, &ctx->z32, (size_t)D.R * D.d * 4));
   IC(dalloc(ctx, &ctx->logits, (size_t)D.R * D.V * 4));
@@ -1208,7 +1213,7 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
   if (M < 1 || N < 1 || K < 1 || !A || !B || !C || mode < 0 || mode > 2 || splits < 1 || splits > 8 ||
       (bn != 64 && bn != 128 && bn != 256) || (bm != 128 && bm != 256))
     return set_err(SART_EINVAL, "bad args");
-  bf16 *dA = nullptr, *dB = nullptr, *dact = nullptr;
+  bf16 *dA = nullptr, *dB = nullptr, *dact = nullptr, *dBt = nullptr;
   float *dC = nullptr, *dbias = nullptr;
   const size_t outn = mode == GEMM_SWIGLU ? (size_t)M * (N / 2) : (size_t)M * N;
   cudaError_t e = cudaSuccess;
@@ -1223,8 +1228,15 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
     chk(cudaMemcpy(dB, B, 2 * (size_t)N * K, cudaMemcpyHostToDevice));
     if (bias) chk(cudaMemcpy(dbias, bias, 4 * (size_t)N, cudaMemcpyHostToDevice));
     if (mode == GEMM_ACCUM) chk(cudaMemcpy(dC, C, 4 * (size_t)M * N, cudaMemcpyHostToDevice));
+    // SART_GEMM_BTILED=1: run from the pre-tiled weight layout (what the engine uses)
+    const bool tiled = getenv("SART_GEMM_BTILED") && atoi(getenv("SART_GEMM_BTILED"));
+    if (tiled) {
+      chk(cudaMalloc(&dBt, 2 * tiled_b_elems(N, K, bn)));
+      if (e == cudaSuccess) launch_tile_b(dB, dBt, N, K, bn, 0);
+    }
     chk(cudaDeviceSynchronize());   // the kernel prefetches B before its PDL wait: B must be resident
-    if (!launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, bm / 128, 0)) e = cudaErrorInvalidValue;
+    if (!launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, bm / 128, 0, dBt))
+      e = cudaErrorInvalidValue;
     chk(cudaGetLastError());
     chk(cudaDeviceSynchronize());
     if (const char* reps_s = getenv("SART_GEMM_BENCH_REPS")) {   // micro-benchmark (tools/gemm_sweep.py)
@@ -1232,17 +1244,35 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
       cudaEvent_t a, b;
       cudaEventCreate(&a);
       cudaEventCreate(&b);
+      // SART_GEMM_BENCH_COPIES=n: cycle over n copies of B so that the weights stream from HBM
+      // (n x |B| > L2) as they do in a decode step, instead of staying L2-resident
+      const int ncp = getenv("SART_GEMM_BENCH_COPIES") ? std::max(1, atoi(getenv("SART_GEMM_BENCH_COPIES"))) : 1;
+      std::vector<bf16*> Bs(1, tiled ? dBt : dB);
+      const size_t bel = tiled ? tiled_b_elems(N, K, bn) : (size_t)N * K;
+      for (int i = 1; i < ncp; ++i) {
+        bf16* p = nullptr;
+        if (cudaMalloc(&p, 2 * bel) != cudaSuccess) break;
+        cudaMemcpy(p, Bs[0], 2 * bel, cudaMemcpyDeviceToDevice);
+        Bs.push_back(p);
+      }
+      auto run = [&](bf16* p) {
+        if (tiled) launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, bm / 128, 0, p);
+        else launch_gemm_tc_split(dA, p, dbias, dC, dact, M, N, K, mode, splits, bn, bm / 128, 0);
+      };
+      for (auto p : Bs) run(p);
+      cudaDeviceSynchronize();
       cudaEventRecord(a, 0);
-      for (int i = 0; i < reps; ++i) launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, bm / 128, 0);
+      for (int i = 0; i < reps; ++i) run(Bs[i % Bs.size()]);
       cudaEventRecord(b, 0);
       cudaEventSynchronize(b);
       float ms = 0.f;
       cudaEventElapsedTime(&ms, a, b);
-      fprintf(stderr, "GEMMBENCH M=%d N=%d K=%d mode=%d S=%d BM=%d BN=%d us=%.2f TFLOPs=%.1f\n", M, N, K, mode, splits,
-              bm, bn,
+      fprintf(stderr, "GEMMBENCH M=%d N=%d K=%d mode=%d S=%d BM=%d BN=%d copies=%d tiled=%d us=%.2f TFLOPs=%.1f\n", M,
+              N, K, mode, splits, bm, bn, (int)Bs.size(), (int)tiled,
               1e3 * ms / reps, 2.0 * M * N * K / (ms / reps * 1e-3) / 1e12);
       cudaEventDestroy(a);
       cudaEventDestroy(b);
+      for (size_t i = 1; i < Bs.size(); ++i) cudaFree(Bs[i]);
     }
     if (getenv("SART_GEMM_TS")) {
       gemm_ts_reset();
@@ -1257,6 +1287,12 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
                        (long long)(h[i][0] - h[i - 1][8]));
         fprintf(stderr, "\n");
       }
+      unsigned long long tr[2][64];
+      gemm_trace_fetch(&tr[0][0]);
+      fprintf(stderr, "GEMMTRACE M=%d N=%d K=%d S=%d BN=%d (ns from first issue) issue/landed:", M, N, K, splits, bn);
+      for (int k = 0; k < 64 && tr[1][k] >= tr[0][0] && tr[1][k] - tr[0][0] < 1000000; ++k)
+        fprintf(stderr, " %lld/%lld", (long long)(tr[0][k] - tr[0][0]), (long long)(tr[1][k] - tr[0][0]));
+      fprintf(stderr, "\n");
     }
     if (mode == GEMM_SWIGLU) {
       std::vector<uint16_t> h(outn);
@@ -1269,7 +1305,7 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
       chk(cudaMemcpy(C, dC, 4 * (size_t)M * N * splits, cudaMemcpyDeviceToHost));
     }
   }
-  cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dact); if (dbias) cudaFree(dbias);
+  cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dact); if (dbias) cudaFree(dbias); if (dBt) cudaFree(dBt);
   if (e != cudaSuccess) return set_err(SART_ECUDA, cudaGetErrorString(e));
   return SART_OK;
 }

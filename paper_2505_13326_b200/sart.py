@@ -13,7 +13,7 @@ from typing import Dict, List, Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsart.so")
+LIB_PATH = os.environ.get("SART_LIB", os.path.join(HERE, "libsart.so"))   # SART_LIB: A/B of build variants
 
 SART_OK, SART_EINVAL, SART_ENOMEM, SART_ECUDA, SART_EFULL, SART_ESTATE, SART_EDUP = 0, -1, -2, -3, -4, -5, -6
 SART_BF16, SART_FP32 = 0, 1

@@ -13,8 +13,11 @@ def rnd(rng, shape, scale=1.0):
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 256, 64), (7, 512, 128), (128, 256, 256), (130, 2048, 1536),
-                                   (512, 1536, 8960), (37, 151936, 1536), (300, 4608, 3584), (129, 96, 64)])
-def test_gemm_store_bias(M, N, K):
+                                   (512, 1536, 8960), (37, 151936, 1536), (300, 4608, 3584), (129, 96, 64),
+                                   (65, 1000, 200)])
+@pytest.mark.parametrize("tiled", [0, 1])
+def test_gemm_store_bias(M, N, K, tiled, monkeypatch):
+    monkeypatch.setenv("SART_GEMM_BTILED", str(tiled))
     rng = np.random.default_rng(M * 7 + N)
     A, B = rnd(rng, (M, K)), rnd(rng, (N, K), 0.05)
     bias = rng.standard_normal(N).astype(np.float32)
@@ -36,8 +39,10 @@ def test_gemm_accumulate():
     assert np.max(np.abs(C - ref)) / np.max(np.abs(ref)) < 1e-4
 
 
-@pytest.mark.parametrize("M,bm", [(70, 128), (70, 256), (300, 256), (512, 256)])
-def test_gemm_swiglu_interleaved(M, bm):
+@pytest.mark.parametrize("M,bm,tiled", [(70, 128, 0), (70, 256, 0), (300, 256, 0), (512, 256, 0), (70, 128, 1),
+                                        (300, 256, 1)])
+def test_gemm_swiglu_interleaved(M, bm, tiled, monkeypatch):
+    monkeypatch.setenv("SART_GEMM_BTILED", str(tiled))
     rng = np.random.default_rng(2 + M)
     F, K = 1024, 512
     A = rnd(rng, (M, K))
@@ -59,13 +64,15 @@ def test_gemm_swiglu_interleaved(M, bm):
                                            (512, 1536, 8960, 8, 128, 256), (300, 1536, 1536, 3, 128, 256),
                                            (129, 640, 512, 2, 256, 256), (1, 256, 512, 1, 256, 256),
                                            (640, 512, 256, 1, 64, 128)])
-def test_gemm_split_k(M, N, K, S, BN, BM):
+@pytest.mark.parametrize("tiled", [0, 1])
+def test_gemm_split_k(M, N, K, S, BN, BM, tiled, monkeypatch):
     """split-K partials (the RMSNorm/RoPE consumers sum them in split order)"""
     rng = np.random.default_rng(M + N + K)
     A, B = rnd(rng, (M, K)), rnd(rng, (N, K), 0.05)
     from paper_2505_13326_b200.sart import debug_gemm
     if S > 8:
         pytest.skip("splits > 8 not exposed")
+    monkeypatch.setenv("SART_GEMM_BTILED", str(tiled))   # pre-tiled weight layout (bulk copies)
     parts = debug_gemm(A, B, mode=0, splits=S, bn=BN, bm=BM)
     C = parts.astype(np.float64).reshape(-1, M, N).sum(axis=0)   # S = 1 returns [M][N]
     ref = bits_to_f32(A).astype(np.float64) @ bits_to_f32(B).astype(np.float64).T

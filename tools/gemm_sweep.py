@@ -1,4 +1,7 @@
-"""Sweep split-K / tile width of the tcgen05 GEMM on the C2 decode shapes (M = 512 rows)."""
+"""Sweep split-K / tile shape of the tcgen05 GEMM on the C2 decode shapes (M = 512 rows).
+
+    SART_GEMM_BENCH_COPIES=8 SWEEP_TILES=128x128,128x256 python tools/gemm_sweep.py o down
+SART_GEMM_BENCH_COPIES cycles over copies of the weights so they stream from HBM as in a step."""
 import os
 import sys
 
@@ -17,7 +20,8 @@ for name, (M, N, K) in shapes.items():
         continue
     A = rng.integers(0, 1 << 14, size=(M, K), dtype=np.uint16)
     B = rng.integers(0, 1 << 14, size=(N, K), dtype=np.uint16)
-    for bm, bn in ((128, 128), (128, 256), (256, 128), (256, 256)):
+    tiles = os.environ.get("SWEEP_TILES", "128x128,128x256,256x128,256x256")
+    for bm, bn in [tuple(int(v) for v in t.split("x")) for t in tiles.split(",")]:
         for S in (1, 2, 3, 4, 6, 8):
             if S > max(1, K // 128):
                 continue
