@@ -12,7 +12,7 @@
 // stand-alone kernel hides with full occupancy.)
 // Phase 2: one warp per row reduces the chunks (exact max with the lowest-v tie rule, so the
 // reduction order does not matter) and updates the row: history, EOS / cap, counters.
-constexpr int SCHUNK = 4096;
+constexpr int SCHUNK = 16384;   // 16 groups of 4 per thread: pruning bound warms up early
 
 __global__ void __launch_bounds__(256) k_sample_part(const float* __restrict__ logits, Dims D, Rows rows, Reqs reqs,
                                                       float* __restrict__ pkey, int* __restrict__ pv, int nchunk) {
@@ -32,12 +32,30 @@ __global__ void __launch_bounds__(256) k_sample_part(const float* __restrict__ l
   float bk = -INFINITY;
   int bv = 0x7fffffff;
   const int g_lo = c * (SCHUNK / 4), g_hi = min((c + 1) * (SCHUNK / 4), (D.V + 3) >> 2);
-  for (int g4 = g_lo + threadIdx.x; g4 < g_hi; g4 += blockDim.x) {
+  if (D.tau > 0.f && g_lo + (int)threadIdx.x < g_hi) {
+    // pilot: the first entry of this thread's first group seeds the pruning bound (it is a
+    // legitimate candidate; re-visiting it in the loop cannot change (bk, bv))
+    const int v = 4 * (g_lo + threadIdx.x);
+    if (!(mask_eos && v == D.eos)) {
+      const u32x4 w = philox4x32_10(u32x4{(uint32_t)(v >> 2), (uint32_t)s, rid, (uint32_t)b}, k0, k1);
+      better(bk, bv, (D.tau == 1.0f ? lg[v] : lg[v] / D.tau) + gumbel_from_word(w.x), v);
+    }
+  }
+  for (int base = g_lo; base < g_hi; base += blockDim.x) {   // uniform trip count (warp shuffles)
+    // best key held anywhere in the warp so far: a valid pruning bound for every lane
+    float wb = bk;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wb = fmaxf(wb, __shfl_xor_sync(0xffffffffu, wb, o));
+    const int g4 = base + threadIdx.x;
+    if (g4 >= g_hi) continue;
     const float4 l4 = (D.V % 4 == 0 && 4 * g4 + 3 < D.V) ? *reinterpret_cast<const float4*>(lg + 4 * g4)
                                          : make_float4(lg[4 * g4], 4 * g4 + 1 < D.V ? lg[4 * g4 + 1] : 0.f,
                                                        4 * g4 + 2 < D.V ? lg[4 * g4 + 2] : 0.f, 0.f);
     const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-    sample_group4(bk, bv, lv, 4 * g4, D.V, s, rid, (uint32_t)b, k0, k1, D.tau, mask_eos, D.eos);
+#ifdef SART_SAMPLE_NOPRUNE
+    wb = -INFINITY;
+#endif
+    sample_group4(bk, bv, lv, 4 * g4, D.V, s, rid, (uint32_t)b, k0, k1, D.tau, mask_eos, D.eos, wb);
   }
   __shared__ float sk[8];
   __shared__ int sv[8];

@@ -19,10 +19,20 @@ __device__ __forceinline__ void better(float& bk, int& bv, float k, int v) {
   if (k > bk || (k == bk && v < bv)) { bk = k; bv = v; }
 }
 
-// fold 4 consecutive vocab entries v0..v0+3 (v0 % 4 == 0) into (bk, bv)
+// Exact pruning (no change to any result): with E = -ln u >= 1 - u, the key l' + G = l' - ln E
+// is < l' - ln(1 - u), so an entry whose (1 - u) exceeds exp(l' - bound) (0.1% margin, which
+// covers the fp32 rounding of every step) cannot reach `bound` -- a key some entry already
+// has -- and its two logarithms are skipped.  bound = -inf disables pruning.
+__device__ __forceinline__ bool gumbel_cannot_reach(uint32_t w, float lp, float bound) {
+  const float one_minus_u = ((float)((1u << 24) - (w >> 8)) - 0.5f) * (1.0f / 16777216.0f);
+  return one_minus_u > __expf(lp - bound) * 1.001f;
+}
+
+// fold 4 consecutive vocab entries v0..v0+3 (v0 % 4 == 0) into (bk, bv); entries whose key
+// provably stays below `bound` are skipped (see gumbel_cannot_reach)
 __device__ __forceinline__ void sample_group4(float& bk, int& bv, const float* lv, int v0, int V, int s, uint32_t rid,
                                               uint32_t b, uint32_t k0, uint32_t k1, float tau, bool mask_eos,
-                                              int eos) {
+                                              int eos, float bound = -INFINITY) {
   u32x4 w{0, 0, 0, 0};
   if (tau > 0.f) w = philox4x32_10(u32x4{(uint32_t)(v0 >> 2), (uint32_t)s, rid, b}, k0, k1);
   const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
@@ -31,8 +41,13 @@ __device__ __forceinline__ void sample_group4(float& bk, int& bv, const float* l
     const int v = v0 + j;
     if (v >= V || (mask_eos && v == eos)) continue;
     float key;
-    if (tau > 0.f) key = (tau == 1.0f ? lv[j] : lv[j] / tau) + gumbel_from_word(ws[j]);
-    else key = lv[j];
+    if (tau > 0.f) {
+      const float lp = tau == 1.0f ? lv[j] : lv[j] / tau;
+      if (gumbel_cannot_reach(ws[j], lp, bound)) continue;
+      key = lp + gumbel_from_word(ws[j]);
+    } else {
+      key = lv[j];
+    }
     better(bk, bv, key, v);
   }
 }
