@@ -167,6 +167,37 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+
+def step_roofline(shape, n_avg, attn_bytes_step, ms_step, peaks):
+    """Whole decode step against its roofline: t_roofline = sum over kernels of
+    max(algorithmic bytes / HBM peak, flops / tensor peak), per decode step at the average
+    number of running rows n.  GEMMs: weights once per step + activations in/out; attention:
+    the device-counted algorithmic bytes (prefix once per request, suffixes, KV appends);
+    RMSNorm: fp32 residual read + bf16 out; sampler: fp32 logits written and read once."""
+    bw = peaks.get("hbm_gbs", 6650.0) * 1e9
+    tc = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1668.0)) * 1e12
+    d, L, V, F = shape.d_model, shape.n_layers, shape.vocab, shape.d_ff
+    qkv = shape.qkv_dim
+    gemms = {"qkv": (d, qkv, 2), "o": (shape.n_heads * shape.head_dim, d, 4), "gate_up": (d, 2 * F, 2),
+             "down": (F, d, 4)}
+    per = {}
+    for name, (K, N, ob) in gemms.items():
+        by = N * K * 2 + n_avg * K * 2 + n_avg * N * ob
+        fl = 2.0 * n_avg * N * K
+        per[name] = L * max(by / bw, fl / tc)
+    by = V * d * 2 + n_avg * d * 2 + n_avg * V * 4
+    per["lm_head"] = max(by / bw, 2.0 * n_avg * V * d / tc)
+    per["attention"] = attn_bytes_step / bw
+    per["rmsnorm"] = (2 * L + 1) * n_avg * d * (4 + 2) / bw
+    per["sampler"] = n_avg * V * 4 / bw
+    t = sum(per.values())
+    return {"t_roofline_ms": t * 1e3, "t_measured_ms": ms_step, "frac": t * 1e3 / ms_step if ms_step > 0 else None,
+            "n_avg_running_rows": n_avg, "per_kernel_ms": {k: v * 1e3 for k, v in per.items()},
+            "peaks": {"hbm_gbs": bw / 1e9, "bf16_tflops": tc / 1e12,
+                      "tc_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernels inside a long step)"},
+            "t_measured": "timed region / decode steps (includes admission, prefill and boundaries)"}
+
+
 # ------------------------------------------------------------------ GPU arm
 def main():
     args = parse()
@@ -257,16 +288,26 @@ def main():
     attn_bytes = q1["attn_bytes"] - q0["attn_bytes"]
     n_attn = max(1, q1["attn_launches"] - q0["attn_launches"])
     peaks = load_peaks()
+    try:   # ncu --set full capture of the same kernel in the same workload (tools/attn_traffic.py)
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "attn_traffic.json")))
+    except Exception:
+        traffic = {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     achieved = attn_bytes / (attn_ms / 1e3) / 1e9 if attn_ms > 0 else 0.0
     roofline = {"bound": "hbm", "kernel": "k_attn_cascade + k_attn_merge (cascade decode attention)",
                 "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": None,
+                "traffic": traffic.get("dram_bytes_per_launch"),
+                "traffic_source": traffic.get("source", "no ncu capture committed (profiles/attn_traffic.json)"),
+                "traffic_algorithmic_bytes_at_capture": traffic.get("algorithmic_bytes_per_launch"),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s",
                 "bytes_per_launch": attn_bytes / n_attn, "launch_avg_ms": attn_ms / n_attn,
                 "launches_measured": n_attn,
                 "measured_over": "1 eager window after the timed region (%d decode steps)" % (sp1["steps"] - sp0["steps"]),
                 "attn_ms_per_step": attn_ms / max(1, sp1["steps"] - sp0["steps"])}
+
+    # whole decode step vs its roofline; attention bytes per step from the accounted window
+    step_rl = step_roofline(shape, tokens / max(1, dec_steps), attn_bytes / max(1, sp1["steps"] - sp0["steps"]),
+                            ms_max / max(1, dec_steps), peaks)
 
     # ---------------- e2e: the public C-ABI path with host buffers, H2D/D2H inside the timed region
     e2e = None
@@ -320,7 +361,7 @@ def main():
                 "requests_per_s": fin_all / (ms_max / 1e3), "decode_steps_timed": dec_steps,
                 "prefill_ms_timed": p1["prefill_ms"] - p0["prefill_ms"],
                 "branch_tokens_timed": tok_all, "gpu_launches": launches, "clocks": clocks,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e}
+                "roofline": roofline, "step_roofline": step_rl, "cpu_baseline": cpu, "e2e": e2e}
         print(json.dumps(line), flush=True)
     eng.close()
     if world > 1:

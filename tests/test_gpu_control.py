@@ -80,3 +80,60 @@ def test_paper_defaults_many_requests():
     cap, T, bs = 96, 16, 16
     reqs = gen_requests(12, shape, 8, 4, 0.5, 4, cap, T, eos_id=1, p_range=(20, 120), root_seed=11)
     run_pair(shape, reqs, bs, nb=3 * (8 * 6 + 8), T=T, cap=cap, B=40, check_every=1)
+
+
+def _mixed_requests(rng, shape, n, cap, T, first_id, root_seed):
+    """n requests with independently drawn N, M, alpha, beta and prompt length (one engine
+    serves them all; T, cap and bs are per-engine)."""
+    from synth import Request, gen_prompt, gen_script
+    reqs = []
+    for i in range(n):
+        rid = first_id + i
+        N = int(rng.integers(1, 33))
+        M = int(rng.integers(1, N + 1))
+        alpha = float(np.float32(rng.choice([-1.0, 0.25, 0.5, 0.75])))
+        beta = int(rng.integers(-1, N)) if N > 1 else 0
+        sc = gen_script(rid, N, cap, T, "uniform", (1, cap), root_seed)
+        reqs.append(Request(rid, gen_prompt(rid, shape.vocab, 1, 1, 200, root_seed), N, M, alpha, beta, sc))
+    return reqs
+
+
+@pytest.mark.parametrize("bs,T", [(16, 1), (16, 4), (64, 16), (64, 5), (16, 16), (64, 1)])
+def test_many_mixed_requests_tight_pool(bs, T):
+    """PP2 randomized coverage at volume: 150 requests per engine (900 over the parameter
+    grid) with N up to 32, random M, alpha (incl. disabled), beta (incl. -1 -> N/2), a pool
+    and row limit that force commitment stalls and queuing; every window bit-exact."""
+    rng = np.random.default_rng(1000 * bs + T)
+    shape = SHAPES["tiny"]
+    cap = int(rng.integers(16, 120))
+    reqs = _mixed_requests(rng, shape, 150, cap, T, 0, 7 + T)
+    need = max(-(-(len(r.prompt) - 1) // bs) for r in reqs) + -(-cap // bs)
+    nb = int(need * 6)
+    run_pair(shape, reqs, bs, nb, T, cap, B=int(rng.integers(8, 64)))
+
+
+@pytest.mark.parametrize("policy", ["vanilla", "self_consist", "sart_noprune", "sart"])
+def test_policy_presets_match_oracle(policy):
+    """NEXT row f3: the comparison policies (tools/policies.py) on the same engine are
+    bit-exact with the oracle; Vanilla finalizes every request with its single branch and
+    Self-Consistency completes all N branches."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from tools.policies import POLICIES
+    from synth import Request, Script
+    p = POLICIES[policy]
+    shape = SHAPES["tiny"]
+    cap, T, bs = 96, 16, 16
+    reqs = gen_requests(10, shape, 8, p["M"], p["alpha"], p["beta"], cap, T, eos_id=1, p_range=(20, 120),
+                        root_seed=21)
+    if p["N"] < 8:
+        reqs = [Request(r.request_id, r.prompt, p["N"], p["M"], p["alpha"], p["beta"],
+                        Script(r.script.forced_len[:p["N"]], r.script.scores[:p["N"]],
+                               r.script.final_score[:p["N"]], r.script.answer[:p["N"]])) for r in reqs]
+    res = run_pair(shape, reqs, bs, nb=400, T=T, cap=cap, B=48)
+    if policy == "vanilla":
+        assert all(r["num_completed"] == 1 and r["num_pruned"] == 0 for r in res)
+    if policy == "self_consist":
+        assert all(r["num_completed"] == 8 and r["num_early_stopped"] == 0 for r in res)
+    if policy == "sart_noprune":
+        assert all(r["num_pruned"] == 0 and r["num_completed"] >= 2 for r in res)
