@@ -158,10 +158,13 @@ class ModelSource:
     A request with a script keeps its forced EOS step (O4) and script scores
     unless ``prm_scores`` is set."""
 
-    def __init__(self, model: Model, cfg: EngineConfig, prm_scores: bool = True):
+    def __init__(self, model: Model, cfg: EngineConfig, prm_scores: bool = True,
+                 prm_model: Optional[Model] = None, forced_tokens: Optional[dict] = None):
         self.m = model
         self.cfg = cfg
         self.prm = prm_scores
+        self.prm_model = prm_model      # row f2: separate PRM decoder (else the head on z)
+        self.forced = forced_tokens or {}   # teacher forcing: {rid: int[N][cap]}, y_s := [b][s-1]
         self.prefix = {}
         self.suffix = {}
         self.z = {}
@@ -186,12 +189,19 @@ class ModelSource:
             self.z[(r.rs.rid, r.b)] = z[i]
             sc = r.rs.req.script
             forced = int(sc.forced_len[r.b]) if sc is not None else 0
-            out.append(philox.sample(logits[i].astype(np.float32), r.ell + 1, r.rs.rid, r.b,
-                                     self.cfg.sampler_seed, self.cfg.temperature,
-                                     self.cfg.eos_id, forced))
+            y = philox.sample(logits[i].astype(np.float32), r.ell + 1, r.rs.rid, r.b,
+                              self.cfg.sampler_seed, self.cfg.temperature, self.cfg.eos_id, forced)
+            if r.rs.rid in self.forced:       # teacher forcing replaces the sampled token
+                y = int(self.forced[r.rs.rid][r.b][r.ell])
+            out.append(y)
         return out
 
     def _prm(self, r: Row) -> float:
+        if self.prm_model is not None:
+            # row f2, reading R42: the PRM reads prompt + y_1 .. y_{l-1} (the tokens whose
+            # policy KV entries exist) and scores the last of them
+            seq = list(int(t) for t in r.rs.req.prompt) + list(r.hist[: r.ell - 1])
+            return f32(self.prm_model.prm_model_score(seq))
         return f32(self.m.prm_score(self.z[(r.rs.rid, r.b)])[0])
 
     def score_running(self, r: Row, k: int) -> float:

@@ -27,6 +27,15 @@ Where the method reaches a plain result, this file writes the plain result:
     score = softmax(ReLU(z W1^T + b1) W2^T + b2)[1]   in [0, 1] (alpha = 0.5)
   "parity unpinned" as a model of the paper's PRM; its arithmetic is pinned
   by tests/test_oracle_model.py.
+* Separate PRM model ("a PRM ... evaluates the
+  quality of each intermediate step", "evaluated ... every T steps",
+  P:320 Qwen2.5-Math-PRM-7B): a second decoder of its own shape with the same
+  head.  Its score of a branch is the head applied to the final-norm hidden
+  state of the LAST token of the sequence it has read, computed here by one
+  full causal forward over that sequence (no cache):
+    prm_model_score(seq) = prm_score(forward(seq)[-1])
+  Which tokens it reads is reading R42 (DESIGN.md): prompt + y_1 .. y_{l-1}
+  for a branch with l generated tokens.
 
 All arithmetic is fp64; weights are the synth arrays (bf16-representable
 values) upcast to fp64.  Test infrastructure only (see oracle/__init__.py).
@@ -140,6 +149,28 @@ class Model:
             out.append({"k": k, "v": v})
             h = self._post_attn(l, h, o)
         return out
+
+    # -------------------------------------------------------------- full forward
+    def forward(self, tokens) -> np.ndarray:
+        """Causal forward of a whole token sequence at positions 0..n-1 without a cache
+        (the definition a KV cache reproduces); returns the final-norm hidden states z [n, d]."""
+        s = self.s
+        toks = np.asarray(tokens, dtype=np.int64)
+        n = len(toks)
+        h = self.W("embed")[toks].astype(np.float64)
+        pos = np.arange(n, dtype=np.float64)
+        g = s.n_heads // s.n_kv_heads
+        for l in range(s.n_layers):
+            q, k, v = self._qkv(l, h, pos)
+            o = np.zeros((n, s.n_heads, s.head_dim))
+            for i in range(s.n_heads):
+                o[:, i] = causal_attention(q[:, i], k[:, i // g], v[:, i // g])
+            h = self._post_attn(l, h, o)
+        return rmsnorm(h, self.W("final_norm"), s.rms_eps)
+
+    def prm_model_score(self, tokens) -> float:
+        """Separate-PRM-model score of a sequence (row f2): head on z of its last token."""
+        return float(self.prm_score(self.forward(tokens)[-1])[0])
 
     # -------------------------------------------------------------- decode
     def decode(self, tokens: np.ndarray, positions: np.ndarray, prefix_kv: List, suffix_kv: List,

@@ -70,6 +70,12 @@ SHAPES: Dict[str, ModelShape] = {
     "7B": ModelShape("7B", 28, 3584, 28, 4, 128, 18944, 152064),
     # BASELINE.json configs[4]: 48 layers, d=5120, GQA 40/8
     "14B": ModelShape("14B", 48, 5120, 40, 8, 128, 13824, 152064),
+    # Separate PRM decoders (NEXT row f2).  The PRM reads the policy's tokens, so its vocab is
+    # the policy's.  prm-tiny / prm-small pair with tiny / small in tests; PRM-7B is the
+    # Qwen2.5-Math-PRM-7B shape (= Qwen2.5-7B) over the 1.5B policy's vocab.
+    "prm-tiny": ModelShape("prm-tiny", 3, 384, 6, 2, 64, 768, 512),
+    "prm-small": ModelShape("prm-small", 2, 384, 3, 1, 128, 1024, 2048),
+    "PRM-7B": ModelShape("PRM-7B", 28, 3584, 28, 4, 128, 18944, 151936),
 }
 
 

@@ -311,3 +311,31 @@ def test_queued_branches_discarded_and_fcfs():
     assert [r["request_id"] for r in res] == [0, 1]
     assert res[0]["branch_state"] == [COMPLETED_EOS, COMPLETED_EOS, DISCARDED, DISCARDED]
     assert res[0]["num_discarded_queued"] == 2
+
+
+def test_prm_model_source_scores_the_read_prefix():
+    """Row f2 (reading R42): with a separate PRM model, every completed branch's final score
+    is the PRM's score of prompt + y_1 .. y_{len-1}, computed by one uncached forward; the
+    pool drains back to full."""
+    from oracle.engine import ModelSource
+    from oracle.model import Model
+    from synth import gen_prompt, gen_weights
+    pol, prm = SHAPES["tiny"], SHAPES["prm-tiny"]
+    cfg = EngineConfig(block_size=16, num_blocks=64, max_rows=64, T=4, cap=12, eos_id=1, temperature=1.0,
+                       sampler_seed=3)
+    pm = Model(prm, gen_weights(prm, "fp32", std=0.05, root_seed=91))
+    prompt = gen_prompt(0, pol.vocab, 1, 5, 5)
+    forced = np.random.default_rng(1).integers(2, pol.vocab, size=(3, 12)).astype(np.int32)
+    forced[0, 6] = 1                                   # branch 0 emits EOS at step 7
+    src = ModelSource(Model(pol, gen_weights(pol, "fp32", std=0.05)), cfg, prm_model=pm,
+                      forced_tokens={0: forced})
+    e = Engine(cfg, src)
+    e.admit(Request(0, prompt, 3, 3, -1.0, 0, None))
+    e.step(100)
+    r = e.collect()[0]
+    assert r["branch_len"] == [7, 12, 12] and r["num_completed"] == 3
+    for b in range(3):
+        L = r["branch_len"][b]
+        seq = [int(t) for t in prompt] + [int(t) for t in forced[b, : L - 1]]
+        assert r["branch_score"][b] == np.float32(pm.prm_model_score(seq))
+    assert e.stats()["free_blocks"] == 64

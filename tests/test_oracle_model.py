@@ -155,3 +155,41 @@ def test_causal_attention_equals_per_position_attention():
     Q, K, V = rng.standard_normal((n, hd)), rng.standard_normal((n, hd)) * 2, rng.standard_normal((n, hd))
     ref = np.stack([om.attention(Q[t], K[: t + 1], V[: t + 1]) for t in range(n)])
     assert np.allclose(om.causal_attention(Q, K, V), ref, atol=1e-12)
+
+
+# ------------------------------------------------------------------ separate PRM model (row f2)
+@pytest.mark.parametrize("shape_name,n", [("prm-tiny", 23), ("prm-small", 9), ("tiny", 1)])
+def test_forward_matches_independent_torch(shape_name, n):
+    """Model.forward (no cache) == the independent torch module's z at every position."""
+    shape = SHAPES[shape_name]
+    w = gen_weights(shape, "fp32", std=0.08, root_seed=77)
+    seq = gen_prompt(11, shape.vocab, 1, n, n)
+    z = om.Model(shape, w).forward(seq)
+    zr, _ = TorchRef(shape, w).forward([int(t) for t in seq])
+    assert z.shape == (n, shape.d_model)
+    assert np.allclose(z, zr.numpy(), rtol=0, atol=1e-10)
+
+
+def test_prm_model_score_closed_form_and_cache_identity():
+    """prm_model_score(seq) = sigmoid(l1 - l0) of the head on the torch module's last z, and
+    equals the head on the z the cached path (prefill + decode steps) produces for the same
+    last token (a KV cache reproduces the full causal forward exactly)."""
+    shape = SHAPES["prm-tiny"]
+    w = gen_weights(shape, "fp32", std=0.08, root_seed=78)
+    m = om.Model(shape, w)
+    prompt = gen_prompt(12, shape.vocab, 1, 7, 7)
+    gen = [int(x) for x in np.random.default_rng(6).integers(2, shape.vocab, 5)]
+    seq = [int(t) for t in prompt] + gen
+    zr, _ = TorchRef(shape, w).forward(seq)
+    zl = zr[-1].numpy()
+    hdn = np.maximum(zl @ w["prm_w1"].T.astype(np.float64) + w["prm_b1"], 0)
+    lg = hdn @ w["prm_w2"].T.astype(np.float64) + w["prm_b2"]
+    assert abs(m.prm_model_score(seq) - 1.0 / (1.0 + np.exp(-(lg[1] - lg[0])))) < 1e-12
+    pre = m.prefill(prompt)
+    suf = [{"k": [], "v": []} for _ in range(shape.n_layers)]
+    P = len(prompt)
+    for s in range(1, len(gen) + 1):          # decode inputs: prompt[P-1], gen[0..]
+        tok = prompt[-1] if s == 1 else gen[s - 2]
+        z, _ = m.decode(np.array([tok]), np.array([P - 2 + s]), [pre], [suf])
+    # the last decode step consumed gen[-2] at position P+len(gen)-2 == seq[:-1]'s last token
+    assert abs(float(m.prm_score(z)[0]) - m.prm_model_score(seq[:-1])) < 1e-12
