@@ -101,6 +101,20 @@ typedef struct {
   int32_t enable_forced_tokens; /* allocate teacher-forcing buffers (tests)          */
   int32_t debug_capture;      /* keep per-layer attention outputs of the last step   */
   int32_t profile;            /* time the attention kernels with CUDA events         */
+  /* NEXT row f2: a separate PRM decoder instead of the
+   * 2-way head on the policy's hidden state.  prm_n_layers == 0: the head (row a8).
+   * prm_n_layers > 0: a second pre-norm GQA decoder of these dims (vocab, rope_theta,
+   * rms_eps and dtype are the policy's; head_dim 64 or 128; bf16 needs prm_d_ff % 128 == 0)
+   * with its own 2-way head.  At every boundary it reads each branch's tokens decoded in
+   * the window through its own paged KV cache -- the SAME block ids as the policy's pool
+   * (so reclamation and compaction cover both), the prompt prefix prefilled once per
+   * request -- and scores the last of them (reading R42: the PRM has read prompt + y_1 ..
+   * y_{l-1} after l generated tokens).  prm_host_weights: optional HOST blob in the
+   * host_weights layout with the PRM dims (its lm_head is unused); NULL -> generated on the
+   * device from prm_weight_seed.  num_blocks == 0 sizes the pool for both caches. */
+  int32_t prm_n_layers, prm_d_model, prm_n_heads, prm_n_kv_heads, prm_head_dim, prm_d_ff;
+  uint64_t prm_weight_seed;
+  const void* prm_host_weights;
 } sart_config;
 
 /* Create an engine.  Errors: EINVAL (shape/range), ENOMEM (allocation failure, or
@@ -265,6 +279,9 @@ typedef struct {
   double attn_bytes;       /* algorithmic KV bytes those launches had to move    */
   int64_t kernel_launches; /* kernels this library launched                      */
   double prefill_ms;       /* host-observed prefill time                         */
+  double prm_ms;           /* GPU time of the f2 PRM passes (CUDA events)         */
+  int64_t prm_tokens;      /* suffix entries the PRM model read in those passes   */
+  int64_t prm_passes;      /* boundaries with a PRM pass                          */
 } sart_profile;
 int sart_get_profile(sart_ctx* ctx, sart_profile* out);
 /* Turn per-launch attention timing on or off.  While on, decode steps are launched eagerly

@@ -8,5 +8,5 @@ the binding raises.
 """
 from .sart import (SartError, Engine, SartConfig, load_library, SART_BF16, SART_FP32,  # noqa: F401
                    SART_ATTN_CASCADE, SART_ATTN_FLAT, DBG_LOGITS, DBG_TOKENS, DBG_ROWIDS,
-                   DBG_SCORES, DBG_ATTN, DBG_Z, BR_QUEUED, BR_RUNNING, BR_COMPLETED_EOS,
+                   DBG_SCORES, DBG_ATTN, DBG_Z, DBG_PRM_SCORES, BR_QUEUED, BR_RUNNING, BR_COMPLETED_EOS,
                    BR_COMPLETED_CAP, BR_PRUNED, BR_EARLY_STOPPED, BR_DISCARDED)

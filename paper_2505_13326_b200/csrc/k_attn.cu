@@ -115,7 +115,46 @@ __global__ void __launch_bounds__(128) k_attn_prefill(const T* __restrict__ q, c
   auto loc = [=] __device__(int j, long long& blk, int& t) { blk = ptab[j / bs]; t = j % bs; };
   attend_one<T, HD>(qs, src, p + 1, loc, out + ((long long)i * D.qh + head) * HD, nullptr);
 }
+
+// f2 PRM pass: query i is suffix entry e = sf_ent[i] of batch row sf_row[i] (-1: padding),
+// attending to [prefix ; suffix entries 0..e] (its own entry was appended by this layer).
+template <typename T, int HD>
+__global__ void __launch_bounds__(128) k_attn_suffix(const T* __restrict__ q, const T* __restrict__ pool,
+                                                     T* __restrict__ out, Dims D, int layer, Rows rows, Reqs reqs,
+                                                     const int* __restrict__ sf_row, const int* __restrict__ sf_ent) {
+  const int i = blockIdx.x, head = blockIdx.y;
+  const int r = sf_row[i];
+  if (r < 0) return;
+  const int e = sf_ent[i];
+  __shared__ float qs[HD];
+  for (int x = threadIdx.x; x < HD; x += blockDim.x) qs[x] = to_f(q[((long long)i * D.qh + head) * HD + x]);
+  __syncthreads();
+  const int slot = rows.slot[r];
+  const int npre = reqs.P[slot] - 1;
+  const int* ptab = reqs.prefix + (long long)slot * D.MPB;
+  const int* rtab = rows.table + (long long)r * D.MBR;
+  const int bs = D.bs;
+  KVSrc<T, HD> src{pool, D, layer, head / D.g};
+  auto loc = [=] __device__(int j, long long& blk, int& t) {
+    if (j < npre) { blk = ptab[j / bs]; t = j % bs; }
+    else { j -= npre; blk = rtab[j / bs]; t = j % bs; }
+  };
+  attend_one<T, HD>(qs, src, npre + e + 1, loc, out + ((long long)i * D.qh + head) * HD, nullptr);
+}
 }  // namespace
+
+template <typename T>
+void launch_attn_suffix(const T* q, const T* pool, T* out, Dims D, int layer, Rows rows, Reqs reqs,
+                        const int* sf_row, const int* sf_ent, int n, cudaStream_t s) {
+  if (n <= 0) return;
+  dim3 grid(n, D.qh);
+  if (D.hd == 128) k_attn_suffix<T, 128><<<grid, 128, 0, s>>>(q, pool, out, D, layer, rows, reqs, sf_row, sf_ent);
+  else k_attn_suffix<T, 64><<<grid, 128, 0, s>>>(q, pool, out, D, layer, rows, reqs, sf_row, sf_ent);
+}
+template void launch_attn_suffix<float>(const float*, const float*, float*, Dims, int, Rows, Reqs, const int*,
+                                        const int*, int, cudaStream_t);
+template void launch_attn_suffix<bf16>(const bf16*, const bf16*, bf16*, Dims, int, Rows, Reqs, const int*,
+                                       const int*, int, cudaStream_t);
 
 template <typename T>
 void launch_attn_decode_simple(const T* q, const T* pool, T* out, float* dbg, Dims D, int layer, Rows rows,

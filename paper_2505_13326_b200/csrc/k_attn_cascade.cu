@@ -399,19 +399,42 @@ __global__ void __launch_bounds__(256) k_attn_merge(const float* __restrict__ pa
 // Prompt positions of a batched prefill (Alg. 1 L15): CTA = (64-position query block of one
 // request, q head); 4 warps x 16 query rows; K/V of key positions [64 kb, 64 kb + 64) staged
 // through a 2-stage bulk-copy ring; the last key block is masked causally.
-template <int HD>
+//
+// SUF (row f2, the PRM pass): the CTA is a 64-entry block of one batch row's new suffix
+// entries; keys live in a virtual index space [prefix blocks (pbase = ceil((P-1)/bs) * bs
+// slots, slots >= P-1 masked) ; suffix entries], so every 64-key stage is whole pages of one
+// table and the causal test stays "key index <= query index".
+template <int HD, bool SUF>
 __global__ void __launch_bounds__(128) k_attn_prefill_tc(const bf16* __restrict__ q, const bf16* __restrict__ pool,
                                                          bf16* __restrict__ out, Dims D, int layer, Reqs reqs,
-                                                         const int4* __restrict__ blocks) {
+                                                         const int4* __restrict__ blocks, Rows rows, SufChunk sc) {
   constexpr int KT = 64;                                   // key tokens per stage
   extern __shared__ __align__(128) uint8_t praw[];
   bf16 (*ks)[KT * HD] = reinterpret_cast<bf16 (*)[KT * HD]>(praw);
   bf16 (*vs)[KT * HD] = reinterpret_cast<bf16 (*)[KT * HD]>(praw + 2 * KT * HD * sizeof(bf16));
   uint64_t* full = reinterpret_cast<uint64_t*>(praw + 4 * KT * HD * sizeof(bf16));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int4 blk = blocks[blockIdx.x];                     // {first batch row, rows, slot, first position}
   const int head = blockIdx.y, h = head / D.g;
-  const int r0 = blk.x, nr = blk.y, slot = blk.z, p0 = blk.w;
+  int r0, nr, slot, p0;                                    // first batch token, tokens, slot, first key index
+  int npre = 0x7fffffff, pbase = 0x7fffffff;               // masked prefix padding [npre, pbase); suffix base
+  const int* rtab = nullptr;
+  if constexpr (SUF) {
+    const int nqb = (sc.jn + KT - 1) / KT;
+    const int rl = blockIdx.x / nqb, qb = blockIdx.x % nqb, row = sc.r0 + rl;
+    const int cnt = rows.ell[row] - sc.ell_ws[row];
+    const int ja = sc.j0 + qb * KT;
+    nr = min(KT, min(cnt, sc.j0 + sc.jn) - ja);
+    if (nr <= 0) return;
+    r0 = rl * sc.jn + qb * KT;
+    slot = rows.slot[row];
+    npre = reqs.P[slot] - 1;
+    pbase = (npre + D.bs - 1) / D.bs * D.bs;
+    p0 = pbase + sc.ell_ws[row] + ja;
+    rtab = rows.table + (long long)row * D.MBR;
+  } else {
+    const int4 blk = blocks[blockIdx.x];                   // {first batch row, rows, slot, first position}
+    r0 = blk.x; nr = blk.y; slot = blk.z; p0 = blk.w;
+  }
   const int nkey = p0 + nr;                                // keys 0 .. p0 + nr - 1
   const int nkb = (nkey + KT - 1) / KT;
   const int* ptab = reqs.prefix + (long long)slot * D.MPB;
@@ -431,7 +454,7 @@ __global__ void __launch_bounds__(128) k_attn_prefill_tc(const bf16* __restrict_
     mb_expect(&full[st], 2u * pieces * tpb * HD * 2);
     for (int pc = 0; pc < pieces; ++pc) {
       const int tok = t0 + pc * tpb;
-      const long long b = ptab[tok / D.bs];
+      const long long b = tok < pbase ? ptab[tok / D.bs] : rtab[(tok - pbase) / D.bs];
       const int inb = tok % D.bs;
       bulk_g2s(s_u32(ks[st] + pc * tpb * HD), pool + kv_tile_off(D, layer, b, 0, h) + (long long)inb * HD,
                tpb * HD * 2, &full[st]);
@@ -489,7 +512,7 @@ __global__ void __launch_bounds__(128) k_attn_prefill_tc(const bf16* __restrict_
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int kp = kpos + nt * 8 + (e & 1);
-            if (kp > (e < 2 ? pos0 : pos1)) s[nt][e] = -INFINITY;      // causal (also beyond nkey)
+            if (kp > (e < 2 ? pos0 : pos1) || (kp >= npre && kp < pbase)) s[nt][e] = -INFINITY;   // causal, padding
           }
         float mx0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
         float mx1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
@@ -694,25 +717,30 @@ __global__ void __launch_bounds__(1024) k_attn_account(Dims D, Rows rows, Reqs r
 void launch_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat, cudaStream_t s) {
   k_attn_plan<<<1, 1024, 0, s>>>(D, rows, reqs, pl, n, flat);
 }
+template <int HD, bool SUF>
+static void launch_pf(dim3 grid, const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Reqs reqs,
+                      const int4* blocks, Rows rows, SufChunk c, cudaStream_t s) {
+  const size_t sm = 4 * 64 * (size_t)HD * sizeof(bf16) + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attn_prefill_tc<HD, SUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  k_attn_prefill_tc<HD, SUF><<<grid, 128, sm, s>>>(q, pool, out, D, layer, reqs, blocks, rows, c);
+}
 void launch_attn_prefill_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Reqs reqs,
                             const int4* blocks, int nblocks, cudaStream_t s) {
   if (nblocks <= 0) return;
   dim3 grid(nblocks, D.qh);
-  const size_t sm = 4 * 64 * (size_t)D.hd * sizeof(bf16) + 64;
-  static bool a128 = false, a64 = false;
-  if (D.hd == 128) {
-    if (!a128) {
-      cudaFuncSetAttribute(k_attn_prefill_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      a128 = true;
-    }
-    k_attn_prefill_tc<128><<<grid, 128, sm, s>>>(q, pool, out, D, layer, reqs, blocks);
-  } else {
-    if (!a64) {
-      cudaFuncSetAttribute(k_attn_prefill_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      a64 = true;
-    }
-    k_attn_prefill_tc<64><<<grid, 128, sm, s>>>(q, pool, out, D, layer, reqs, blocks);
-  }
+  if (D.hd == 128) launch_pf<128, false>(grid, q, pool, out, D, layer, reqs, blocks, Rows{}, SufChunk{}, s);
+  else launch_pf<64, false>(grid, q, pool, out, D, layer, reqs, blocks, Rows{}, SufChunk{}, s);
+}
+void launch_attn_suffix_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
+                           SufChunk c, cudaStream_t s) {
+  if (c.nrow <= 0 || c.jn <= 0) return;
+  dim3 grid(c.nrow * ((c.jn + 63) / 64), D.qh);
+  if (D.hd == 128) launch_pf<128, true>(grid, q, pool, out, D, layer, reqs, nullptr, rows, c, s);
+  else launch_pf<64, true>(grid, q, pool, out, D, layer, reqs, nullptr, rows, c, s);
 }
 void launch_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s) {
   launch_pdl(k_attn_items, dim3(1), dim3(1024), 0, s, D, rows, reqs, pl);

@@ -397,7 +397,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         long long blk = 0;
         int sib = 0;
         if (gm < M) {
-          if (epi.a.pf_slot) {
+          if (epi.a.sf_row) {                  // f2 PRM pass: suffix entry of a batch row
+            const int row = epi.a.sf_row[gm];
+            if (row >= 0) {
+              const int l = epi.a.pf_pos[gm];
+              pos = epi.reqs.P[epi.rows.slot[row]] - 1 + l;
+              blk = epi.rows.table[(long long)row * D.MBR + l / D.bs];
+              sib = l % D.bs;
+              kv_ok = true;
+            }
+          } else if (epi.a.pf_slot) {
             pos = epi.a.pf_pos[gm];
             blk = epi.reqs.prefix[(long long)epi.a.pf_slot[gm] * D.MPB + pos / D.bs];
             sib = pos % D.bs;

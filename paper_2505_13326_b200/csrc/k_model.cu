@@ -120,7 +120,14 @@ __global__ void k_rope_append(const float* __restrict__ parts, int np, long long
   int r = blockIdx.x;
   int pos, blk, slot_in_blk;
   bool write_kv = true;
-  if (a.pf_slot) {
+  if (a.sf_row) {                                  // f2 PRM pass: suffix entry of a batch row
+    const int row = a.sf_row[r];
+    if (row < 0) return;
+    const int l = a.pf_pos[r];
+    pos = reqs.P[rows.slot[row]] - 1 + l;
+    blk = rows.table[(long long)row * D.MBR + l / D.bs];
+    slot_in_blk = l % D.bs;
+  } else if (a.pf_slot) {
     pos = a.pf_pos[r];
     blk = reqs.prefix[(long long)a.pf_slot[r] * D.MPB + pos / D.bs];
     slot_in_blk = pos % D.bs;
@@ -231,6 +238,48 @@ void launch_to_f32(const T* in, float* out, long long n, cudaStream_t s) {
   if (n > 0) k_to_f32<T><<<(int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(in, out, n);
 }
 
+// ------------------------------------------------------------ f2 PRM pass
+// Token list of one chunk: token t is per-row index j of row r; its input is the token that
+// produced suffix entry e = ell_ws[r] + j (entry 0: the last prompt token, R22; entry e > 0:
+// the generated token y_e = hist[e-1]).
+__global__ void k_prm_tokens(Dims D, Rows rows, Reqs reqs, SufChunk c, int* __restrict__ tok, int* __restrict__ row,
+                             int* __restrict__ ent) {
+  const int n = c.nrow * c.jn;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int r = c.r0 + t / c.jn, j = c.j0 + t % c.jn;
+    const int ws = c.ell_ws[r];
+    if (j < rows.ell[r] - ws) {
+      const int e = ws + j, slot = rows.slot[r];
+      const long long sb = (long long)slot * SART_MAXN + rows.b[r];
+      tok[t] = e == 0 ? reqs.first_tok[slot] : reqs.hist[sb * D.cap + (e - 1)];
+      row[t] = r;
+      ent[t] = e;
+    } else {
+      tok[t] = 0;
+      row[t] = -1;
+      ent[t] = 0;
+    }
+  }
+}
+void launch_prm_tokens(Dims D, Rows rows, Reqs reqs, SufChunk c, int* tok, int* row, int* ent, cudaStream_t s) {
+  const int n = c.nrow * c.jn;
+  if (n > 0) k_prm_tokens<<<(n + 255) / 256, 256, 0, s>>>(D, rows, reqs, c, tok, row, ent);
+}
+// zrow[r] = z of row r's last entry (the PRM's score position), when it lies in this chunk
+template <typename T>
+__global__ void k_prm_gather(const T* __restrict__ z, T* __restrict__ zrow, Rows rows, SufChunk c, int d) {
+  const int r = c.r0 + blockIdx.x;
+  const int jl = rows.ell[r] - c.ell_ws[r] - 1;
+  if (jl < c.j0 || jl >= c.j0 + c.jn) return;
+  const T* src = z + ((long long)blockIdx.x * c.jn + (jl - c.j0)) * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) zrow[(long long)r * d + i] = src[i];
+}
+template <typename T>
+void launch_prm_gather(const T* z, T* zrow, Dims D, Rows rows, SufChunk c, int d, cudaStream_t s) {
+  (void)D;
+  if (c.nrow > 0) k_prm_gather<T><<<c.nrow, 256, 0, s>>>(z, zrow, rows, c, d);
+}
+
 #define INST(T)                                                                                        \
   template void launch_init_tensor<T>(T*, long long, int, int, float, unsigned long long, cudaStream_t); \
   template void launch_embed<T>(const int*, const T*, float*, int, int, cudaStream_t);                  \
@@ -240,7 +289,8 @@ void launch_to_f32(const T* in, float* out, long long n, cudaStream_t s) {
                                       Rows, Reqs, RopeArgs, int, cudaStream_t);                         \
   template void launch_swiglu<T>(const float*, T*, int, int, cudaStream_t);                             \
   template void launch_convert<T>(const float*, T*, long long, cudaStream_t);                           \
-  template void launch_to_f32<T>(const T*, float*, long long, cudaStream_t);
+  template void launch_to_f32<T>(const T*, float*, long long, cudaStream_t);                           \
+  template void launch_prm_gather<T>(const T*, T*, Dims, Rows, SufChunk, int, cudaStream_t);
 INST(float)
 INST(bf16)
 

@@ -3,10 +3,22 @@
 #include "common.cuh"
 
 struct RopeArgs {
-  // decode mode (pf_slot == nullptr): per-row positions from Rows/Reqs.  Prefill mode: row i
-  // of the batch is prompt position pf_pos[i] of request slot pf_slot[i] (batched prefill).
+  // decode mode (pf_slot == sf_row == nullptr): per-row positions from Rows/Reqs.  Prefill
+  // mode: row i of the batch is prompt position pf_pos[i] of request slot pf_slot[i]
+  // (batched prefill).  Suffix mode (sf_row != nullptr, the f2 PRM pass): row i of the
+  // batch is suffix entry pf_pos[i] of batch row sf_row[i] (-1: padding, no KV written),
+  // at position P-1+entry, appended through that row's block table.
   const int* pf_slot;
   const int* pf_pos;
+  const int* sf_row = nullptr;
+};
+
+// One chunk of the f2 PRM pass: tokens t = (row - r0) * jn + (j - j0) for rows [r0, r0+nrow)
+// and per-row token index j in [j0, j0+jn); token j of a row is its suffix entry
+// ell_ws[row] + j, valid while j < ell[row] - ell_ws[row] (the entries decoded this window).
+struct SufChunk {
+  const int* ell_ws;
+  int r0, nrow, j0, jn;
 };
 
 // ---- model (k_model.cu)
@@ -73,6 +85,10 @@ template <typename T> void launch_attn_decode_simple(const T* q, const T* pool, 
 // over their requests' prefix blocks
 template <typename T> void launch_attn_prefill(const T* q, const T* pool, T* out, Dims D, int layer, Reqs reqs,
                                                const int* pf_slot, const int* pf_pos, int n, cudaStream_t s);
+// f2 PRM pass: causal attention of suffix-entry queries (row i: batch row sf_row[i], entry
+// pf_pos[i]) over [prefix ; that row's suffix entries 0..entry]
+template <typename T> void launch_attn_suffix(const T* q, const T* pool, T* out, Dims D, int layer, Rows rows,
+                                              Reqs reqs, const int* sf_row, const int* sf_ent, int n, cudaStream_t s);
 
 // cascade attention (k_attn_cascade.cu).  Per-window plan of work units.
 struct AttnPlan {
@@ -93,6 +109,10 @@ void launch_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s
 // tensor-core causal prefill: blocks[i] = {first batch row, rows (<= 64), slot, first position}
 void launch_attn_prefill_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Reqs reqs,
                             const int4* blocks, int nblocks, cudaStream_t s);
+// tensor-core variant for one f2 PRM chunk: 64-entry query blocks of each row's new suffix
+// entries over [prefix ; suffix entries 0..entry] (causal)
+void launch_attn_suffix_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
+                           SufChunk c, cudaStream_t s);
 void launch_attn_account(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, double* acc, cudaStream_t s);
 void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse,
                          Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s);
@@ -116,3 +136,8 @@ void launch_admit(const AdmitEvent* ev, int n_ev, int total_pop, int new_rows, i
 void launch_boundary(Dims D, Rows rows, Rows tmp, Reqs reqs, const float* prm_score, int* free_stack,
                      Ctr* ctr, DevResult* res, int* slot_row, int n, cudaStream_t s);
 void launch_window_begin(Ctr* ctr, int n, cudaStream_t s);
+// f2 PRM pass: token list of one chunk (tok: input token of the entry, row: batch row or -1,
+// ent: suffix entry), and the gather of each row's last-entry hidden state
+void launch_prm_tokens(Dims D, Rows rows, Reqs reqs, SufChunk c, int* tok, int* row, int* ent, cudaStream_t s);
+template <typename T> void launch_prm_gather(const T* z, T* zrow, Dims D, Rows rows, SufChunk c, int d,
+                                             cudaStream_t s);

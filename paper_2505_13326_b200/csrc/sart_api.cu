@@ -136,6 +136,18 @@ struct sart_ctx {
   double attn_ms = 0, attn_bytes = 0, attn_bytes_base = 0, prefill_ms = 0;
   long long attn_launches = 0, launches = 0;
 
+  // row f2: the separate PRM decoder is a sub-context holding its own dims, weights, KV pool
+  // and workspaces; it shares rows / reqs / stream with the policy ctx.
+  sart_ctx* prm = nullptr;
+  bool is_prm = false;
+  int* ell_ws = nullptr;                  // [R] rows.ell at the start of the window
+  int *prm_tok = nullptr, *prm_row = nullptr, *prm_ent = nullptr;   // one PRM chunk's tokens
+  int prm_chunk = 0;                      // tokens per PRM-pass chunk (<= W)
+  void* zrow = nullptr;                   // [R][d] final-norm state of each row's last entry
+  cudaEvent_t prm_ev[2] = {nullptr, nullptr};
+  double prm_ms = 0;
+  long long prm_tokens = 0, prm_passes = 0, prm_bt0 = 0;
+
   template <typename T> T* W_(int idx) const { return (T*)wblob + woff[idx]; }
 };
 
@@ -186,6 +198,15 @@ bool is_norm_tensor(const Dims& D, int idx) {
     if (e_ != cudaSuccess) {                                                               \
       ctx->poisoned = true;                                                                \
       return set_err(SART_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));        \
+    }                                                                                      \
+  } while (0)
+#define CK_VOID(x)                                                                         \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) {                                                               \
+      ctx->poisoned = true;                                                                \
+      set_err(SART_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));               \
+      return;                                                                              \
     }                                                                                      \
   } while (0)
 
@@ -364,28 +385,31 @@ void decode_step(sart_ctx* ctx, int n) {
 // loop are processed together, token i being position pf_pos[i] of request slot pf_slot[i];
 // chunks of up to PC tokens run all layers (a later chunk's tokens attend to the KV that
 // earlier chunks wrote).  The last layer only needs its K/V (the prefix has no output).
+//
+// ctx is the decoder being prefilled (the policy, or the f2 PRM model into its own pool);
+// src holds the batch's token lists (always the policy ctx).
 template <typename T>
-void prefill_batch(sart_ctx* ctx, int ntok) {
+void prefill_batch(sart_ctx* ctx, sart_ctx* src, int ntok) {
   const Dims& D = ctx->D;
   cudaStream_t s = ctx->st;
   for (int t0 = 0; t0 < ntok; t0 += ctx->PC) {
     const int c = std::min(ctx->PC, ntok - t0);
-    const RopeArgs ra{ctx->d_pf_slot + t0, ctx->d_pf_pos + t0};
+    const RopeArgs ra{src->d_pf_slot + t0, src->d_pf_pos + t0};
     // 64-position query blocks of each request segment of this chunk (tensor-core prefill)
     int nqb = 0;
     if constexpr (std::is_same<T, bf16>::value) {
       std::vector<int4> qb;
       for (int i = 0; i < c;) {
-        const int slot = ctx->pf_slot_h[t0 + i];
+        const int slot = src->pf_slot_h[t0 + i];
         int j = i;
-        while (j < c && ctx->pf_slot_h[t0 + j] == slot && j - i < 64) ++j;
-        qb.push_back(make_int4(i, j - i, slot, ctx->pf_pos_h[t0 + i]));
+        while (j < c && src->pf_slot_h[t0 + j] == slot && j - i < 64) ++j;
+        qb.push_back(make_int4(i, j - i, slot, src->pf_pos_h[t0 + i]));
         i = j;
       }
       nqb = (int)qb.size();
-      cudaMemcpyAsync(ctx->d_pf_blocks, qb.data(), sizeof(int4) * qb.size(), cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(src->d_pf_blocks, qb.data(), sizeof(int4) * qb.size(), cudaMemcpyHostToDevice, s);
     }
-    launch_embed<T>(ctx->d_prompt + t0, ctx->W_<T>(t_embed()), ctx->h, c, D.d, s);
+    launch_embed<T>(src->d_prompt + t0, ctx->W_<T>(t_embed()), ctx->h, c, D.d, s);
     ctx->launches++;
     int np_res = 0;
     for (int l = 0; l < D.L; ++l) {
@@ -394,7 +418,7 @@ void prefill_batch(sart_ctx* ctx, int ntok) {
       qkv_rope<T>(ctx, l, c, ra);
       if (l == D.L - 1) break;
       if constexpr (std::is_same<T, bf16>::value)
-        launch_attn_prefill_tc((bf16*)ctx->q, (bf16*)ctx->pool, (bf16*)ctx->o, D, l, ctx->reqs, ctx->d_pf_blocks, nqb,
+        launch_attn_prefill_tc((bf16*)ctx->q, (bf16*)ctx->pool, (bf16*)ctx->o, D, l, ctx->reqs, src->d_pf_blocks, nqb,
                                s);
       else
         launch_attn_prefill<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, D, l, ctx->reqs, ra.pf_slot, ra.pf_pos, c, s);
@@ -406,6 +430,61 @@ void prefill_batch(sart_ctx* ctx, int ntok) {
       ctx->launches += 3;
     }
   }
+}
+
+// Row f2: the separate PRM decoder reads every row's suffix entries decoded in this window
+// (entries ell_ws .. ell-1, reading R42) through its own paged KV -- the prefix was
+// prefilled at admission -- and its head scores the last entry's final-norm state.  Rows
+// are processed in chunks of at most m->W tokens (token j of a row at chunk offset
+// (row - r0) * jn + j - j0; entries past a row's count are padding: no KV write, no
+// attention, never gathered).  jmax bounds the entries per row (the window's steps).
+template <typename T>
+void prm_model_scores(sart_ctx* ctx, int n, int jmax) {
+  sart_ctx* m = ctx->prm;
+  const Dims& D = m->D;
+  cudaStream_t s = ctx->st;
+  CK_VOID(cudaEventRecord(m->prm_ev[0], s));
+  std::vector<SufChunk> chunks;
+  if (jmax <= m->prm_chunk) {
+    const int G = std::max(1, m->prm_chunk / jmax);
+    for (int r0 = 0; r0 < n; r0 += G) chunks.push_back(SufChunk{ctx->ell_ws, r0, std::min(G, n - r0), 0, jmax});
+  } else {
+    const int J = std::max(64, m->prm_chunk / 64 * 64);
+    for (int r = 0; r < n; ++r)
+      for (int j0 = 0; j0 < jmax; j0 += J) chunks.push_back(SufChunk{ctx->ell_ws, r, 1, j0, std::min(J, jmax - j0)});
+  }
+  for (const SufChunk& c : chunks) {
+    const int nt = c.nrow * c.jn;
+    const RopeArgs ra{nullptr, m->prm_ent, m->prm_row};
+    launch_prm_tokens(D, m->rows, m->reqs, c, m->prm_tok, m->prm_row, m->prm_ent, s);
+    launch_embed<T>(m->prm_tok, m->W_<T>(t_embed()), m->h, nt, D.d, s);
+    m->launches += 2;
+    int np_res = 0;
+    for (int l = 0; l < D.L; ++l) {
+      launch_rmsnorm<T>(m->h, m->parts, np_res, m->W_<T>(t_layer(l, 0)), (T*)m->a, nullptr, nullptr, nt, D.d, D.eps,
+                        s);
+      qkv_rope<T>(m, l, nt, ra);
+      if constexpr (std::is_same<T, bf16>::value)
+        launch_attn_suffix_tc((bf16*)m->q, (bf16*)m->pool, (bf16*)m->o, D, l, m->rows, m->reqs, c, s);
+      else
+        launch_attn_suffix<T>((T*)m->q, (T*)m->pool, (T*)m->o, D, l, m->rows, m->reqs, m->prm_row, m->prm_ent, nt, s);
+      int np = proj<T>(m, (T*)m->o, m->W_<T>(t_layer(l, 3)), nt, D.d, D.qh * D.hd);
+      launch_rmsnorm<T>(m->h, m->parts, np, m->W_<T>(t_layer(l, 4)), (T*)m->a, nullptr, nullptr, nt, D.d, D.eps, s);
+      mlp_up<T>(m, l, nt);
+      np_res = proj<T>(m, (T*)m->act, m->W_<T>(t_layer(l, 7)), nt, D.d, D.F);
+      m->launches += 3;
+    }
+    launch_rmsnorm<T>(m->h, m->parts, np_res, m->W_<T>(t_final(D)), (T*)m->a, nullptr, nullptr, nt, D.d, D.eps, s);
+    launch_prm_gather<T>((T*)m->a, (T*)m->zrow, D, m->rows, c, D.d, s);
+    m->launches += 2;
+  }
+  gemm<T>(m, (T*)m->zrow, m->W_<T>(t_prm_w1(D)), m->fparams + m->f_prm_b1, m->prm_hid, n, D.d, D.d, GEMM_STORE);
+  launch_prm_head2(m->prm_hid, m->fparams + m->f_prm_w2, m->fparams + m->f_prm_b2, m->prm_score, n, D.d, s);
+  m->launches++;
+  CK_VOID(cudaEventRecord(m->prm_ev[1], s));
+  ctx->launches += m->launches;
+  m->launches = 0;
+  if (m->gemm_failed) ctx->gemm_failed = true;
 }
 
 template <typename T>
@@ -544,8 +623,15 @@ int fill(sart_ctx* ctx) {
     CK(cudaEventRecord(ctx->pf_ev[0], ctx->st));
     ctx->pf_slot_h.swap(ctx->pf_slot);
     ctx->pf_pos_h.swap(ctx->pf_pos);
-    if (ctx->bf16) prefill_batch<bf16>(ctx, ntok);
-    else prefill_batch<float>(ctx, ntok);
+    if (ctx->bf16) prefill_batch<bf16>(ctx, ctx, ntok);
+    else prefill_batch<float>(ctx, ctx, ntok);
+    if (ctx->prm) {   // f2: the PRM model's own prefix KV (same block ids)
+      if (ctx->bf16) prefill_batch<bf16>(ctx->prm, ctx, ntok);
+      else prefill_batch<float>(ctx->prm, ctx, ntok);
+      ctx->launches += ctx->prm->launches;
+      ctx->prm->launches = 0;
+      if (ctx->prm->gemm_failed) return set_err(SART_EINVAL, "GEMM shape unsupported by the tcgen05 kernel (PRM model)");
+    }
     CK(cudaEventRecord(ctx->pf_ev[1], ctx->st));
     CK(cudaGetLastError());
     ctx->pf_pending = true;
@@ -649,6 +735,10 @@ int run_window(sart_ctx* ctx) {
   ctx->ev_used = 0;
   launch_window_begin(ctx->ctr, n, ctx->st);
   ctx->launches++;
+  if (ctx->prm) {
+    CK(cudaMemcpyAsync(ctx->ell_ws, ctx->rows.ell, sizeof(int) * n, cudaMemcpyDeviceToDevice, ctx->st));
+    ctx->prm_bt0 = ctx->branch_tokens;
+  }
   if (ctx->bf16) {   // work units of the cascade attention for this window's batch
     launch_attn_plan(D, ctx->rows, ctx->reqs, ctx->plan, n, ctx->cfg.attn_mode == SART_ATTN_FLAT, ctx->st);
     ctx->launches++;
@@ -683,7 +773,9 @@ int run_window(sart_ctx* ctx) {
   }
   constexpr int POLL = 16;
   int polls = 0;
+  int enq = 0;   // decode steps enqueued this window (bounds the entries a row decoded)
   for (int k = 1; k <= D.T; ++k) {
+    enq = k;
     if (k > 1 && (k % POLL) == 1) {
       if (polls >= 2) {   // bound the run-ahead: wait for the poll two periods back
         CK(cudaEventSynchronize(ctx->poll_ev[polls & 1]));
@@ -708,13 +800,25 @@ int run_window(sart_ctx* ctx) {
   // rows of this window (debug), then the boundary: PRM head -> control kernel
   CK(cudaMemcpyAsync(ctx->dbg_slot, ctx->rows.slot, sizeof(int) * n, cudaMemcpyDeviceToDevice, ctx->st));
   CK(cudaMemcpyAsync(ctx->dbg_b, ctx->rows.b, sizeof(int) * n, cudaMemcpyDeviceToDevice, ctx->st));
-  prm_scores<T>(ctx, n);
-  launch_boundary(D, ctx->rows, ctx->tmp, ctx->reqs, ctx->prm_score, ctx->free_stack, ctx->ctr, ctx->res,
+  if (ctx->prm) {
+    prm_model_scores<T>(ctx, n, enq);
+    if (ctx->poisoned) return SART_ECUDA;
+    if (ctx->gemm_failed) return set_err(SART_EINVAL, "GEMM shape unsupported by the tcgen05 kernel (PRM model)");
+  } else {
+    prm_scores<T>(ctx, n);
+  }
+  launch_boundary(D, ctx->rows, ctx->tmp, ctx->reqs, ctx->prm ? ctx->prm->prm_score : ctx->prm_score, ctx->free_stack, ctx->ctr, ctx->res,
                   ctx->slot_row, n, ctx->st);
   ctx->launches++;
   CK(cudaGetLastError());
   int rc = read_boundary(ctx);
   if (rc) return rc;
+  if (ctx->prm) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->prm->prm_ev[0], ctx->prm->prm_ev[1]) == cudaSuccess) ctx->prm_ms += ms;
+    ctx->prm_passes++;
+    ctx->prm_tokens += ctx->h_ctr->branch_tokens - ctx->prm_bt0;
+  }
   if (ctx->cfg.profile) {
     for (int i = 0; i + 1 < ctx->ev_used; i += 2) {
       float ms = 0.f;
@@ -725,6 +829,96 @@ int run_window(sart_ctx* ctx) {
   return SART_OK;
 }
 }  // namespace
+
+// Weights (host blob or device-generated), fp32 epilogue vectors, RoPE table and the
+// per-token workspaces of one decoder: the policy, or the f2 PRM model (sub-context).
+int init_model(sart_ctx* ctx, const void* host_w, uint64_t seed, float wstd) {
+  const Dims& D = ctx->D;
+  const size_t es = ctx->bf16 ? 2 : 4;
+  const size_t W = ctx->W;
+  cudaError_t e;
+#define MC(x)                                                                   \
+  do {                                                                          \
+    e = (x);                                                                    \
+    if (e != cudaSuccess)                                                       \
+      return set_err(e == cudaErrorMemoryAllocation ? SART_ENOMEM : SART_ECUDA, \
+                     std::string(#x) + ": " + cudaGetErrorString(e));           \
+  } while (0)
+  // ---- weights
+  std::vector<size_t> sizes = tensor_sizes(D);
+  size_t total = 0;
+  for (size_t s : sizes) { ctx->woff.push_back(total); total += s; }
+  MC(cudaMalloc(&ctx->wblob, total * es));
+  if (host_w) {
+    MC(cudaMemcpy(ctx->wblob, host_w, total * es, cudaMemcpyHostToDevice));
+  } else {
+    for (size_t i = 0; i < sizes.size(); ++i) {
+      bool norm = is_norm_tensor(D, (int)i);
+      if (ctx->bf16)
+        launch_init_tensor<bf16>((bf16*)ctx->wblob + ctx->woff[i], (long long)sizes[i], (int)i, norm, wstd,
+                                 seed, ctx->st);
+      else
+        launch_init_tensor<float>((float*)ctx->wblob + ctx->woff[i], (long long)sizes[i], (int)i, norm,
+                                  wstd, seed, ctx->st);
+    }
+    MC(cudaGetLastError());
+  }
+  if (ctx->bf16) {
+    if (D.F % 128 != 0) {
+      return set_err(SART_EINVAL, "bf16 mode needs d_ff % 128 == 0 (fused SwiGLU tiles)");
+    }
+    bf16* tmpw = nullptr;
+    MC(cudaMalloc(&tmpw, sizeof(bf16) * 2 * (size_t)D.F * D.d));
+    for (int l = 0; l < D.L; ++l) launch_interleave_gate_up(ctx->W_<bf16>(t_layer(l, 5)), tmpw, D.F, D.d, ctx->st);
+    MC(cudaStreamSynchronize(ctx->st));
+    cudaFree(tmpw);
+  }
+  // fp32 copies of the small vectors used in epilogues
+  size_t nf = (size_t)D.L * D.qkv + D.d + 2 * (size_t)D.d + 2;
+  MC(dalloc(ctx, &ctx->fparams, nf * sizeof(float)));
+  ctx->f_bqkv = 0;
+  ctx->f_prm_b1 = (size_t)D.L * D.qkv;
+  ctx->f_prm_w2 = ctx->f_prm_b1 + D.d;
+  ctx->f_prm_b2 = ctx->f_prm_w2 + 2 * (size_t)D.d;
+  auto tof = [&](int idx, size_t off, size_t n) {
+    if (ctx->bf16) launch_to_f32<bf16>(ctx->W_<bf16>(idx), ctx->fparams + off, (long long)n, ctx->st);
+    else launch_to_f32<float>(ctx->W_<float>(idx), ctx->fparams + off, (long long)n, ctx->st);
+  };
+  for (int l = 0; l < D.L; ++l) tof(t_layer(l, 2), (size_t)l * D.qkv, D.qkv);
+  tof(t_prm_b1(D), ctx->f_prm_b1, D.d);
+  tof(t_prm_w2(D), ctx->f_prm_w2, 2 * (size_t)D.d);
+  tof(t_prm_b2(D), ctx->f_prm_b2, 2);
+  MC(cudaGetLastError());
+  // ---- RoPE table (fp64 on the host, stored fp32): [pos][cos(hd/2) | sin(hd/2)]
+  {
+    std::vector<float> cs((size_t)D.max_pos * D.hd);
+    const int half = D.hd / 2;
+    for (int p = 0; p < D.max_pos; ++p)
+      for (int i = 0; i < half; ++i) {
+        double inv = std::pow((double)D.theta, -2.0 * i / D.hd);
+        double ang = p * inv;
+        cs[(size_t)p * D.hd + i] = (float)std::cos(ang);
+        cs[(size_t)p * D.hd + half + i] = (float)std::sin(ang);
+      }
+    MC(dalloc(ctx, &ctx->rope_cs, cs.size() * sizeof(float), false));
+    MC(cudaMemcpy(ctx->rope_cs, cs.data(), cs.size() * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  MC(dalloc(ctx, &ctx->h, W * D.d * 4));
+  MC(dalloc(ctx, &ctx->parts, W * std::max(D.qkv, D.d) * 8 * 4, false));   // split-K partials (S <= 8)
+  ctx->qkv_cnt_cap = (D.qkv / D.hd) * ((int)((W + 127) / 128)) * 8;
+  MC(dalloc(ctx, &ctx->qkv_cnt, sizeof(int) * (size_t)ctx->qkv_cnt_cap));   // QKV split-K arrivals (zeroed)
+  if (!ctx->bf16) MC(dalloc(ctx, &ctx->gu, W * 2 * D.F * 4));   // bf16: fused SwiGLU epilogue
+  MC(dalloc(ctx, &ctx->z32, (size_t)D.R * D.d * 4));
+  MC(dalloc(ctx, &ctx->prm_hid, (size_t)D.R * D.d * 4));
+  MC(dalloc(ctx, &ctx->prm_score, (size_t)D.R * 4));
+  MC(dalloc(ctx, &ctx->a, W * D.d * es));
+  MC(dalloc(ctx, &ctx->q, W * D.qh * D.hd * es));
+  MC(dalloc(ctx, &ctx->o, W * D.qh * D.hd * es));
+  MC(dalloc(ctx, &ctx->act, W * D.F * es));
+  MC(dalloc(ctx, &ctx->zT, (size_t)D.R * D.d * es));
+#undef MC
+  return SART_OK;
+}
 
 // ====================================================================== C-ABI
 extern "C" {
@@ -747,6 +941,12 @@ int sart_destroy(sart_ctx* ctx) {
   if (!ctx) return SART_OK;
   cudaSetDevice(ctx->cfg.device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
+  if (ctx->prm) {
+    sart_destroy(ctx->prm);   // shares the stream; frees its own weights, pool, workspaces
+    ctx->prm = nullptr;
+  }
+  for (auto e : ctx->prm_ev)
+    if (e) cudaEventDestroy(e);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (auto e : ctx->poll_ev)
     if (e) cudaEventDestroy(e);
@@ -789,6 +989,15 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   if (!(cfg.temperature >= 0.f)) return set_err(SART_EINVAL, "temperature must be >= 0");
   if (cfg.select_mode != 0 && cfg.select_mode != 1) return set_err(SART_EINVAL, "select_mode");
   if (cfg.attn_mode != 0 && cfg.attn_mode != 1) return set_err(SART_EINVAL, "attn_mode");
+  if (cfg.prm_n_layers < 0) return set_err(SART_EINVAL, "prm_n_layers < 0");
+  if (cfg.prm_n_layers > 0) {   // row f2: separate PRM decoder
+    if (cfg.prm_d_model < 1 || cfg.prm_n_heads < 1 || cfg.prm_n_kv_heads < 1 || cfg.prm_d_ff < 1)
+      return set_err(SART_EINVAL, "PRM model dims must be positive");
+    if (cfg.prm_head_dim != 64 && cfg.prm_head_dim != 128) return set_err(SART_EINVAL, "prm_head_dim must be 64 or 128");
+    if (cfg.prm_n_heads % cfg.prm_n_kv_heads || cfg.prm_n_heads / cfg.prm_n_kv_heads > 16)
+      return set_err(SART_EINVAL, "prm_n_heads must be a multiple of prm_n_kv_heads with ratio <= 16");
+    if (cfg.prm_d_model % 8 || cfg.prm_d_ff % 8) return set_err(SART_EINVAL, "prm_d_model and prm_d_ff: multiples of 8");
+  }
 
   sart_ctx* ctx = new sart_ctx();
   ctx->cfg = cfg;
@@ -826,91 +1035,57 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     IC(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
     ctx->own_stream = true;
   }
-  // ---- weights
-  std::vector<size_t> sizes = tensor_sizes(D);
-  size_t total = 0;
-  for (size_t s : sizes) { ctx->woff.push_back(total); total += s; }
-  IC(cudaMalloc(&ctx->wblob, total * es));
-  if (cfg.host_weights) {
-    IC(cudaMemcpy(ctx->wblob, cfg.host_weights, total * es, cudaMemcpyHostToDevice));
-  } else {
-    for (size_t i = 0; i < sizes.size(); ++i) {
-      bool norm = is_norm_tensor(D, (int)i);
-      if (ctx->bf16)
-        launch_init_tensor<bf16>((bf16*)ctx->wblob + ctx->woff[i], (long long)sizes[i], (int)i, norm, cfg.weight_std,
-                                 cfg.weight_seed, ctx->st);
-      else
-        launch_init_tensor<float>((float*)ctx->wblob + ctx->woff[i], (long long)sizes[i], (int)i, norm,
-                                  cfg.weight_std, cfg.weight_seed, ctx->st);
-    }
-    IC(cudaGetLastError());
-  }
-  if (ctx->bf16) {
-    if (D.F % 128 != 0) {
-      set_err(SART_EINVAL, "bf16 mode needs d_ff % 128 == 0 (fused SwiGLU tiles)");
-      sart_destroy(ctx);
-      return SART_EINVAL;
-    }
-    bf16* tmpw = nullptr;
-    IC(cudaMalloc(&tmpw, sizeof(bf16) * 2 * (size_t)D.F * D.d));
-    for (int l = 0; l < D.L; ++l) launch_interleave_gate_up(ctx->W_<bf16>(t_layer(l, 5)), tmpw, D.F, D.d, ctx->st);
-    IC(cudaStreamSynchronize(ctx->st));
-    cudaFree(tmpw);
-  }
-  // fp32 copies of the small vectors used in epilogues
-  size_t nf = (size_t)D.L * D.qkv + D.d + 2 * (size_t)D.d + 2;
-  IC(dalloc(ctx, &ctx->fparams, nf * sizeof(float)));
-  ctx->f_bqkv = 0;
-  ctx->f_prm_b1 = (size_t)D.L * D.qkv;
-  ctx->f_prm_w2 = ctx->f_prm_b1 + D.d;
-  ctx->f_prm_b2 = ctx->f_prm_w2 + 2 * (size_t)D.d;
-  auto tof = [&](int idx, size_t off, size_t n) {
-    if (ctx->bf16) launch_to_f32<bf16>(ctx->W_<bf16>(idx), ctx->fparams + off, (long long)n, ctx->st);
-    else launch_to_f32<float>(ctx->W_<float>(idx), ctx->fparams + off, (long long)n, ctx->st);
-  };
-  for (int l = 0; l < D.L; ++l) tof(t_layer(l, 2), (size_t)l * D.qkv, D.qkv);
-  tof(t_prm_b1(D), ctx->f_prm_b1, D.d);
-  tof(t_prm_w2(D), ctx->f_prm_w2, 2 * (size_t)D.d);
-  tof(t_prm_b2(D), ctx->f_prm_b2, 2);
-  IC(cudaGetLastError());
-  // ---- RoPE table (fp64 on the host, stored fp32): [pos][cos(hd/2) | sin(hd/2)]
   {
-    std::vector<float> cs((size_t)D.max_pos * D.hd);
-    const int half = D.hd / 2;
-    for (int p = 0; p < D.max_pos; ++p)
-      for (int i = 0; i < half; ++i) {
-        double inv = std::pow((double)D.theta, -2.0 * i / D.hd);
-        double ang = p * inv;
-        cs[(size_t)p * D.hd + i] = (float)std::cos(ang);
-        cs[(size_t)p * D.hd + half + i] = (float)std::sin(ang);
-      }
-    IC(dalloc(ctx, &ctx->rope_cs, cs.size() * sizeof(float), false));
-    IC(cudaMemcpy(ctx->rope_cs, cs.data(), cs.size() * sizeof(float), cudaMemcpyHostToDevice));
+    const int rc = init_model(ctx, cfg.host_weights, cfg.weight_seed, cfg.weight_std);
+    if (rc) {
+      sart_destroy(ctx);
+      return rc;
+    }
   }
   // ---- state
   IC(alloc_rows(ctx, ctx->rows));
   IC(alloc_rows(ctx, ctx->tmp));
   IC(alloc_reqs(ctx));
+  if (cfg.prm_n_layers > 0) {   // row f2: the PRM decoder as a sub-context sharing rows / reqs / stream
+    sart_ctx* m = new sart_ctx();
+    ctx->prm = m;
+    m->is_prm = true;
+    m->cfg = cfg;
+    m->bf16 = ctx->bf16;
+    m->st = ctx->st;
+    m->D = D;
+    Dims& P = m->D;
+    P.L = cfg.prm_n_layers; P.d = cfg.prm_d_model; P.qh = cfg.prm_n_heads; P.kvh = cfg.prm_n_kv_heads;
+    P.hd = cfg.prm_head_dim; P.F = cfg.prm_d_ff; P.qkv = (P.qh + 2 * P.kvh) * P.hd; P.g = P.qh / P.kvh;
+    m->PC = ctx->PC;
+    // chunk of the boundary pass: all rows x T entries when that is small, else 8192 tokens
+    m->W = std::max(m->PC, (int)std::min<long long>(8192, (long long)((D.R + 63) / 64 * 64) * D.T));
+    m->prm_chunk = m->W;
+    if (const char* ev = getenv("SART_PRM_CHUNK"))   // tests: exercise the multi-chunk paths
+      m->prm_chunk = std::max(64, std::min(m->W, atoi(ev)));
+    m->rows = ctx->rows;
+    m->reqs = ctx->reqs;
+    {
+      const int rc = init_model(m, cfg.prm_host_weights, cfg.prm_weight_seed, cfg.weight_std);
+      if (rc) {
+        sart_destroy(ctx);
+        return rc;
+      }
+    }
+    IC(dalloc(m, &m->prm_tok, sizeof(int) * (size_t)m->W));
+    IC(dalloc(m, &m->prm_row, sizeof(int) * (size_t)m->W));
+    IC(dalloc(m, &m->prm_ent, sizeof(int) * (size_t)m->W));
+    IC(dalloc(m, &m->zrow, (size_t)D.R * P.d * es));
+    IC(cudaEventCreate(&m->prm_ev[0]));
+    IC(cudaEventCreate(&m->prm_ev[1]));
+    IC(dalloc(ctx, &ctx->ell_ws, sizeof(int) * (size_t)D.R));
+  }
   IC(dalloc(ctx, &ctx->ctr, sizeof(Ctr) + sizeof(int) * D.S));
   IC(dalloc(ctx, &ctx->res, sizeof(DevResult) * D.S));
   IC(dalloc(ctx, &ctx->slot_row, sizeof(int) * (size_t)D.S * SART_MAXN));
   IC(cudaMemset(ctx->slot_row, 0xff, sizeof(int) * (size_t)D.S * SART_MAXN));
   // ---- workspaces
-  const size_t W = ctx->W;
-  IC(dalloc(ctx, &ctx->h, W * D.d * 4));
-  IC(dalloc(ctx, &ctx->parts, W * std::max(D.qkv, D.d) * 8 * 4, false));   // split-K partials (S <= 8)
-  ctx->qkv_cnt_cap = (D.qkv / D.hd) * ((int)((W + 127) / 128)) * 8;
-  IC(dalloc(ctx, &ctx->qkv_cnt, sizeof(int) * (size_t)ctx->qkv_cnt_cap));   // QKV split-K arrivals (zeroed)
-  IC(dalloc(ctx, &ctx->gu, W * 2 * D.F * 4));
-  IC(dalloc(ctx, &ctx->z32, (size_t)D.R * D.d * 4));
   IC(dalloc(ctx, &ctx->logits, (size_t)D.R * D.V * 4));
-  IC(dalloc(ctx, &ctx->prm_hid, (size_t)D.R * D.d * 4));
-  IC(dalloc(ctx, &ctx->prm_score, (size_t)D.R * 4));
-  IC(dalloc(ctx, &ctx->a, W * D.d * es));
-  IC(dalloc(ctx, &ctx->q, W * D.qh * D.hd * es));
-  IC(dalloc(ctx, &ctx->o, W * D.qh * D.hd * es));
-  IC(dalloc(ctx, &ctx->act, W * D.F * es));
-  IC(dalloc(ctx, &ctx->zT, (size_t)D.R * D.d * es));
   IC(dalloc(ctx, &ctx->dbg_tok, (size_t)D.R * 4));
   IC(dalloc(ctx, &ctx->skey, (size_t)D.R * sample_chunks(D.V) * 4));
   IC(dalloc(ctx, &ctx->sv, (size_t)D.R * sample_chunks(D.V) * 4));
@@ -958,12 +1133,15 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   if (getenv("SART_NO_GRAPHS")) ctx->use_graphs = false;
   // ---- KV pool
   const size_t blk_bytes = (size_t)D.L * 2 * D.kvh * D.bs * D.hd * es;
+  // f2: the PRM cache uses the same block ids, so one block costs both decoders' pages
+  const size_t prm_blk_bytes =
+      ctx->prm ? (size_t)ctx->prm->D.L * 2 * ctx->prm->D.kvh * D.bs * ctx->prm->D.hd * es : 0;
   long long NB = cfg.num_blocks;
   if (NB <= 0) {
     size_t fr = 0, tot = 0;
     IC(cudaMemGetInfo(&fr, &tot));
     const size_t reserve = (size_t)3 << 30;
-    NB = fr > reserve ? (long long)((fr - reserve) / blk_bytes) : 0;
+    NB = fr > reserve ? (long long)((fr - reserve) / (blk_bytes + prm_blk_bytes)) : 0;
   }
   if (NB < cdiv(D.cap, D.bs)) {
     set_err(SART_ENOMEM, "KV pool cannot hold one branch of max_new_tokens");
@@ -972,6 +1150,10 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   }
   D.NB = NB;
   IC(dalloc(ctx, &ctx->pool, (size_t)NB * blk_bytes));
+  if (ctx->prm) {
+    ctx->prm->D.NB = NB;
+    IC(dalloc(ctx->prm, &ctx->prm->pool, (size_t)NB * prm_blk_bytes));
+  }
   IC(dalloc(ctx, &ctx->free_stack, sizeof(int) * (size_t)NB, false));
   {
     std::vector<int> fs(NB);
@@ -1182,7 +1364,7 @@ int sart_debug_fetch(sart_ctx* ctx, int32_t what, int32_t layer, void* host_out,
     case SART_DBG_LOGITS: need = (size_t)n * D.V * 4; src = ctx->logits; break;
     case SART_DBG_TOKENS: need = (size_t)n * 4; src = ctx->dbg_tok; break;
     case SART_DBG_SCORES:
-    case SART_DBG_PRM_SCORES: need = (size_t)n * 4; src = ctx->prm_score; break;
+    case SART_DBG_PRM_SCORES: need = (size_t)n * 4; src = ctx->prm ? ctx->prm->prm_score : ctx->prm_score; break;
     case SART_DBG_Z: need = (size_t)n * D.d * 4; src = ctx->z32; break;
     case SART_DBG_ATTN:
       if (!ctx->dbg_attn || layer < 0 || layer >= D.L) return set_err(SART_EINVAL, "needs debug_capture and a layer");
@@ -1317,6 +1499,9 @@ int sart_get_profile(sart_ctx* ctx, sart_profile* o) {
   o->attn_bytes = ctx->attn_bytes;
   o->kernel_launches = ctx->launches;
   o->prefill_ms = ctx->prefill_ms;
+  o->prm_ms = ctx->prm_ms;
+  o->prm_tokens = ctx->prm_tokens;
+  o->prm_passes = ctx->prm_passes;
   return SART_OK;
 }
 int sart_set_profile(sart_ctx* ctx, int32_t enable) {
@@ -1333,7 +1518,8 @@ int sart_set_profile(sart_ctx* ctx, int32_t enable) {
 int sart_reset_profile(sart_ctx* ctx) {
   if (!ctx) return set_err(SART_EINVAL, "null argument");
   ctx->attn_bytes_base += ctx->attn_bytes;
-  ctx->attn_ms = ctx->attn_bytes = ctx->prefill_ms = 0;
+  ctx->attn_ms = ctx->attn_bytes = ctx->prefill_ms = ctx->prm_ms = 0;
+  ctx->prm_tokens = ctx->prm_passes = 0;
   ctx->attn_launches = ctx->launches = 0;
   return SART_OK;
 }

@@ -41,6 +41,9 @@ class SartConfig(C.Structure):
         ("sampler_seed", C.c_uint64), ("select_mode", C.c_int32), ("attn_mode", C.c_int32),
         ("device", C.c_int32), ("stream", C.c_void_p), ("enable_forced_tokens", C.c_int32),
         ("debug_capture", C.c_int32), ("profile", C.c_int32),
+        ("prm_n_layers", C.c_int32), ("prm_d_model", C.c_int32), ("prm_n_heads", C.c_int32),
+        ("prm_n_kv_heads", C.c_int32), ("prm_head_dim", C.c_int32), ("prm_d_ff", C.c_int32),
+        ("prm_weight_seed", C.c_uint64), ("prm_host_weights", C.c_void_p),
     ]
 
 
@@ -92,7 +95,8 @@ class SartState(C.Structure):
 
 class SartProfile(C.Structure):
     _fields_ = [("attn_ms", C.c_double), ("attn_launches", C.c_int64), ("attn_bytes", C.c_double),
-                ("kernel_launches", C.c_int64), ("prefill_ms", C.c_double)]
+                ("kernel_launches", C.c_int64), ("prefill_ms", C.c_double), ("prm_ms", C.c_double),
+                ("prm_tokens", C.c_int64), ("prm_passes", C.c_int64)]
 
 
 _lib = None
@@ -176,7 +180,10 @@ class Engine:
                  max_rows: int = 0, max_requests: int = 0, max_prompt: int = 0, T: int = 400, cap: int = 4096,
                  eos_id: int = 1, temperature: float = 1.0, sampler_seed: int = 0, select_mode: int = 0,
                  attn_mode: int = SART_ATTN_CASCADE, device: int = 0, stream: int = 0,
-                 enable_forced_tokens: bool = False, debug_capture: bool = False, profile: bool = False):
+                 enable_forced_tokens: bool = False, debug_capture: bool = False, profile: bool = False,
+                 prm_shape=None, prm_host_weights: Optional[np.ndarray] = None, prm_weight_seed: int = 0):
+        """prm_shape (a synth.ModelShape, vocab = the policy's): the separate PRM decoder of
+        row f2; None -> the PRM head on the policy's hidden state."""
         self.lib = load_library()
         self.shape = shape
         self.cap, self.T = cap, T
@@ -197,9 +204,19 @@ class Engine:
         cfg.device, cfg.stream = device, stream or None
         cfg.enable_forced_tokens, cfg.debug_capture = int(enable_forced_tokens), int(debug_capture)
         cfg.profile = int(profile)
+        self._prm_weights = None
+        if prm_shape is not None:
+            if prm_shape.vocab != shape.vocab:
+                raise ValueError("the PRM model reads the policy's tokens: vocab must match")
+            cfg.prm_n_layers, cfg.prm_d_model, cfg.prm_n_heads = prm_shape.n_layers, prm_shape.d_model, prm_shape.n_heads
+            cfg.prm_n_kv_heads, cfg.prm_head_dim, cfg.prm_d_ff = prm_shape.n_kv_heads, prm_shape.head_dim, prm_shape.d_ff
+            cfg.prm_weight_seed = prm_weight_seed
+            if prm_host_weights is not None:
+                self._prm_weights = np.ascontiguousarray(prm_host_weights)
+                cfg.prm_host_weights = self._prm_weights.ctypes.data
         h = C.c_void_p()
         _check(self.lib.sart_init(C.byref(cfg), C.byref(h)))
-        self._weights = None
+        self._weights = self._prm_weights = None
         self.ctx = h
         self.cfg = cfg
 
