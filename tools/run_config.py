@@ -7,8 +7,12 @@ c3: 7B shape, 32 requests/GPU (the per-GPU share of 256 on 8 GPUs), N=16, M=4, c
     T=400, alpha 0.5, beta 8, scripted rewards (BJ configs[2]); admission is commitment-limited
 c5: 14B shape, 8192-token shared prompt, N=32, M=16, alpha 0.5, beta 16, cap 16384, T=400,
     1 request per GPU (BJ configs[4])
+c2p: C2's workload (1.5B, 64 requests, N=8, M=4, cap 4096, T=400) with PRM pruning
+    (alpha 0.5, beta 4) scored by a separate PRM decoder (row f2): --prm PRM-7B is the
+    Qwen2.5-Math-PRM-7B shape.  Scripted lengths, PRM-model scores.
 Values: branch-tokens/s over the timed windows (CUDA events), attention roofline over one
-extra eager window (same method as bench.py).
+extra eager window (same method as bench.py); with --prm also the PRM pass GPU time per
+boundary and its tensor-pipe rate (2 x matmul params x entries read, attention flops excluded).
 """
 import argparse
 import json
@@ -21,6 +25,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 CONFIGS = {
     "c1": dict(shape="tiny", n_req=1, N=4, M=2, alpha=0.5, beta=2, cap=64, T=16, p=(16, 16), B=64, bs=16),
     "c3": dict(shape="7B", n_req=32, N=16, M=4, alpha=0.5, beta=8, cap=8192, T=400, p=(64, 1024), B=1024, bs=64),
+    "c2p": dict(shape="1.5B", n_req=64, N=8, M=4, alpha=0.5, beta=4, cap=4096, T=400, p=(64, 1024), B=512, bs=64),
     "c5": dict(shape="14B", n_req=1, N=32, M=16, alpha=0.5, beta=16, cap=16384, T=400, p=(8193, 8193), B=64, bs=64),
 }
 
@@ -30,22 +35,27 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--windows", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--prm", default=None, help="separate PRM decoder shape (row f2), e.g. PRM-7B")
+    ap.add_argument("--requests", type=int, default=0, help="override the config's request count")
     a = ap.parse_args()
     import torch
     from paper_2505_13326_b200 import Engine
     from synth import SHAPES, gen_requests
-    c = CONFIGS[a.config]
+    c = dict(CONFIGS[a.config])
+    if a.requests:
+        c["n_req"] = a.requests
     shape = SHAPES[c["shape"]]
+    prm = SHAPES[a.prm] if a.prm else None
     stream = torch.cuda.current_stream()
     t0 = time.time()
     eng = Engine(shape, "bf16", weight_seed=3, block_size=c["bs"], num_blocks=0, max_rows=c["B"], max_requests=256,
                  max_prompt=c["p"][1] + 1, T=c["T"], cap=c["cap"], eos_id=1, temperature=1.0, sampler_seed=5,
-                 stream=stream.cuda_stream)
+                 stream=stream.cuda_stream, prm_shape=prm, prm_weight_seed=11)
     init_s = time.time() - t0
     reqs = gen_requests(c["n_req"], shape, c["N"], c["M"], c["alpha"], c["beta"], c["cap"], c["T"], eos_id=1,
                         p_range=c["p"])
     for r in reqs:
-        eng.admit(r)
+        eng.admit(r, use_script_scores=prm is None)     # with a PRM model its scores drive pruning
     if a.config == "c1":      # latency config: time the whole request (no warm-up)
         a.warmup, a.windows = 0, 1000
     t0 = time.time()
@@ -81,6 +91,19 @@ def main():
            "attn_frac_of_6455": att_b / (att_ms / 1e3) / 1e9 / 6455.3 if att_ms else None,
            "attn_ms_per_launch": att_ms / max(1, q1["attn_launches"] - q0["attn_launches"]),
            "init_s": init_s, "warmup_s": warm_s}
+    if prm is not None:
+        d, F, L = prm.d_model, prm.d_ff, prm.n_layers
+        params = L * (d * prm.qkv_dim + d * prm.n_heads * prm.head_dim + 3 * d * F) + d * d
+        passes = p1["prm_passes"] - p0["prm_passes"]
+        pms, ptok = p1["prm_ms"] - p0["prm_ms"], p1["prm_tokens"] - p0["prm_tokens"]
+        out.update({"prm_shape": a.prm, "prm_passes": passes, "prm_ms_per_pass": pms / max(1, passes),
+                    "prm_share_of_timed": pms / ms, "prm_entries_per_s": ptok / (pms / 1e3) if pms else None,
+                    "prm_matmul_TFLOPs": 2.0 * params * ptok / (pms / 1e3) / 1e12 if pms else None,
+                    "prm_frac_of_1385_TFLOPs": 2.0 * params * ptok / (pms / 1e3) / 1e12 / 1385.5 if pms else None,
+                    "pruned_total": None})
+        res = eng.collect()
+        out["pruned_total"] = sum(r["num_pruned"] for r in res)
+        out["early_stopped_total"] = sum(r["num_early_stopped"] for r in res)
     print(json.dumps(out), flush=True)
     eng.close()
 
