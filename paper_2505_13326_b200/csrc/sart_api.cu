@@ -21,6 +21,7 @@
 
 #include "../../include/sart.h"
 #include "kernels.h"
+#include <cuda_profiler_api.h>
 
 namespace {
 thread_local std::string g_last_error;
@@ -443,6 +444,11 @@ void prm_model_scores(sart_ctx* ctx, int n, int jmax) {
   sart_ctx* m = ctx->prm;
   const Dims& D = m->D;
   cudaStream_t s = ctx->st;
+  // SART_NCU_PRM_PASS=k: bracket the k-th pass (1-based) with cudaProfilerStart/Stop so
+  // that `ncu --profile-from-start off` captures exactly one PRM pass
+  static const int ncu_pass = getenv("SART_NCU_PRM_PASS") ? atoi(getenv("SART_NCU_PRM_PASS")) : 0;
+  const bool ncu_range = ncu_pass > 0 && ctx->prm_passes + 1 == ncu_pass;
+  if (ncu_range) cudaProfilerStart();
   CK_VOID(cudaEventRecord(m->prm_ev[0], s));
   std::vector<SufChunk> chunks;
   if (jmax <= m->prm_chunk) {
@@ -482,6 +488,7 @@ void prm_model_scores(sart_ctx* ctx, int n, int jmax) {
   launch_prm_head2(m->prm_hid, m->fparams + m->f_prm_w2, m->fparams + m->f_prm_b2, m->prm_score, n, D.d, s);
   m->launches++;
   CK_VOID(cudaEventRecord(m->prm_ev[1], s));
+  if (ncu_range) cudaProfilerStop();
   ctx->launches += m->launches;
   m->launches = 0;
   if (m->gemm_failed) ctx->gemm_failed = true;

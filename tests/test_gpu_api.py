@@ -64,6 +64,13 @@ def test_init_validation_codes():
     with pytest.raises(SartError) as e:
         eng(num_blocks=1)                                  # < ceil(cap / bs) = 2
     assert e.value.code == SART_ENOMEM
+    # row f2: a separate PRM decoder with an unsupported head_dim / GQA ratio / FFN width
+    for bad in (dict(head_dim=96), dict(n_kv_heads=4), dict(d_ff=1000)):
+        with pytest.raises(SartError) as e:
+            eng(prm_shape=dataclasses.replace(SHAPES["prm-tiny"], **bad))
+        assert e.value.code == SART_EINVAL, bad
+    with pytest.raises(ValueError):                        # the PRM reads the policy's vocab
+        eng(prm_shape=dataclasses.replace(SHAPES["prm-tiny"], vocab=1024))
 
 
 def run_model_mode(seed):
