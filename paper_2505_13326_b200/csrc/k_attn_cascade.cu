@@ -396,36 +396,41 @@ __global__ void __launch_bounds__(256) k_attn_merge(const float* __restrict__ pa
 }
 
 // ------------------------------------------------------------------ causal prefill (f1)
-// Prompt positions of a batched prefill (Alg. 1 L15): CTA = (64-position query block of one
-// request, q head); 4 warps x 16 query rows; K/V of key positions [64 kb, 64 kb + 64) staged
-// through a 2-stage bulk-copy ring; the last key block is masked causally.
+// Prompt positions of a batched prefill (Alg. 1 L15): CTA = (QP-position query block of one
+// request, HG q heads of one kv head); warp w = 16 query rows (tile w % QT) of head w / QT,
+// so each K/V stage -- key positions [64 kb, 64 kb + 64) through a 2-stage bulk-copy ring --
+// serves every q head of the GQA group (read once per group, not once per q head); the last
+// key block is masked causally.  QT, HG: pf_shape() (<= 8 warps).
 //
 // SUF (row f2, the PRM pass): the CTA is a 64-entry block of one batch row's new suffix
 // entries; keys live in a virtual index space [prefix blocks (pbase = ceil((P-1)/bs) * bs
 // slots, slots >= P-1 masked) ; suffix entries], so every 64-key stage is whole pages of one
 // table and the causal test stays "key index <= query index".
 template <int HD, bool SUF>
-__global__ void __launch_bounds__(128) k_attn_prefill_tc(const bf16* __restrict__ q, const bf16* __restrict__ pool,
+__global__ void __launch_bounds__(256) k_attn_prefill_tc(const bf16* __restrict__ q, const bf16* __restrict__ pool,
                                                          bf16* __restrict__ out, Dims D, int layer, Reqs reqs,
-                                                         const int4* __restrict__ blocks, Rows rows, SufChunk sc) {
+                                                         const int4* __restrict__ blocks, Rows rows, SufChunk sc,
+                                                         int QT, int HG) {
   constexpr int KT = 64;                                   // key tokens per stage
   extern __shared__ __align__(128) uint8_t praw[];
   bf16 (*ks)[KT * HD] = reinterpret_cast<bf16 (*)[KT * HD]>(praw);
   bf16 (*vs)[KT * HD] = reinterpret_cast<bf16 (*)[KT * HD]>(praw + 2 * KT * HD * sizeof(bf16));
   uint64_t* full = reinterpret_cast<uint64_t*>(praw + 4 * KT * HD * sizeof(bf16));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int head = blockIdx.y, h = head / D.g;
+  const int qt = warp % QT;                                // this warp's 16-row query tile
+  const int head = blockIdx.y * HG + warp / QT, h = head / D.g;
+  const int QP = 16 * QT;                                  // query positions per CTA
   int r0, nr, slot, p0;                                    // first batch token, tokens, slot, first key index
   int npre = 0x7fffffff, pbase = 0x7fffffff;               // masked prefix padding [npre, pbase); suffix base
   const int* rtab = nullptr;
   if constexpr (SUF) {
-    const int nqb = (sc.jn + KT - 1) / KT;
+    const int nqb = (sc.jn + QP - 1) / QP;
     const int rl = blockIdx.x / nqb, qb = blockIdx.x % nqb, row = sc.r0 + rl;
     const int cnt = rows.ell[row] - sc.ell_ws[row];
-    const int ja = sc.j0 + qb * KT;
-    nr = min(KT, min(cnt, sc.j0 + sc.jn) - ja);
+    const int ja = sc.j0 + qb * QP;
+    nr = min(QP, min(cnt, sc.j0 + sc.jn) - ja);
     if (nr <= 0) return;
-    r0 = rl * sc.jn + qb * KT;
+    r0 = rl * sc.jn + qb * QP;
     slot = rows.slot[row];
     npre = reqs.P[slot] - 1;
     pbase = (npre + D.bs - 1) / D.bs * D.bs;
@@ -463,14 +468,14 @@ __global__ void __launch_bounds__(128) k_attn_prefill_tc(const bf16* __restrict_
     }
   };
   // stale smem of a partial stage is multiplied by P = 0: keep it finite
-  for (int e = threadIdx.x; e < 4 * KT * HD / 8; e += 128) reinterpret_cast<uint4*>(praw)[e] = make_uint4(0, 0, 0, 0);
+  for (int e = threadIdx.x; e < 4 * KT * HD / 8; e += blockDim.x) reinterpret_cast<uint4*>(praw)[e] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   if (threadIdx.x == 0) {
     issue(0);
     if (nkb > 1) issue(1);
   }
   // Q fragments of this warp's 16 rows (zero beyond nr)
-  const int qr0 = warp * 16 + (lane >> 2), qr1 = qr0 + 8, cc = 2 * (lane & 3);
+  const int qr0 = qt * 16 + (lane >> 2), qr1 = qr0 + 8, cc = 2 * (lane & 3);
   const bf16* q0 = qr0 < nr ? q + ((long long)(r0 + qr0) * D.qh + head) * HD : nullptr;
   const bf16* q1 = qr1 < nr ? q + ((long long)(r0 + qr1) * D.qh + head) * HD : nullptr;
   uint32_t qa[HD / 16][4];
@@ -491,10 +496,10 @@ __global__ void __launch_bounds__(128) k_attn_prefill_tc(const bf16* __restrict_
     mb_wait(&full[st], (kb >> 1) & 1);
     const uint32_t kbase = s_u32(ks[st]), vbase = s_u32(vs[st]);
     const int t0 = kb * KT;
-    if (t0 <= p0 + warp * 16 + 15) {                       // some key of this block is visible to the warp
+    if (t0 <= p0 + qt * 16 + 15) {                         // some key of this block is visible to the warp
 #pragma unroll 1
       for (int sub = 0; sub < KT; sub += 16) {
-        if (t0 + sub > p0 + warp * 16 + 15) break;
+        if (t0 + sub > p0 + qt * 16 + 15) break;
         float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
@@ -717,6 +722,19 @@ __global__ void __launch_bounds__(1024) k_attn_account(Dims D, Rows rows, Reqs r
 void launch_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat, cudaStream_t s) {
   k_attn_plan<<<1, 1024, 0, s>>>(D, rows, reqs, pl, n, flat);
 }
+// GQA grouping of the prefill / PRM-pass attention: HG q heads (a divisor of g, <= 8) per
+// CTA, QT 16-row query tiles per head, QT * HG <= 8 warps.
+void pf_shape(const Dims& D, int& QT, int& HG) {
+  HG = 1;
+  for (int d = 1; d <= 8 && d <= D.g; ++d)
+    if (D.g % d == 0) HG = d;
+  QT = std::max(1, std::min(4, 8 / HG));
+}
+int prefill_query_block(const Dims& D) {
+  int QT, HG;
+  pf_shape(D, QT, HG);
+  return 16 * QT;
+}
 template <int HD, bool SUF>
 static void launch_pf(dim3 grid, const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Reqs reqs,
                       const int4* blocks, Rows rows, SufChunk c, cudaStream_t s) {
@@ -726,7 +744,10 @@ static void launch_pf(dim3 grid, const bf16* q, const bf16* pool, bf16* out, Dim
     cudaFuncSetAttribute(k_attn_prefill_tc<HD, SUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
-  k_attn_prefill_tc<HD, SUF><<<grid, 128, sm, s>>>(q, pool, out, D, layer, reqs, blocks, rows, c);
+  int QT, HG;
+  pf_shape(D, QT, HG);
+  grid.y = D.qh / HG;
+  k_attn_prefill_tc<HD, SUF><<<grid, 32 * QT * HG, sm, s>>>(q, pool, out, D, layer, reqs, blocks, rows, c, QT, HG);
 }
 void launch_attn_prefill_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Reqs reqs,
                             const int4* blocks, int nblocks, cudaStream_t s) {
@@ -738,7 +759,8 @@ void launch_attn_prefill_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, 
 void launch_attn_suffix_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
                            SufChunk c, cudaStream_t s) {
   if (c.nrow <= 0 || c.jn <= 0) return;
-  dim3 grid(c.nrow * ((c.jn + 63) / 64), D.qh);
+  const int QP = prefill_query_block(D);
+  dim3 grid(c.nrow * ((c.jn + QP - 1) / QP), D.qh);
   if (D.hd == 128) launch_pf<128, true>(grid, q, pool, out, D, layer, reqs, nullptr, rows, c, s);
   else launch_pf<64, true>(grid, q, pool, out, D, layer, reqs, nullptr, rows, c, s);
 }

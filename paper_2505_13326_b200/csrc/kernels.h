@@ -106,9 +106,11 @@ struct AttnPlan {
 };
 void launch_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat, cudaStream_t s);
 void launch_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s);
-// tensor-core causal prefill: blocks[i] = {first batch row, rows (<= 64), slot, first position}
+// tensor-core causal prefill: blocks[i] = {first batch row, rows (<= prefill_query_block(D)),
+// slot, first position}
 void launch_attn_prefill_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Reqs reqs,
                             const int4* blocks, int nblocks, cudaStream_t s);
+int prefill_query_block(const Dims& D);   // query positions per prefill CTA (16, 32 or 64)
 // tensor-core variant for one f2 PRM chunk: 64-entry query blocks of each row's new suffix
 // entries over [prefix ; suffix entries 0..entry] (causal)
 void launch_attn_suffix_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,

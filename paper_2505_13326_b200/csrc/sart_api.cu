@@ -400,10 +400,11 @@ void prefill_batch(sart_ctx* ctx, sart_ctx* src, int ntok) {
     int nqb = 0;
     if constexpr (std::is_same<T, bf16>::value) {
       std::vector<int4> qb;
+      const int QP = prefill_query_block(D);
       for (int i = 0; i < c;) {
         const int slot = src->pf_slot_h[t0 + i];
         int j = i;
-        while (j < c && src->pf_slot_h[t0 + j] == slot && j - i < 64) ++j;
+        while (j < c && src->pf_slot_h[t0 + j] == slot && j - i < QP) ++j;
         qb.push_back(make_int4(i, j - i, slot, src->pf_pos_h[t0 + i]));
         i = j;
       }
@@ -1102,7 +1103,7 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   IC(dalloc(ctx, &ctx->d_prompt, (size_t)ctx->pf_cap * 4));
   IC(dalloc(ctx, &ctx->d_pf_slot, (size_t)ctx->pf_cap * 4));
   IC(dalloc(ctx, &ctx->d_pf_pos, (size_t)ctx->pf_cap * 4));
-  IC(dalloc(ctx, &ctx->d_pf_blocks, sizeof(int4) * (size_t)(ctx->PC / 64 + D.S + 8)));
+  IC(dalloc(ctx, &ctx->d_pf_blocks, sizeof(int4) * (size_t)(ctx->PC / 16 + D.S + 8)));   // >= 16-position blocks
   IC(cudaEventCreate(&ctx->pf_ev[0]));
   IC(cudaEventCreate(&ctx->pf_ev[1]));
   ctx->ev_cap = D.R + D.S + 64;
