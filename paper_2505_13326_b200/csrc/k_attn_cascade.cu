@@ -406,16 +406,19 @@ __global__ void __launch_bounds__(256) k_attn_merge(const float* __restrict__ pa
 // entries; keys live in a virtual index space [prefix blocks (pbase = ceil((P-1)/bs) * bs
 // slots, slots >= P-1 masked) ; suffix entries], so every 64-key stage is whole pages of one
 // table and the causal test stays "key index <= query index".
-template <int HD, bool SUF>
-__global__ void __launch_bounds__(256) k_attn_prefill_tc(const bf16* __restrict__ q, const bf16* __restrict__ pool,
+#ifndef SART_PF_MINB
+#define SART_PF_MINB 1   // min CTAs per SM for the prefill kernel (2: <= 128 registers)
+#endif
+template <int HD, bool SUF, int NST>
+__global__ void __launch_bounds__(256, SART_PF_MINB) k_attn_prefill_tc(const bf16* __restrict__ q, const bf16* __restrict__ pool,
                                                          bf16* __restrict__ out, Dims D, int layer, Reqs reqs,
                                                          const int4* __restrict__ blocks, Rows rows, SufChunk sc,
                                                          int QT, int HG) {
   constexpr int KT = 64;                                   // key tokens per stage
   extern __shared__ __align__(128) uint8_t praw[];
   bf16 (*ks)[KT * HD] = reinterpret_cast<bf16 (*)[KT * HD]>(praw);
-  bf16 (*vs)[KT * HD] = reinterpret_cast<bf16 (*)[KT * HD]>(praw + 2 * KT * HD * sizeof(bf16));
-  uint64_t* full = reinterpret_cast<uint64_t*>(praw + 4 * KT * HD * sizeof(bf16));
+  bf16 (*vs)[KT * HD] = reinterpret_cast<bf16 (*)[KT * HD]>(praw + NST * KT * HD * sizeof(bf16));
+  uint64_t* full = reinterpret_cast<uint64_t*>(praw + 2 * NST * KT * HD * sizeof(bf16));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = warp % QT;                                // this warp's 16-row query tile
   const int head = blockIdx.y * HG + warp / QT, h = head / D.g;
@@ -445,13 +448,12 @@ __global__ void __launch_bounds__(256) k_attn_prefill_tc(const bf16* __restrict_
   const int* ptab = reqs.prefix + (long long)slot * D.MPB;
   const float sl2 = 1.4426950408889634f * rsqrtf((float)HD);
   if (threadIdx.x == 0) {
-    mb_init(&full[0], 1);
-    mb_init(&full[1], 1);
+    for (int i = 0; i < NST; ++i) mb_init(&full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   auto issue = [&](int kb) {
-    const int st = kb & 1;
+    const int st = kb % NST;
     const int t0 = kb * KT, ntok = min(KT, nkey - t0);
     const int tpb = min(D.bs, KT);
     const int pieces = (ntok + tpb - 1) / tpb;
@@ -468,11 +470,10 @@ __global__ void __launch_bounds__(256) k_attn_prefill_tc(const bf16* __restrict_
     }
   };
   // stale smem of a partial stage is multiplied by P = 0: keep it finite
-  for (int e = threadIdx.x; e < 4 * KT * HD / 8; e += blockDim.x) reinterpret_cast<uint4*>(praw)[e] = make_uint4(0, 0, 0, 0);
+  for (int e = threadIdx.x; e < 2 * NST * KT * HD / 8; e += blockDim.x) reinterpret_cast<uint4*>(praw)[e] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   if (threadIdx.x == 0) {
-    issue(0);
-    if (nkb > 1) issue(1);
+    for (int i = 0; i < NST && i < nkb; ++i) issue(i);
   }
   // Q fragments of this warp's 16 rows (zero beyond nr)
   const int qr0 = qt * 16 + (lane >> 2), qr1 = qr0 + 8, cc = 2 * (lane & 3);
@@ -492,8 +493,8 @@ __global__ void __launch_bounds__(256) k_attn_prefill_tc(const bf16* __restrict_
   for (int nt = 0; nt < HD / 8; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   for (int kb = 0; kb < nkb; ++kb) {
-    const int st = kb & 1;
-    mb_wait(&full[st], (kb >> 1) & 1);
+    const int st = kb % NST;
+    mb_wait(&full[st], (kb / NST) & 1);
     const uint32_t kbase = s_u32(ks[st]), vbase = s_u32(vs[st]);
     const int t0 = kb * KT;
     if (t0 <= p0 + qt * 16 + 15) {                         // some key of this block is visible to the warp
@@ -557,7 +558,7 @@ __global__ void __launch_bounds__(256) k_attn_prefill_tc(const bf16* __restrict_
       }
     }
     __syncthreads();                                       // every warp is done with this stage
-    if (threadIdx.x == 0 && kb + 2 < nkb) issue(kb + 2);
+    if (threadIdx.x == 0 && kb + NST < nkb) issue(kb + NST);
   }
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
@@ -724,10 +725,13 @@ void launch_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat
 }
 // GQA grouping of the prefill / PRM-pass attention: HG q heads (a divisor of g, <= 8) per
 // CTA, QT 16-row query tiles per head, QT * HG <= 8 warps.
+// SART_PF_GROUP=0: one q head per CTA (64 positions, 4 warps) -- the A/B baseline.
 void pf_shape(const Dims& D, int& QT, int& HG) {
+  static const int grp = getenv("SART_PF_GROUP") ? atoi(getenv("SART_PF_GROUP")) : 1;
   HG = 1;
-  for (int d = 1; d <= 8 && d <= D.g; ++d)
-    if (D.g % d == 0) HG = d;
+  if (grp)
+    for (int d = 1; d <= 8 && d <= D.g; ++d)
+      if (D.g % d == 0) HG = d;
   QT = std::max(1, std::min(4, 8 / HG));
 }
 int prefill_query_block(const Dims& D) {
@@ -735,19 +739,30 @@ int prefill_query_block(const Dims& D) {
   pf_shape(D, QT, HG);
   return 16 * QT;
 }
+template <int HD, bool SUF, int NST>
+static void launch_pf_n(dim3 grid, int threads, const bf16* q, const bf16* pool, bf16* out, Dims D, int layer,
+                        Reqs reqs, const int4* blocks, Rows rows, SufChunk c, int QT, int HG, cudaStream_t s) {
+  const size_t sm = 2 * NST * 64 * (size_t)HD * sizeof(bf16) + 8 * NST;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attn_prefill_tc<HD, SUF, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  k_attn_prefill_tc<HD, SUF, NST><<<grid, threads, sm, s>>>(q, pool, out, D, layer, reqs, blocks, rows, c, QT, HG);
+}
+// ring depth: 2 stages while two CTAs share an SM (<= 4 warps); 4 stages for the larger
+// grouped CTAs, which the register file limits to one per SM (SART_PF_NST overrides)
 template <int HD, bool SUF>
 static void launch_pf(dim3 grid, const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Reqs reqs,
                       const int4* blocks, Rows rows, SufChunk c, cudaStream_t s) {
-  const size_t sm = 4 * 64 * (size_t)HD * sizeof(bf16) + 64;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_attn_prefill_tc<HD, SUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
   int QT, HG;
   pf_shape(D, QT, HG);
   grid.y = D.qh / HG;
-  k_attn_prefill_tc<HD, SUF><<<grid, 32 * QT * HG, sm, s>>>(q, pool, out, D, layer, reqs, blocks, rows, c, QT, HG);
+  static const int nst_env = getenv("SART_PF_NST") ? atoi(getenv("SART_PF_NST")) : 0;
+  const int nst = nst_env ? nst_env : (QT * HG > 4 ? 4 : 2);
+  const int th = 32 * QT * HG;
+  if (nst >= 4) launch_pf_n<HD, SUF, 4>(grid, th, q, pool, out, D, layer, reqs, blocks, rows, c, QT, HG, s);
+  else launch_pf_n<HD, SUF, 2>(grid, th, q, pool, out, D, layer, reqs, blocks, rows, c, QT, HG, s);
 }
 void launch_attn_prefill_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Reqs reqs,
                             const int4* blocks, int nblocks, cudaStream_t s) {

@@ -24,13 +24,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def run(warm: int):
+def run(warm: int, num_blocks: int):
     import bench
     from paper_2505_13326_b200 import Engine
     from synth import SHAPES
     cfg = dict(bench.C2)
     shape = SHAPES["1.5B"]
-    eng = Engine(shape, "bf16", weight_seed=1234, block_size=64, num_blocks=0, max_rows=512, max_requests=256,
+    # a pool that holds all 64 resident requests (R34 needs ~33.3K blocks) but leaves ncu room
+    # to back up device memory ON the device between replay passes (a pool sized from all
+    # free HBM forces a host-memory backup, under which the replayed run failed to launch)
+    eng = Engine(shape, "bf16", weight_seed=1234, block_size=64, num_blocks=num_blocks, max_rows=512, max_requests=256,
                  max_prompt=1025, T=cfg["T"], cap=cfg["cap"], eos_id=1, temperature=1.0, sampler_seed=7,
                  profile=True)   # eager launches (ncu replays single kernels, not graph nodes)
     for r in bench.make_requests(0, 1, 0, cfg["concurrent"] + 24 * (warm + 2), shape, cfg):
@@ -74,8 +77,9 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--warm", type=int, default=3)
     ap.add_argument("--summarise", nargs=2)
+    ap.add_argument("--num-blocks", type=int, default=40000)
     a = ap.parse_args()
     if a.summarise:
         summarise(*a.summarise)
     else:
-        run(a.warm)
+        run(a.warm, a.num_blocks)
