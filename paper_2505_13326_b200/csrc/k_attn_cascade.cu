@@ -402,8 +402,8 @@ __global__ void __launch_bounds__(256) k_attn_merge(const float* __restrict__ pa
 // serves every q head of the GQA group (read once per group, not once per q head); the last
 // key block is masked causally.  QT, HG: pf_shape() (<= 8 warps).
 //
-// SUF (row f2, the PRM pass): the CTA is a 64-entry block of one batch row's new suffix
-// entries; keys live in a virtual index space [prefix blocks (pbase = ceil((P-1)/bs) * bs
+// SUF (row f2, the PRM pass): the CTA is a block of <= QP of one batch row's new suffix
+// entries (descriptor {first token, count, row, first entry}); keys live in a virtual index space [prefix blocks (pbase = ceil((P-1)/bs) * bs
 // slots, slots >= P-1 masked) ; suffix entries], so every 64-key stage is whole pages of one
 // table and the causal test stays "key index <= query index".
 #ifndef SART_PF_MINB
@@ -412,8 +412,7 @@ __global__ void __launch_bounds__(256) k_attn_merge(const float* __restrict__ pa
 template <int HD, bool SUF, int NST>
 __global__ void __launch_bounds__(256, SART_PF_MINB) k_attn_prefill_tc(const bf16* __restrict__ q, const bf16* __restrict__ pool,
                                                          bf16* __restrict__ out, Dims D, int layer, Reqs reqs,
-                                                         const int4* __restrict__ blocks, Rows rows, SufChunk sc,
-                                                         int QT, int HG) {
+                                                         const int4* __restrict__ blocks, Rows rows, int QT, int HG) {
   constexpr int KT = 64;                                   // key tokens per stage
   extern __shared__ __align__(128) uint8_t praw[];
   bf16 (*ks)[KT * HD] = reinterpret_cast<bf16 (*)[KT * HD]>(praw);
@@ -422,22 +421,17 @@ __global__ void __launch_bounds__(256, SART_PF_MINB) k_attn_prefill_tc(const bf1
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = warp % QT;                                // this warp's 16-row query tile
   const int head = blockIdx.y * HG + warp / QT, h = head / D.g;
-  const int QP = 16 * QT;                                  // query positions per CTA
   int r0, nr, slot, p0;                                    // first batch token, tokens, slot, first key index
   int npre = 0x7fffffff, pbase = 0x7fffffff;               // masked prefix padding [npre, pbase); suffix base
   const int* rtab = nullptr;
   if constexpr (SUF) {
-    const int nqb = (sc.jn + QP - 1) / QP;
-    const int rl = blockIdx.x / nqb, qb = blockIdx.x % nqb, row = sc.r0 + rl;
-    const int cnt = rows.ell[row] - sc.ell_ws[row];
-    const int ja = sc.j0 + qb * QP;
-    nr = min(QP, min(cnt, sc.j0 + sc.jn) - ja);
-    if (nr <= 0) return;
-    r0 = rl * sc.jn + qb * QP;
+    const int4 blk = blocks[blockIdx.x];                   // {first token, entries, row, first entry}
+    const int row = blk.z;
+    r0 = blk.x; nr = blk.y;
     slot = rows.slot[row];
     npre = reqs.P[slot] - 1;
     pbase = (npre + D.bs - 1) / D.bs * D.bs;
-    p0 = pbase + sc.ell_ws[row] + ja;
+    p0 = pbase + blk.w;
     rtab = rows.table + (long long)row * D.MBR;
   } else {
     const int4 blk = blocks[blockIdx.x];                   // {first batch row, rows, slot, first position}
@@ -741,43 +735,42 @@ int prefill_query_block(const Dims& D) {
 }
 template <int HD, bool SUF, int NST>
 static void launch_pf_n(dim3 grid, int threads, const bf16* q, const bf16* pool, bf16* out, Dims D, int layer,
-                        Reqs reqs, const int4* blocks, Rows rows, SufChunk c, int QT, int HG, cudaStream_t s) {
+                        Reqs reqs, const int4* blocks, Rows rows, int QT, int HG, cudaStream_t s) {
   const size_t sm = 2 * NST * 64 * (size_t)HD * sizeof(bf16) + 8 * NST;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_attn_prefill_tc<HD, SUF, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
-  k_attn_prefill_tc<HD, SUF, NST><<<grid, threads, sm, s>>>(q, pool, out, D, layer, reqs, blocks, rows, c, QT, HG);
+  k_attn_prefill_tc<HD, SUF, NST><<<grid, threads, sm, s>>>(q, pool, out, D, layer, reqs, blocks, rows, QT, HG);
 }
 // ring depth: 2 stages while two CTAs share an SM (<= 4 warps); 4 stages for the larger
 // grouped CTAs, which the register file limits to one per SM (SART_PF_NST overrides)
 template <int HD, bool SUF>
 static void launch_pf(dim3 grid, const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Reqs reqs,
-                      const int4* blocks, Rows rows, SufChunk c, cudaStream_t s) {
+                      const int4* blocks, Rows rows, cudaStream_t s) {
   int QT, HG;
   pf_shape(D, QT, HG);
   grid.y = D.qh / HG;
   static const int nst_env = getenv("SART_PF_NST") ? atoi(getenv("SART_PF_NST")) : 0;
   const int nst = nst_env ? nst_env : (QT * HG > 4 ? 4 : 2);
   const int th = 32 * QT * HG;
-  if (nst >= 4) launch_pf_n<HD, SUF, 4>(grid, th, q, pool, out, D, layer, reqs, blocks, rows, c, QT, HG, s);
-  else launch_pf_n<HD, SUF, 2>(grid, th, q, pool, out, D, layer, reqs, blocks, rows, c, QT, HG, s);
+  if (nst >= 4) launch_pf_n<HD, SUF, 4>(grid, th, q, pool, out, D, layer, reqs, blocks, rows, QT, HG, s);
+  else launch_pf_n<HD, SUF, 2>(grid, th, q, pool, out, D, layer, reqs, blocks, rows, QT, HG, s);
 }
 void launch_attn_prefill_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Reqs reqs,
                             const int4* blocks, int nblocks, cudaStream_t s) {
   if (nblocks <= 0) return;
   dim3 grid(nblocks, D.qh);
-  if (D.hd == 128) launch_pf<128, false>(grid, q, pool, out, D, layer, reqs, blocks, Rows{}, SufChunk{}, s);
-  else launch_pf<64, false>(grid, q, pool, out, D, layer, reqs, blocks, Rows{}, SufChunk{}, s);
+  if (D.hd == 128) launch_pf<128, false>(grid, q, pool, out, D, layer, reqs, blocks, Rows{}, s);
+  else launch_pf<64, false>(grid, q, pool, out, D, layer, reqs, blocks, Rows{}, s);
 }
 void launch_attn_suffix_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
-                           SufChunk c, cudaStream_t s) {
-  if (c.nrow <= 0 || c.jn <= 0) return;
-  const int QP = prefill_query_block(D);
-  dim3 grid(c.nrow * ((c.jn + QP - 1) / QP), D.qh);
-  if (D.hd == 128) launch_pf<128, true>(grid, q, pool, out, D, layer, reqs, nullptr, rows, c, s);
-  else launch_pf<64, true>(grid, q, pool, out, D, layer, reqs, nullptr, rows, c, s);
+                           const int4* qblocks, int nqb, cudaStream_t s) {
+  if (nqb <= 0) return;
+  dim3 grid(nqb, D.qh);
+  if (D.hd == 128) launch_pf<128, true>(grid, q, pool, out, D, layer, reqs, qblocks, rows, s);
+  else launch_pf<64, true>(grid, q, pool, out, D, layer, reqs, qblocks, rows, s);
 }
 void launch_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s) {
   launch_pdl(k_attn_items, dim3(1), dim3(1024), 0, s, D, rows, reqs, pl);

@@ -239,45 +239,34 @@ void launch_to_f32(const T* in, float* out, long long n, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------ f2 PRM pass
-// Token list of one chunk: token t is per-row index j of row r; its input is the token that
-// produced suffix entry e = ell_ws[r] + j (entry 0: the last prompt token, R22; entry e > 0:
-// the generated token y_e = hist[e-1]).
-__global__ void k_prm_tokens(Dims D, Rows rows, Reqs reqs, SufChunk c, int* __restrict__ tok, int* __restrict__ row,
-                             int* __restrict__ ent) {
-  const int n = c.nrow * c.jn;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-    const int r = c.r0 + t / c.jn, j = c.j0 + t % c.jn;
-    const int ws = c.ell_ws[r];
-    if (j < rows.ell[r] - ws) {
-      const int e = ws + j, slot = rows.slot[r];
-      const long long sb = (long long)slot * SART_MAXN + rows.b[r];
-      tok[t] = e == 0 ? reqs.first_tok[slot] : reqs.hist[sb * D.cap + (e - 1)];
-      row[t] = r;
-      ent[t] = e;
-    } else {
-      tok[t] = 0;
-      row[t] = -1;
-      ent[t] = 0;
-    }
+// Token list of one packed chunk: segment {first token, count, row, first entry}; token
+// t0 + j is suffix entry e = e0 + j of that row, whose input is the last prompt token for
+// e = 0 (R22) and the generated token y_e = hist[e-1] otherwise.
+__global__ void k_prm_tokens(Dims D, Rows rows, Reqs reqs, const int4* __restrict__ seg, int* __restrict__ tok,
+                             int* __restrict__ row, int* __restrict__ ent) {
+  const int4 sg = seg[blockIdx.x];
+  const int r = sg.z, slot = rows.slot[r];
+  const long long sb = (long long)slot * SART_MAXN + rows.b[r];
+  for (int j = threadIdx.x; j < sg.y; j += blockDim.x) {
+    const int e = sg.w + j, t = sg.x + j;
+    tok[t] = e == 0 ? reqs.first_tok[slot] : reqs.hist[sb * D.cap + (e - 1)];
+    row[t] = r;
+    ent[t] = e;
   }
 }
-void launch_prm_tokens(Dims D, Rows rows, Reqs reqs, SufChunk c, int* tok, int* row, int* ent, cudaStream_t s) {
-  const int n = c.nrow * c.jn;
-  if (n > 0) k_prm_tokens<<<(n + 255) / 256, 256, 0, s>>>(D, rows, reqs, c, tok, row, ent);
+void launch_prm_tokens(Dims D, Rows rows, Reqs reqs, const int4* seg, int nseg, int* tok, int* row, int* ent,
+                       cudaStream_t s) {
+  if (nseg > 0) k_prm_tokens<<<nseg, 256, 0, s>>>(D, rows, reqs, seg, tok, row, ent);
 }
-// zrow[r] = z of row r's last entry (the PRM's score position), when it lies in this chunk
+// zrow[row] = z[token of the row's last entry] (the PRM's score position)
 template <typename T>
-__global__ void k_prm_gather(const T* __restrict__ z, T* __restrict__ zrow, Rows rows, SufChunk c, int d) {
-  const int r = c.r0 + blockIdx.x;
-  const int jl = rows.ell[r] - c.ell_ws[r] - 1;
-  if (jl < c.j0 || jl >= c.j0 + c.jn) return;
-  const T* src = z + ((long long)blockIdx.x * c.jn + (jl - c.j0)) * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) zrow[(long long)r * d + i] = src[i];
+__global__ void k_prm_gather(const T* __restrict__ z, T* __restrict__ zrow, const int4* __restrict__ gat, int d) {
+  const int4 g = gat[blockIdx.x];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) zrow[(long long)g.x * d + i] = z[(long long)g.y * d + i];
 }
 template <typename T>
-void launch_prm_gather(const T* z, T* zrow, Dims D, Rows rows, SufChunk c, int d, cudaStream_t s) {
-  (void)D;
-  if (c.nrow > 0) k_prm_gather<T><<<c.nrow, 256, 0, s>>>(z, zrow, rows, c, d);
+void launch_prm_gather(const T* z, T* zrow, const int4* gat, int ng, int d, cudaStream_t s) {
+  if (ng > 0) k_prm_gather<T><<<ng, 256, 0, s>>>(z, zrow, gat, d);
 }
 
 #define INST(T)                                                                                        \
@@ -290,7 +279,7 @@ void launch_prm_gather(const T* z, T* zrow, Dims D, Rows rows, SufChunk c, int d
   template void launch_swiglu<T>(const float*, T*, int, int, cudaStream_t);                             \
   template void launch_convert<T>(const float*, T*, long long, cudaStream_t);                           \
   template void launch_to_f32<T>(const T*, float*, long long, cudaStream_t);                           \
-  template void launch_prm_gather<T>(const T*, T*, Dims, Rows, SufChunk, int, cudaStream_t);
+  template void launch_prm_gather<T>(const T*, T*, const int4*, int, int, cudaStream_t);
 INST(float)
 INST(bf16)
 

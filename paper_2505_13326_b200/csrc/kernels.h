@@ -13,13 +13,11 @@ struct RopeArgs {
   const int* sf_row = nullptr;
 };
 
-// One chunk of the f2 PRM pass: tokens t = (row - r0) * jn + (j - j0) for rows [r0, r0+nrow)
-// and per-row token index j in [j0, j0+jn); token j of a row is its suffix entry
-// ell_ws[row] + j, valid while j < ell[row] - ell_ws[row] (the entries decoded this window).
-struct SufChunk {
-  const int* ell_ws;
-  int r0, nrow, j0, jn;
-};
+// Packed f2 PRM pass: a chunk's tokens are the new suffix entries of its rows back to back.
+// Descriptors (int4) built on the host from the rows' entry counts:
+//   segment  {first token, count, batch row, first entry}   (k_prm_tokens, one CTA each)
+//   qblock   {first token, count <= QP, batch row, first entry}   (suffix attention CTAs)
+//   gather   {batch row, token of its last entry, 0, 0}      (k_prm_gather)
 
 // ---- model (k_model.cu)
 template <typename T> void launch_init_tensor(T* p, long long n, int tensor_id, int is_norm, float std,
@@ -114,7 +112,7 @@ int prefill_query_block(const Dims& D);   // query positions per prefill CTA (16
 // tensor-core variant for one f2 PRM chunk: 64-entry query blocks of each row's new suffix
 // entries over [prefix ; suffix entries 0..entry] (causal)
 void launch_attn_suffix_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
-                           SufChunk c, cudaStream_t s);
+                           const int4* qblocks, int nqb, cudaStream_t s);
 void launch_attn_account(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, double* acc, cudaStream_t s);
 void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse,
                          Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s);
@@ -138,8 +136,8 @@ void launch_admit(const AdmitEvent* ev, int n_ev, int total_pop, int new_rows, i
 void launch_boundary(Dims D, Rows rows, Rows tmp, Reqs reqs, const float* prm_score, int* free_stack,
                      Ctr* ctr, DevResult* res, int* slot_row, int n, cudaStream_t s);
 void launch_window_begin(Ctr* ctr, int n, cudaStream_t s);
-// f2 PRM pass: token list of one chunk (tok: input token of the entry, row: batch row or -1,
-// ent: suffix entry), and the gather of each row's last-entry hidden state
-void launch_prm_tokens(Dims D, Rows rows, Reqs reqs, SufChunk c, int* tok, int* row, int* ent, cudaStream_t s);
-template <typename T> void launch_prm_gather(const T* z, T* zrow, Dims D, Rows rows, SufChunk c, int d,
-                                             cudaStream_t s);
+// f2 PRM pass: token list of one chunk from its segments (tok: input token of the entry,
+// row: batch row, ent: suffix entry), and the gather of each row's last-entry state
+void launch_prm_tokens(Dims D, Rows rows, Reqs reqs, const int4* seg, int nseg, int* tok, int* row, int* ent,
+                       cudaStream_t s);
+template <typename T> void launch_prm_gather(const T* z, T* zrow, const int4* gat, int ng, int d, cudaStream_t s);

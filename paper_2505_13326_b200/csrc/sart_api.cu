@@ -141,13 +141,15 @@ struct sart_ctx {
   // and workspaces; it shares rows / reqs / stream with the policy ctx.
   sart_ctx* prm = nullptr;
   bool is_prm = false;
-  int* ell_ws = nullptr;                  // [R] rows.ell at the start of the window
+  int *h_ell_ws = nullptr, *h_ell = nullptr;   // pinned [R]: rows.ell at window start / at the boundary
   int *prm_tok = nullptr, *prm_row = nullptr, *prm_ent = nullptr;   // one PRM chunk's tokens
+  int4 *prm_desc = nullptr, *h_prm_desc = nullptr;   // packed-pass descriptors (device / pinned host)
+  size_t prm_desc_cap = 0;
   int prm_chunk = 0;                      // tokens per PRM-pass chunk (<= W)
   void* zrow = nullptr;                   // [R][d] final-norm state of each row's last entry
   cudaEvent_t prm_ev[2] = {nullptr, nullptr};
   double prm_ms = 0;
-  long long prm_tokens = 0, prm_passes = 0, prm_bt0 = 0;
+  long long prm_tokens = 0, prm_passes = 0;
 
   template <typename T> T* W_(int idx) const { return (T*)wblob + woff[idx]; }
 };
@@ -436,12 +438,13 @@ void prefill_batch(sart_ctx* ctx, sart_ctx* src, int ntok) {
 
 // Row f2: the separate PRM decoder reads every row's suffix entries decoded in this window
 // (entries ell_ws .. ell-1, reading R42) through its own paged KV -- the prefix was
-// prefilled at admission -- and its head scores the last entry's final-norm state.  Rows
-// are processed in chunks of at most m->W tokens (token j of a row at chunk offset
-// (row - r0) * jn + j - j0; entries past a row's count are padding: no KV write, no
-// attention, never gathered).  jmax bounds the entries per row (the window's steps).
+// prefilled at admission -- and its head scores the last entry's final-norm state.  The
+// host reads the rows' entry counts and packs the entries back to back into chunks of at
+// most prm_chunk tokens (a row longer than the room left continues in the next chunk,
+// processed in order, so its later entries attend to the KV its earlier ones appended):
+// no padding, exact GEMM sizes.  Descriptors for every chunk go up in one copy.
 template <typename T>
-void prm_model_scores(sart_ctx* ctx, int n, int jmax) {
+void prm_model_scores(sart_ctx* ctx, int n) {
   sart_ctx* m = ctx->prm;
   const Dims& D = m->D;
   cudaStream_t s = ctx->st;
@@ -449,21 +452,65 @@ void prm_model_scores(sart_ctx* ctx, int n, int jmax) {
   // that `ncu --profile-from-start off` captures exactly one PRM pass
   static const int ncu_pass = getenv("SART_NCU_PRM_PASS") ? atoi(getenv("SART_NCU_PRM_PASS")) : 0;
   const bool ncu_range = ncu_pass > 0 && ctx->prm_passes + 1 == ncu_pass;
+  CK_VOID(cudaMemcpyAsync(m->h_ell, ctx->rows.ell, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+  CK_VOID(cudaStreamSynchronize(s));
   if (ncu_range) cudaProfilerStart();
   CK_VOID(cudaEventRecord(m->prm_ev[0], s));
-  std::vector<SufChunk> chunks;
-  if (jmax <= m->prm_chunk) {
-    const int G = std::max(1, m->prm_chunk / jmax);
-    for (int r0 = 0; r0 < n; r0 += G) chunks.push_back(SufChunk{ctx->ell_ws, r0, std::min(G, n - r0), 0, jmax});
-  } else {
-    const int J = std::max(64, m->prm_chunk / 64 * 64);
-    for (int r = 0; r < n; ++r)
-      for (int j0 = 0; j0 < jmax; j0 += J) chunks.push_back(SufChunk{ctx->ell_ws, r, 1, j0, std::min(J, jmax - j0)});
+  const int QP = prefill_query_block(D), Wc = m->prm_chunk;
+  struct Chunk { int ntok, seg, nseg, qb, nqb, gat, ngat; };
+  std::vector<Chunk> chunks;
+  std::vector<int4> seg, qb, gat;
+  std::vector<std::pair<size_t, size_t>> spans;   // per chunk: [seg begin, qb begin, gat begin) offsets
+  int fill = 0;
+  Chunk cur{0, 0, 0, 0, 0, 0, 0};
+  auto close_chunk = [&]() {
+    if (cur.ntok == 0) return;
+    chunks.push_back(cur);
+    cur = Chunk{0, (int)seg.size(), 0, (int)qb.size(), 0, (int)gat.size(), 0};
+    fill = 0;
+  };
+  long long entries = 0;
+  for (int r = 0; r < n; ++r) {
+    const int cnt = m->h_ell[r] - m->h_ell_ws[r];
+    entries += std::max(0, cnt);
+    for (int j = 0; j < cnt;) {
+      const int take = std::min(cnt - j, Wc - fill);
+      const int e0 = m->h_ell_ws[r] + j;
+      seg.push_back(make_int4(fill, take, r, e0));
+      cur.nseg++;
+      for (int k = 0; k < take; k += QP) {
+        qb.push_back(make_int4(fill + k, std::min(QP, take - k), r, e0 + k));
+        cur.nqb++;
+      }
+      if (j + take == cnt) {
+        gat.push_back(make_int4(r, fill + take - 1, 0, 0));
+        cur.ngat++;
+      }
+      fill += take;
+      cur.ntok = fill;
+      j += take;
+      if (fill == Wc) close_chunk();
+    }
   }
-  for (const SufChunk& c : chunks) {
-    const int nt = c.nrow * c.jn;
+  close_chunk();
+  // one upload: [all segments | all q-blocks | all gathers]
+  const size_t nd = seg.size() + qb.size() + gat.size();
+  if (nd > m->prm_desc_cap) {
+    ctx->poisoned = true;
+    set_err(SART_ECUDA, "PRM-pass descriptor buffer too small");
+    return;
+  }
+  std::copy(seg.begin(), seg.end(), m->h_prm_desc);
+  std::copy(qb.begin(), qb.end(), m->h_prm_desc + seg.size());
+  std::copy(gat.begin(), gat.end(), m->h_prm_desc + seg.size() + qb.size());
+  if (nd) CK_VOID(cudaMemcpyAsync(m->prm_desc, m->h_prm_desc, sizeof(int4) * nd, cudaMemcpyHostToDevice, s));
+  const int4* dseg = m->prm_desc;
+  const int4* dqb = m->prm_desc + seg.size();
+  const int4* dgat = m->prm_desc + seg.size() + qb.size();
+  for (const Chunk& c : chunks) {
+    const int nt = c.ntok;
     const RopeArgs ra{nullptr, m->prm_ent, m->prm_row};
-    launch_prm_tokens(D, m->rows, m->reqs, c, m->prm_tok, m->prm_row, m->prm_ent, s);
+    launch_prm_tokens(D, m->rows, m->reqs, dseg + c.seg, c.nseg, m->prm_tok, m->prm_row, m->prm_ent, s);
     launch_embed<T>(m->prm_tok, m->W_<T>(t_embed()), m->h, nt, D.d, s);
     m->launches += 2;
     int np_res = 0;
@@ -472,7 +519,7 @@ void prm_model_scores(sart_ctx* ctx, int n, int jmax) {
                         s);
       qkv_rope<T>(m, l, nt, ra);
       if constexpr (std::is_same<T, bf16>::value)
-        launch_attn_suffix_tc((bf16*)m->q, (bf16*)m->pool, (bf16*)m->o, D, l, m->rows, m->reqs, c, s);
+        launch_attn_suffix_tc((bf16*)m->q, (bf16*)m->pool, (bf16*)m->o, D, l, m->rows, m->reqs, dqb + c.qb, c.nqb, s);
       else
         launch_attn_suffix<T>((T*)m->q, (T*)m->pool, (T*)m->o, D, l, m->rows, m->reqs, m->prm_row, m->prm_ent, nt, s);
       int np = proj<T>(m, (T*)m->o, m->W_<T>(t_layer(l, 3)), nt, D.d, D.qh * D.hd);
@@ -482,7 +529,7 @@ void prm_model_scores(sart_ctx* ctx, int n, int jmax) {
       m->launches += 3;
     }
     launch_rmsnorm<T>(m->h, m->parts, np_res, m->W_<T>(t_final(D)), (T*)m->a, nullptr, nullptr, nt, D.d, D.eps, s);
-    launch_prm_gather<T>((T*)m->a, (T*)m->zrow, D, m->rows, c, D.d, s);
+    launch_prm_gather<T>((T*)m->a, (T*)m->zrow, dgat + c.gat, c.ngat, D.d, s);
     m->launches += 2;
   }
   gemm<T>(m, (T*)m->zrow, m->W_<T>(t_prm_w1(D)), m->fparams + m->f_prm_b1, m->prm_hid, n, D.d, D.d, GEMM_STORE);
@@ -492,6 +539,7 @@ void prm_model_scores(sart_ctx* ctx, int n, int jmax) {
   if (ncu_range) cudaProfilerStop();
   ctx->launches += m->launches;
   m->launches = 0;
+  ctx->prm_tokens += entries;
   if (m->gemm_failed) ctx->gemm_failed = true;
 }
 
@@ -743,10 +791,8 @@ int run_window(sart_ctx* ctx) {
   ctx->ev_used = 0;
   launch_window_begin(ctx->ctr, n, ctx->st);
   ctx->launches++;
-  if (ctx->prm) {
-    CK(cudaMemcpyAsync(ctx->ell_ws, ctx->rows.ell, sizeof(int) * n, cudaMemcpyDeviceToDevice, ctx->st));
-    ctx->prm_bt0 = ctx->branch_tokens;
-  }
+  if (ctx->prm)   // entries decoded this window = ell(boundary) - ell(now), per row (f2 pass)
+    CK(cudaMemcpyAsync(ctx->prm->h_ell_ws, ctx->rows.ell, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->st));
   if (ctx->bf16) {   // work units of the cascade attention for this window's batch
     launch_attn_plan(D, ctx->rows, ctx->reqs, ctx->plan, n, ctx->cfg.attn_mode == SART_ATTN_FLAT, ctx->st);
     ctx->launches++;
@@ -781,9 +827,7 @@ int run_window(sart_ctx* ctx) {
   }
   constexpr int POLL = 16;
   int polls = 0;
-  int enq = 0;   // decode steps enqueued this window (bounds the entries a row decoded)
   for (int k = 1; k <= D.T; ++k) {
-    enq = k;
     if (k > 1 && (k % POLL) == 1) {
       if (polls >= 2) {   // bound the run-ahead: wait for the poll two periods back
         CK(cudaEventSynchronize(ctx->poll_ev[polls & 1]));
@@ -809,7 +853,7 @@ int run_window(sart_ctx* ctx) {
   CK(cudaMemcpyAsync(ctx->dbg_slot, ctx->rows.slot, sizeof(int) * n, cudaMemcpyDeviceToDevice, ctx->st));
   CK(cudaMemcpyAsync(ctx->dbg_b, ctx->rows.b, sizeof(int) * n, cudaMemcpyDeviceToDevice, ctx->st));
   if (ctx->prm) {
-    prm_model_scores<T>(ctx, n, enq);
+    prm_model_scores<T>(ctx, n);
     if (ctx->poisoned) return SART_ECUDA;
     if (ctx->gemm_failed) return set_err(SART_EINVAL, "GEMM shape unsupported by the tcgen05 kernel (PRM model)");
   } else {
@@ -825,7 +869,6 @@ int run_window(sart_ctx* ctx) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ctx->prm->prm_ev[0], ctx->prm->prm_ev[1]) == cudaSuccess) ctx->prm_ms += ms;
     ctx->prm_passes++;
-    ctx->prm_tokens += ctx->h_ctr->branch_tokens - ctx->prm_bt0;
   }
   if (ctx->cfg.profile) {
     for (int i = 0; i + 1 < ctx->ev_used; i += 2) {
@@ -964,6 +1007,9 @@ int sart_destroy(sart_ctx* ctx) {
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->wblob) cudaFree(ctx->wblob);
   if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
+  if (ctx->h_ell_ws) cudaFreeHost(ctx->h_ell_ws);
+  if (ctx->h_ell) cudaFreeHost(ctx->h_ell);
+  if (ctx->h_prm_desc) cudaFreeHost(ctx->h_prm_desc);
   if (ctx->h_live) cudaFreeHost(ctx->h_live);
   if (ctx->own_stream && ctx->st) cudaStreamDestroy(ctx->st);
   delete ctx;
@@ -1086,7 +1132,13 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     IC(dalloc(m, &m->zrow, (size_t)D.R * P.d * es));
     IC(cudaEventCreate(&m->prm_ev[0]));
     IC(cudaEventCreate(&m->prm_ev[1]));
-    IC(dalloc(ctx, &ctx->ell_ws, sizeof(int) * (size_t)D.R));
+    IC(cudaMallocHost(&m->h_ell_ws, sizeof(int) * (size_t)D.R));
+    IC(cudaMallocHost(&m->h_ell, sizeof(int) * (size_t)D.R));
+    // descriptors: segments <= rows + chunks, q-blocks <= rows + tokens / 16, gathers <= rows
+    const size_t max_tok = (size_t)D.R * D.T;
+    m->prm_desc_cap = 3 * (size_t)D.R + 2 * (max_tok / m->prm_chunk + 1) + max_tok / 16 + 16;
+    IC(dalloc(m, &m->prm_desc, sizeof(int4) * m->prm_desc_cap, false));
+    IC(cudaMallocHost(&m->h_prm_desc, sizeof(int4) * m->prm_desc_cap));
   }
   IC(dalloc(ctx, &ctx->ctr, sizeof(Ctr) + sizeof(int) * D.S));
   IC(dalloc(ctx, &ctx->res, sizeof(DevResult) * D.S));

@@ -9,8 +9,8 @@ tensor-core kernel, the chunking of the pass and the last-entry gather all at on
 
 Inputs: teacher-forced token streams (PP1) with EOS planted mid-window for some branches;
 prompt lengths cover an empty prefix (P = 1), P-1 a multiple of the block size and ragged
-prefixes; SART_PRM_CHUNK forces the multi-chunk paths (several rows per chunk, one row split
-over several chunks).  Tolerance: abs 2e-2 on the score for bf16, 1e-5 for fp32 (north_star).
+prefixes; SART_PRM_CHUNK forces the multi-chunk paths (the pass packs every row's new
+entries back to back, so rows straddle chunk boundaries and long rows span several chunks).  Tolerance: abs 2e-2 on the score for bf16, 1e-5 for fp32 (north_star).
 """
 import os
 
@@ -61,8 +61,9 @@ CASES = [
     ("tiny", "prm-tiny", "fp32", 16, 40, None),
     ("small", "prm-small", "bf16", 16, 40, None),
     ("small", "prm-small", "fp32", 16, 40, None),
-    ("tiny", "prm-tiny", "bf16", 16, 40, 128),     # 8 rows per chunk, 2 chunks
-    ("small", "prm-small", "bf16", 80, 200, 64),   # one row over two chunks (j-split)
+    ("tiny", "prm-tiny", "bf16", 16, 40, 100),     # packed chunks of 100 entries: rows straddle chunks
+    ("tiny", "prm-tiny", "fp32", 16, 40, 100),
+    ("small", "prm-small", "bf16", 80, 200, 64),   # a row's window entries over two chunks
 ]
 
 

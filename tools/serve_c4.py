@@ -7,6 +7,12 @@ records: E2E = final - arrival, queuing = prefill start - arrival (R27), inferen
 queuing.  Percentiles are nearest-rank.
 
     python tools/serve_c4.py --requests 120 --rate 1.0
+    python tools/serve_c4.py --prm PRM-7B     # scores from a separate PRM-7B decoder (row f2)
+
+Without --prm the pruning scores are the synthetic script's (DESIGN.md input recipe); with
+--prm they come from the separate PRM model (random-init weights: the pruning decisions are
+then arbitrary, but the serving cost -- a 7B forward over every branch's new tokens at each
+boundary -- is the paper's).
 """
 import argparse
 import json
@@ -33,15 +39,20 @@ def main():
     ap.add_argument("--shape", default="7B")
     ap.add_argument("--cap", type=int, default=8192)
     ap.add_argument("--T", type=int, default=400)
+    ap.add_argument("--prm", default=None, help="separate PRM decoder shape (row f2), e.g. PRM-7B")
     a = ap.parse_args()
     import torch
     from paper_2505_13326_b200 import Engine
     from synth import SHAPES, gen_arrivals, gen_requests
     shape = SHAPES[a.shape]
+    prm = None
+    if a.prm:   # the PRM reads the policy's tokens: give it the policy's vocab
+        import dataclasses
+        prm = dataclasses.replace(SHAPES[a.prm], vocab=shape.vocab)
     stream = torch.cuda.current_stream()
     eng = Engine(shape, "bf16", weight_seed=4, block_size=64, num_blocks=0, max_rows=1024, max_requests=512,
                  max_prompt=1025, T=a.T, cap=a.cap, eos_id=1, temperature=1.0, sampler_seed=9,
-                 stream=stream.cuda_stream)
+                 stream=stream.cuda_stream, prm_shape=prm, prm_weight_seed=12)
     reqs = gen_requests(a.requests, shape, 8, 2, 0.8, 4, a.cap, a.T, eos_id=1, p_range=(64, 1024))
     arr = gen_arrivals(a.requests, a.rate)            # ns offsets of a Poisson process
     t0 = time.monotonic_ns()
@@ -52,7 +63,7 @@ def main():
         now = time.monotonic_ns() - t0
         while nxt < a.requests and arr[nxt] <= now:
             reqs[nxt].arrival_ns = t0 + int(arr[nxt])     # absolute, same clock as the engine
-            eng.admit(reqs[nxt])
+            eng.admit(reqs[nxt], use_script_scores=prm is None)
             nxt += 1
         st = eng.step(1)
         windows += 1
@@ -65,7 +76,10 @@ def main():
     inf = [x - y for x, y in zip(e2e, que)]
     pct = lambda xs: {f"p{p}": nearest_rank(xs, p) for p in (50, 90, 97, 99)}
     st = eng.step(0)
-    out = {"config": "C4 (BJ configs[3]) single GPU", "shape": a.shape, "requests": a.requests,
+    prof = eng.profile()
+    out = {"config": "C4 (BJ configs[3]) single GPU", "shape": a.shape, "prm_model": a.prm,
+           "prm_ms_per_boundary": prof["prm_ms"] / max(1, prof["prm_passes"]) if a.prm else None,
+           "prm_share_of_wall": prof["prm_ms"] / 1e3 / wall if a.prm else None, "requests": a.requests,
            "rate_req_per_s": a.rate, "wall_s": wall, "requests_per_s": a.requests / wall,
            "branch_tokens_per_s": st["branch_tokens"] / wall, "windows": windows,
            "e2e_s": pct(e2e), "queuing_s": pct(que), "inference_s": pct(inf),
