@@ -17,11 +17,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--warm", type=int, default=3)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--T", type=int, default=400)
+ap.add_argument("--num-blocks", type=int, default=0, help="0: pool from free HBM (use ~40000 under ncu --set full)")
 a = ap.parse_args()
 cfg = dict(bench.C2)
 cfg["T"] = a.T
 shape = SHAPES["1.5B"]
-eng = Engine(shape, "bf16", weight_seed=1, block_size=64, num_blocks=0, max_rows=512, max_requests=256,
+eng = Engine(shape, "bf16", weight_seed=1, block_size=64, num_blocks=a.num_blocks, max_rows=512, max_requests=256,
              max_prompt=1025, T=cfg["T"], cap=cfg["cap"], eos_id=1, profile=True)
 for r in bench.make_requests(0, 1, 0, 200, shape, cfg):
     eng.admit(r)
