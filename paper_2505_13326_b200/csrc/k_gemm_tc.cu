@@ -634,6 +634,21 @@ bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float
   return launch_bn<256, GEMM_SWIGLU>(A, B, bias, C, act, M, N, K, S, s, nullptr, Bt);
 }
 
+// Split count that minimises the wave-quantised time of t output tiles x S splits on the SMs
+// of a persistent launch: cost(S) = ceil(t S / SMs) / S (a unit does 1/S of a tile's K);
+// ties go to fewer splits (less partial traffic).  E.g. t = 32 tiles: S = 4 (128 units, one
+// wave) instead of 5 (160 units = two waves, the second 12 units long).
+static int wave_split(int t, int smax) {
+  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
+  int best = 1;
+  double bc = 1e30;
+  for (int S = 1; S <= smax; ++S) {
+    const double c = (double)((t * S + g_num_sms - 1) / g_num_sms) / S;
+    if (c < bc - 1e-9) { bc = c; best = S; }
+  }
+  return best;
+}
+
 bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const QkvEpi& epi, cudaStream_t s,
                      const bf16* Bt) {
   if (M <= 0) return true;
@@ -644,12 +659,12 @@ bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const Qk
   const int mt = (M + BM - 1) / BM, heads = N / epi.D.hd, kb = (K + BK - 1) / BK;
   int S = 1;
   if (epi.parts && epi.cnt && heads * mt * 8 <= epi.cnt_cap && epi.D.hd >= 128) {
-    S = (g_num_sms + heads * mt / 2) / (heads * mt);
-    S = std::max(1, std::min(S, std::min(8, kb / 2)));
-    // measured on C2: the fused single-pass kernel is 3% faster per step than S = 2 with the
-    // partial round trip, so split-K is opt-in (SART_QKV_SPLIT=max splits) for other shapes
-    static const int smax = getenv("SART_QKV_SPLIT") ? atoi(getenv("SART_QKV_SPLIT")) : 1;
-    S = std::max(1, std::min(S, smax));
+    // measured on C2 (K = 1536): the fused single-pass kernel is 3% faster per step than S = 2
+    // with the partial round trip; long-K projections (14B / 70B, K >= 4096) at small M leave
+    // most SMs idle without splits.  SART_QKV_SPLIT = max splits overrides.
+    static const int smax_env = getenv("SART_QKV_SPLIT") ? atoi(getenv("SART_QKV_SPLIT")) : 0;
+    const int smax = smax_env ? smax_env : 1;
+    S = wave_split(heads * mt, std::max(1, std::min(smax, std::min(8, kb / 2))));
   }
   if (epi.D.hd == 128) return launch_bn<128, GEMM_QKV>(A, B, nullptr, epi.parts, nullptr, M, N, K, S, s, &epi, Bt);
   if (epi.D.hd == 64) return launch_bn<64, GEMM_QKV>(A, B, nullptr, epi.parts, nullptr, M, N, K, S, s, &epi, Bt);
@@ -668,10 +683,7 @@ void choose_split(int M, int N, int K, int& S, int& BN, int& MSUB) {
   if (t256 >= g_num_sms * 3 / 4) { S = 1; BN = 256; return; }
   BN = K >= 4096 ? 256 : 128;
   const int t = mt * ((N + BN - 1) / BN);
-  S = (g_num_sms + t / 2) / t;
-  if (S < 1) S = 1;
-  if (S > 8) S = 8;
-  if (S > kb / 2) S = kb / 2 > 0 ? kb / 2 : 1;
+  S = wave_split(t, std::max(1, std::min(8, kb / 2)));
 }
 
 // ------------------------------------------------------------------ pre-tiled weights

@@ -70,6 +70,10 @@ SHAPES: Dict[str, ModelShape] = {
     "7B": ModelShape("7B", 28, 3584, 28, 4, 128, 18944, 152064),
     # BASELINE.json configs[4]: 48 layers, d=5120, GQA 40/8
     "14B": ModelShape("14B", 48, 5120, 40, 8, 128, 13824, 152064),
+    # The paper's second model (DeepSeek-R1-Distill-Llama-70B = the Llama-3.3-70B shape:
+    # 80 layers, d=8192, GQA 64/8, hd 128, F 28672, V 128256, RoPE theta 5e5).  141 GB of bf16
+    # weights: it runs on ONE B200 (TP = 1) with ~30 GB left for the KV pool.
+    "70B": ModelShape("70B", 80, 8192, 64, 8, 128, 28672, 128256, rope_theta=5.0e5, rms_eps=1.0e-5),
     # Separate PRM decoders (NEXT row f2).  The PRM reads the policy's tokens, so its vocab is
     # the policy's.  prm-tiny / prm-small pair with tiny / small in tests; PRM-7B is the
     # Qwen2.5-Math-PRM-7B shape (= Qwen2.5-7B) over the 1.5B policy's vocab.

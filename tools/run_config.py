@@ -5,6 +5,8 @@
 c1: tiny decoder, 1 request, N=4, M=2, cap 64, T=16, alpha 0.5, beta 2 (BJ configs[0])
 c3: 7B shape, 32 requests/GPU (the per-GPU share of 256 on 8 GPUs), N=16, M=4, cap 8192,
     T=400, alpha 0.5, beta 8, scripted rewards (BJ configs[2]); admission is commitment-limited
+c70: the paper's 70B model shape on ONE B200 (TP = 1; row f4's TP path is not built),
+    16 requests (commitment admits ~66 rows at a time, the rest queue), N=8, M=4, cap 2048, alpha 0.5, beta 4
 c5: 14B shape, 8192-token shared prompt, N=32, M=16, alpha 0.5, beta 16, cap 16384, T=400,
     1 request per GPU (BJ configs[4])
 c2p: C2's workload (1.5B, 64 requests, N=8, M=4, cap 4096, T=400) with PRM pruning
@@ -26,6 +28,9 @@ CONFIGS = {
     "c1": dict(shape="tiny", n_req=1, N=4, M=2, alpha=0.5, beta=2, cap=64, T=16, p=(16, 16), B=64, bs=16),
     "c3": dict(shape="7B", n_req=32, N=16, M=4, alpha=0.5, beta=8, cap=8192, T=400, p=(64, 1024), B=1024, bs=64),
     "c2p": dict(shape="1.5B", n_req=64, N=8, M=4, alpha=0.5, beta=4, cap=4096, T=400, p=(64, 1024), B=512, bs=64),
+    # the paper's 70B model on one GPU (TP = 1): N=8, M=4, cap 2048 (the ~30 GB pool left
+    # after 141 GB of weights commits ~40 rows of 2048 tokens), scripted lengths and rewards
+    "c70": dict(shape="70B", n_req=16, N=8, M=4, alpha=0.5, beta=4, cap=2048, T=400, p=(64, 1024), B=512, bs=64),
     "c5": dict(shape="14B", n_req=1, N=32, M=16, alpha=0.5, beta=16, cap=16384, T=400, p=(8193, 8193), B=64, bs=64),
 }
 
