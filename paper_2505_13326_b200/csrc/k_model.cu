@@ -64,9 +64,10 @@ template <> __device__ __forceinline__ float4 load4<bf16>(const bf16* p) {
   return make_float4(__low2float(a), __high2float(a), __low2float(b), __high2float(b));
 }
 
-// one 128-thread CTA per row, float4 vectorised (d % 4 == 0, checked at init)
+// one CTA per row, float4 vectorised (d % 4 == 0, checked at init); the CTA width depends
+// on d only (rmsnorm_threads), so a row's rounding never depends on the batch size
 template <typename T>
-__global__ void __launch_bounds__(128) k_rmsnorm(float* __restrict__ h, const float* __restrict__ parts, int np,
+__global__ void __launch_bounds__(512) k_rmsnorm(float* __restrict__ h, const float* __restrict__ parts, int np,
                                                   long long pstride, const T* __restrict__ g, T* __restrict__ out,
                                                   float* __restrict__ out32, const int* __restrict__ status, int n,
                                                   int d, float eps) {
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(128) k_rmsnorm(float* __restrict__ h, const fl
   float4* x = reinterpret_cast<float4*>(h + (long long)r * d);
   const int d4 = d >> 2;
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d4; i += 128) {
+  for (int i = threadIdx.x; i < d4; i += blockDim.x) {
     float4 v = x[i];
     for (int sp = 0; sp < np; ++sp) {   // split order: deterministic
       const float4 p = reinterpret_cast<const float4*>(parts + sp * pstride + (long long)r * d)[i];
@@ -86,13 +87,15 @@ __global__ void __launch_bounds__(128) k_rmsnorm(float* __restrict__ h, const fl
     if (np) x[i] = v;
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
-  __shared__ float red[4];
+  __shared__ float red[16];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  const float inv = rsqrtf((red[0] + red[1] + red[2] + red[3]) / d + eps);
-  for (int i = threadIdx.x; i < d4; i += 128) {
+  float tot = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];   // fixed order
+  const float inv = rsqrtf(tot / d + eps);
+  for (int i = threadIdx.x; i < d4; i += blockDim.x) {
     const float4 v = x[i];
     const float4 gg = load4<T>(g + 4 * i);
     const float4 y = make_float4(v.x * inv * gg.x, v.y * inv * gg.y, v.z * inv * gg.z, v.w * inv * gg.w);
@@ -100,12 +103,20 @@ __global__ void __launch_bounds__(128) k_rmsnorm(float* __restrict__ h, const fl
     if (out32) reinterpret_cast<float4*>(out32 + (long long)r * d)[i] = y;
   }
 }
+// 128 threads up to d = 2048 (C2: d = 1536), then ~16 elements per thread up to 512 threads:
+// small-M decode (14B / 70B) has few rows, and a 128-thread CTA per 8192-wide row left the
+// kernel latency-bound (19.6 us per launch at 64 rows on the 70B shape)
+static int rmsnorm_threads(int d) {
+  int t = 128;
+  while (t < 512 && d / t > 16) t *= 2;
+  return t;
+}
 template <typename T>
 void launch_rmsnorm(float* h, const float* parts, int np, const T* g, T* out, float* out32, const int* status, int n,
                     int d, float eps, cudaStream_t s) {
   if (n > 0)
-    launch_pdl(k_rmsnorm<T>, dim3(n), dim3(128), 0, s, h, parts, np, (long long)n * d, g, out, out32, status, n, d,
-               eps);
+    launch_pdl(k_rmsnorm<T>, dim3(n), dim3(rmsnorm_threads(d)), 0, s, h, parts, np, (long long)n * d, g, out, out32,
+               status, n, d, eps);
 }
 
 // ------------------------------------------------------------ RoPE + KV append

@@ -296,6 +296,22 @@ template <typename T>
 void qkv_rope(sart_ctx* ctx, int l, int n, RopeArgs ra) {
   const Dims& D = ctx->D;
   const float* bias = ctx->fparams + ctx->f_bqkv + (size_t)l * D.qkv;
+  // long-K QKV (14B / 70B, K >= 4096) at small M: the fused kernel has one CTA per (head,
+  // m-tile) -- 80 CTAs on 148 SMs for 70B at M <= 128 -- and streams the weights at half the
+  // HBM rate, so it runs as a wave-split GEMM + the RoPE / append kernel instead
+  bool fused = true;
+  if constexpr (std::is_same<T, bf16>::value) {
+    static int nsm = 0;
+    if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->cfg.device);
+    fused = !(D.d >= 4096 && (D.qkv / D.hd) * ((n + 127) / 128) < nsm * 3 / 4);
+  }
+  if (!fused) {
+    int np = proj<T>(ctx, (T*)ctx->a, ctx->W_<T>(t_layer(l, 1)), n, D.qkv, D.d);
+    launch_rope_append<T>(ctx->parts, np, bias, (T*)ctx->q, (T*)ctx->pool, ctx->rope_cs, D, l, ctx->rows, ctx->reqs,
+                          ra, n, ctx->st);
+    ctx->launches++;
+    return;
+  }
   if constexpr (std::is_same<T, bf16>::value) {
     QkvEpi e{bias,       (bf16*)ctx->q, (bf16*)ctx->pool, ctx->rope_cs, D,           l,
              ctx->rows, ctx->reqs,    ra,               ctx->parts,    ctx->qkv_cnt, ctx->qkv_cnt_cap};
