@@ -273,6 +273,19 @@ int sart_debug_fetch(sart_ctx* ctx, int32_t what, int32_t layer, void* host_out,
 int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const uint16_t* B, const float* bias,
                     float* C, int32_t mode, int32_t splits, int32_t bn, int32_t bm);
 
+/* Host-only test hook (no GPU needed): the packing plan of one f2 PRM pass.  Row r (n rows)
+ * has ell[r] - ell_ws[r] >= 0 new suffix entries starting at entry ell_ws[r]; they are laid
+ * back to back in chunks of <= chunk tokens, rows straddling chunk boundaries in order.
+ * out receives int32x4 records [segments | query blocks | gathers] (cap records):
+ *   segment {first token in chunk, count, row, first entry};
+ *   query block {first token, count <= qp, row, first entry} (inside one segment);
+ *   gather {row, token of the row's last entry, 0, 0} (in the chunk where the row ends);
+ * chunks receives (tokens, segments, query blocks, gathers) per chunk (chunk_cap chunks).
+ * Counts are always written; EFULL when a buffer is too small (nothing else written). */
+int sart_debug_prm_plan(const int32_t* ell_ws, const int32_t* ell, int32_t n, int32_t chunk, int32_t qp,
+                        int32_t* out, int32_t cap, int32_t* n_seg, int32_t* n_qb, int32_t* n_gat, int32_t* chunks,
+                        int32_t chunk_cap, int32_t* n_chunks);
+
 typedef struct {
   double attn_ms;          /* sum of attention-kernel durations (CUDA events)    */
   int64_t attn_launches;

@@ -452,6 +452,54 @@ void prefill_batch(sart_ctx* ctx, sart_ctx* src, int ntok) {
   }
 }
 
+// Packing plan of one f2 PRM pass (host only; also exported as sart_debug_prm_plan): row r
+// has ell[r] - ell_ws[r] new suffix entries starting at entry ell_ws[r]; they are laid back
+// to back in chunks of <= Wc tokens (a row that does not fit continues in the next chunk).
+// Per chunk: segments {first token, count, row, first entry}, query blocks of <= QP entries
+// inside a segment {first token, count, row, first entry}, and gathers {row, token of its
+// last entry} for the rows that end in the chunk.
+struct PrmPlan {
+  struct Chunk { int ntok, seg, nseg, qb, nqb, gat, ngat; };
+  std::vector<Chunk> chunks;
+  std::vector<int4> seg, qb, gat;
+  long long entries = 0;
+};
+PrmPlan plan_prm_pass(const int* ell_ws, const int* ell, int n, int Wc, int QP) {
+  PrmPlan P;
+  int fill = 0;
+  PrmPlan::Chunk cur{0, 0, 0, 0, 0, 0, 0};
+  auto close_chunk = [&]() {
+    if (cur.ntok == 0) return;
+    P.chunks.push_back(cur);
+    cur = PrmPlan::Chunk{0, (int)P.seg.size(), 0, (int)P.qb.size(), 0, (int)P.gat.size(), 0};
+    fill = 0;
+  };
+  for (int r = 0; r < n; ++r) {
+    const int cnt = ell[r] - ell_ws[r];
+    P.entries += std::max(0, cnt);
+    for (int j = 0; j < cnt;) {
+      const int take = std::min(cnt - j, Wc - fill);
+      const int e0 = ell_ws[r] + j;
+      P.seg.push_back(make_int4(fill, take, r, e0));
+      cur.nseg++;
+      for (int k = 0; k < take; k += QP) {
+        P.qb.push_back(make_int4(fill + k, std::min(QP, take - k), r, e0 + k));
+        cur.nqb++;
+      }
+      if (j + take == cnt) {
+        P.gat.push_back(make_int4(r, fill + take - 1, 0, 0));
+        cur.ngat++;
+      }
+      fill += take;
+      cur.ntok = fill;
+      j += take;
+      if (fill == Wc) close_chunk();
+    }
+  }
+  close_chunk();
+  return P;
+}
+
 // Row f2: the separate PRM decoder reads every row's suffix entries decoded in this window
 // (entries ell_ws .. ell-1, reading R42) through its own paged KV -- the prefix was
 // prefilled at admission -- and its head scores the last entry's final-norm state.  The
@@ -472,43 +520,10 @@ void prm_model_scores(sart_ctx* ctx, int n) {
   CK_VOID(cudaStreamSynchronize(s));
   if (ncu_range) cudaProfilerStart();
   CK_VOID(cudaEventRecord(m->prm_ev[0], s));
-  const int QP = prefill_query_block(D), Wc = m->prm_chunk;
-  struct Chunk { int ntok, seg, nseg, qb, nqb, gat, ngat; };
-  std::vector<Chunk> chunks;
-  std::vector<int4> seg, qb, gat;
-  std::vector<std::pair<size_t, size_t>> spans;   // per chunk: [seg begin, qb begin, gat begin) offsets
-  int fill = 0;
-  Chunk cur{0, 0, 0, 0, 0, 0, 0};
-  auto close_chunk = [&]() {
-    if (cur.ntok == 0) return;
-    chunks.push_back(cur);
-    cur = Chunk{0, (int)seg.size(), 0, (int)qb.size(), 0, (int)gat.size(), 0};
-    fill = 0;
-  };
-  long long entries = 0;
-  for (int r = 0; r < n; ++r) {
-    const int cnt = m->h_ell[r] - m->h_ell_ws[r];
-    entries += std::max(0, cnt);
-    for (int j = 0; j < cnt;) {
-      const int take = std::min(cnt - j, Wc - fill);
-      const int e0 = m->h_ell_ws[r] + j;
-      seg.push_back(make_int4(fill, take, r, e0));
-      cur.nseg++;
-      for (int k = 0; k < take; k += QP) {
-        qb.push_back(make_int4(fill + k, std::min(QP, take - k), r, e0 + k));
-        cur.nqb++;
-      }
-      if (j + take == cnt) {
-        gat.push_back(make_int4(r, fill + take - 1, 0, 0));
-        cur.ngat++;
-      }
-      fill += take;
-      cur.ntok = fill;
-      j += take;
-      if (fill == Wc) close_chunk();
-    }
-  }
-  close_chunk();
+  const PrmPlan pl = plan_prm_pass(m->h_ell_ws, m->h_ell, n, m->prm_chunk, prefill_query_block(D));
+  const std::vector<int4>&seg = pl.seg, &qb = pl.qb, &gat = pl.gat;
+  const std::vector<PrmPlan::Chunk>& chunks = pl.chunks;
+  const long long entries = pl.entries;
   // one upload: [all segments | all q-blocks | all gathers]
   const size_t nd = seg.size() + qb.size() + gat.size();
   if (nd > m->prm_desc_cap) {
@@ -523,7 +538,7 @@ void prm_model_scores(sart_ctx* ctx, int n) {
   const int4* dseg = m->prm_desc;
   const int4* dqb = m->prm_desc + seg.size();
   const int4* dgat = m->prm_desc + seg.size() + qb.size();
-  for (const Chunk& c : chunks) {
+  for (const PrmPlan::Chunk& c : chunks) {
     const int nt = c.ntok;
     const RopeArgs ra{nullptr, m->prm_ent, m->prm_row};
     launch_prm_tokens(D, m->rows, m->reqs, dseg + c.seg, c.nseg, m->prm_tok, m->prm_row, m->prm_ent, s);
@@ -1565,6 +1580,31 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
   }
   cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dact); if (dbias) cudaFree(dbias); if (dBt) cudaFree(dBt);
   if (e != cudaSuccess) return set_err(SART_ECUDA, cudaGetErrorString(e));
+  return SART_OK;
+}
+
+int sart_debug_prm_plan(const int32_t* ell_ws, const int32_t* ell, int32_t n, int32_t chunk, int32_t qp,
+                        int32_t* out, int32_t cap, int32_t* n_seg, int32_t* n_qb, int32_t* n_gat, int32_t* chunks,
+                        int32_t chunk_cap, int32_t* n_chunks) {
+  if ((n > 0 && (!ell_ws || !ell)) || !out || !n_seg || !n_qb || !n_gat || !chunks || !n_chunks || n < 0 ||
+      chunk < 1 || qp < 1)
+    return set_err(SART_EINVAL, "bad args");
+  for (int r = 0; r < n; ++r)
+    if (ell[r] < ell_ws[r]) return set_err(SART_EINVAL, "ell < ell_ws");
+  const PrmPlan P = plan_prm_pass(ell_ws, ell, n, chunk, qp);
+  *n_seg = (int32_t)P.seg.size();
+  *n_qb = (int32_t)P.qb.size();
+  *n_gat = (int32_t)P.gat.size();
+  *n_chunks = (int32_t)P.chunks.size();
+  const size_t nd = P.seg.size() + P.qb.size() + P.gat.size();
+  if (nd > (size_t)cap || P.chunks.size() > (size_t)chunk_cap) return set_err(SART_EFULL, "buffers too small");
+  int32_t* o = out;
+  for (const auto* v : {&P.seg, &P.qb, &P.gat})
+    for (const int4& x : *v) { o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w; o += 4; }
+  for (size_t c = 0; c < P.chunks.size(); ++c) {
+    const PrmPlan::Chunk& k = P.chunks[c];
+    chunks[4 * c] = k.ntok; chunks[4 * c + 1] = k.nseg; chunks[4 * c + 2] = k.nqb; chunks[4 * c + 3] = k.ngat;
+  }
   return SART_OK;
 }
 

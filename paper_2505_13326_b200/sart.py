@@ -127,7 +127,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.sart_set_profile.argtypes = [C.c_void_p, C.c_int32]
     lib.sart_debug_gemm.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_int32, C.c_int32, C.c_int32, C.c_int32]
-    for f in ("sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
+    lib.sart_debug_prm_plan.argtypes = [P32, P32, C.c_int32, C.c_int32, C.c_int32, P32, C.c_int32, P32, P32, P32,
+                                        P32, C.c_int32, P32]
+    for f in ("sart_debug_prm_plan", "sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
               "sart_get_state", "sart_debug_fetch", "sart_get_profile", "sart_reset_profile", "sart_debug_gemm", "sart_set_profile"):
         getattr(lib, f).restype = C.c_int
     _lib = lib
@@ -136,7 +138,24 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 
 EXPORTED = ["sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
             "sart_strerror", "sart_last_error", "sart_get_state", "sart_debug_fetch", "sart_get_profile",
-            "sart_reset_profile", "sart_debug_gemm", "sart_set_profile"]
+            "sart_reset_profile", "sart_debug_gemm", "sart_set_profile", "sart_debug_prm_plan"]
+
+
+def debug_prm_plan(ell_ws, ell, chunk: int, qp: int):
+    """sart_debug_prm_plan (host only): returns (segments, qblocks, gathers, chunks) as int
+    arrays [k][4] (chunks: tokens, segments, q-blocks, gathers)."""
+    lib = load_library()
+    ws, el = _i32(ell_ws), _i32(ell)
+    n = len(ws)
+    cap = 3 * n + 4 * (int(np.sum(el - ws)) // max(1, min(chunk, qp)) + 8) + 64
+    out = np.zeros((cap, 4), np.int32)
+    ch = np.zeros((int(np.sum(el - ws)) // chunk + n + 2, 4), np.int32)
+    ns, nq, ng, nc = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+    _check(lib.sart_debug_prm_plan(ws.ctypes.data_as(P32), el.ctypes.data_as(P32), n, chunk, qp,
+                                   out.ctypes.data_as(P32), cap, C.byref(ns), C.byref(nq), C.byref(ng),
+                                   ch.ctypes.data_as(P32), len(ch), C.byref(nc)))
+    a, b, c = ns.value, nq.value, ng.value
+    return out[:a], out[a:a + b], out[a + b:a + b + c], ch[:nc.value]
 
 
 def debug_gemm(A_bits: np.ndarray, B_bits: np.ndarray, bias=None, C=None, mode: int = 0, splits: int = 1,
