@@ -1197,6 +1197,7 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     pl.CH = 512;   // tokens per attention chunk (SART_ATTN_CH overrides; multiple of 64)
     if (const char* e = getenv("SART_ATTN_CH")) pl.CH = std::max(64, atoi(e) / 64 * 64);
     pl.qr_max = std::max(1, std::min(SART_MAXN, 64 / D.g));
+    if (const char* e = getenv("SART_ATTN_QR")) pl.qr_max = std::max(1, std::min(SART_MAXN, atoi(e)));   // A/B
     pl.npc_max = std::max(1, cdiv(cfg.max_prompt - 1, pl.CH));
     const int nsc_max = cdiv(D.cap, pl.CH);
     pl.nslot = pl.npc_max + nsc_max;
