@@ -1,0 +1,13 @@
+#!/bin/bash
+# compute-sanitizer memcheck over the smallest end-to-end paths: smoke (C1 control + logits)
+# and the f2 PRM-model pass (tiny policy + prm-tiny, bf16 and fp32).
+mkdir -p gpurun_out
+timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" \
+  > gpurun_out/sanitize_smoke.log 2>&1; echo smoke_rc=$?; tail -3 gpurun_out/sanitize_smoke.log
+timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_prm_model.py -x -q \
+  -k "tiny-prm-tiny-bf16-16-40-None or tiny-prm-tiny-fp32-16-40-100" > gpurun_out/sanitize_f2.log 2>&1; echo f2_rc=$?; tail -3 gpurun_out/sanitize_f2.log
+# shared-memory races and barrier misuse on the same small paths
+for tool in racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests/test_gpu_prm_model.py -x -q \
+    -k "tiny-prm-tiny-bf16-16-40-None" > gpurun_out/sanitize_$tool.log 2>&1; echo ${tool}_rc=$?; tail -2 gpurun_out/sanitize_$tool.log
+done
