@@ -11,3 +11,10 @@ for tool in racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests/test_gpu_prm_model.py -x -q \
     -k "tiny-prm-tiny-bf16-16-40-None" > gpurun_out/sanitize_$tool.log 2>&1; echo ${tool}_rc=$?; tail -2 gpurun_out/sanitize_$tool.log
 done
+# memcheck over the small-shape decode parity (cascade attention, tcgen05 GEMMs, sampler, prefill)
+# and the on-device control traces
+if [ -n "$SANITIZE_DECODE" ]; then
+timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_parity.py tests/test_gpu_control.py -x -q \
+  -k "tiny_bf16 or small_gqa or sampler or trace_A or trace_B or random_scripted_workloads[0] or tight_pool[16-4]" \
+  > gpurun_out/sanitize_decode.log 2>&1; echo decode_rc=$?; tail -3 gpurun_out/sanitize_decode.log
+fi
