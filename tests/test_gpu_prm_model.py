@@ -129,3 +129,43 @@ def test_prm_model_control_matches_oracle_engine_fp32():
     assert len(gres) == len(prompts)
     assert sum(r["num_pruned"] for r in ores) > 0, "workload must exercise pruning"
     compare_results(gres, ores, {rid: N for rid in range(len(prompts))}, score_tol=1e-5)
+
+
+def test_prm_model_production_tiles_1p5b_shape():
+    """The f2 pass with production tile shapes: a 1.5B-shape policy and a 1.5B-shape PRM (hd 128,
+    GQA 12/2 -> six q heads per prefill CTA, 4-stage ring), 2 layers each, 64 rows, prompts of
+    64-200 tokens in 64-token blocks (multi-page prefixes, ragged tails); 8 sampled rows are
+    checked at both boundaries against the uncached oracle forward (bf16, abs 2e-2)."""
+    pol = SHAPES["1.5B"].with_layers(2)
+    prm = SHAPES["1.5B"].with_layers(2)
+    wp = gen_weights(pol, "bf16", std=0.02)
+    wm = gen_weights(prm, "bf16", std=0.02, root_seed=0x79)
+    N, n_req, T, cap = 4, 16, 16, 32
+    prompts = [gen_prompt(300 + i, pol.vocab, EOS, 64, 200) for i in range(n_req)]
+    rng = np.random.default_rng(8)
+    forced = {rid: rng.integers(2, pol.vocab, size=(N, cap)).astype(np.int32) for rid in range(n_req)}
+    g = gpu_engine(pol, "bf16", wp, block_size=64, num_blocks=2048, max_rows=64, max_requests=32, max_prompt=201, T=T,
+                   cap=cap, eos_id=EOS, temperature=1.0, sampler_seed=3, enable_forced_tokens=True, prm_shape=prm,
+                   prm_host_weights=pack_blob(prm, wm, "bf16"))
+    for rid in range(n_req):
+        g.admit(Request(rid, prompts[rid], N, N, -1.0, 0, None), forced_tokens=forced[rid])
+    m = Model(prm, wm)
+    sampled = {(0, 0), (3, 3), (7, 1), (9, 2), (11, 0), (13, 3), (14, 2), (15, 1)}
+    worst, seen = 0.0, 0
+    for w in (1, 2):
+        g.step(1)
+        ids = g.debug_fetch(DBG_ROWIDS)
+        sc = g.debug_fetch(DBG_PRM_SCORES)
+        assert len(ids) == n_req * N
+        for i, k in enumerate(ids):
+            key = (int(k) >> 8, int(k) & 0xFF)
+            if key not in sampled:
+                continue
+            rid, b = key
+            seq = [int(t) for t in prompts[rid]] + [int(t) for t in forced[rid][b, : w * T - 1]]
+            worst = max(worst, abs(float(sc[i]) - m.prm_model_score(seq)))
+            seen += 1
+    g.close()
+    print(f"f2 1.5B-shape tiles: {seen} sampled row scores, worst abs err {worst:.2e}")
+    assert seen == 2 * len(sampled)
+    assert worst <= 2e-2, worst
