@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--prm", default=None, help="separate PRM decoder shape (row f2), e.g. PRM-7B")
     ap.add_argument("--requests", type=int, default=0, help="override the config's request count")
+    ap.add_argument("--num-blocks", type=int, default=0, help="KV pool blocks (0: from free HBM; ncu needs room)")
     a = ap.parse_args()
     import torch
     from paper_2505_13326_b200 import Engine
@@ -53,7 +54,7 @@ def main():
     prm = SHAPES[a.prm] if a.prm else None
     stream = torch.cuda.current_stream()
     t0 = time.time()
-    eng = Engine(shape, "bf16", weight_seed=3, block_size=c["bs"], num_blocks=0, max_rows=c["B"], max_requests=256,
+    eng = Engine(shape, "bf16", weight_seed=3, block_size=c["bs"], num_blocks=a.num_blocks, max_rows=c["B"], max_requests=256,
                  max_prompt=c["p"][1] + 1, T=c["T"], cap=c["cap"], eos_id=1, temperature=1.0, sampler_seed=5,
                  stream=stream.cuda_stream, prm_shape=prm, prm_weight_seed=11)
     init_s = time.time() - t0
