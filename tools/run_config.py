@@ -51,7 +51,10 @@ def main():
     if a.requests:
         c["n_req"] = a.requests
     shape = SHAPES[c["shape"]]
-    prm = SHAPES[a.prm] if a.prm else None
+    prm = None
+    if a.prm:   # the PRM reads the policy's tokens: give it the policy's vocab
+        import dataclasses
+        prm = dataclasses.replace(SHAPES[a.prm], vocab=shape.vocab)
     stream = torch.cuda.current_stream()
     t0 = time.time()
     eng = Engine(shape, "bf16", weight_seed=3, block_size=c["bs"], num_blocks=a.num_blocks, max_rows=c["B"], max_requests=256,
