@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(512) k_rmsnorm(float* __restrict__ h, const fl
 // small-M decode (14B / 70B) has few rows, and a 128-thread CTA per 8192-wide row left the
 // kernel latency-bound (19.6 us per launch at 64 rows on the 70B shape)
 static int rmsnorm_threads(int d) {
+  if (d % 128 == 0 && d / 4 <= 512) return d / 4;   // one float4 per thread (C2: 384 threads)
   int t = 128;
   while (t < 512 && d / t > 16) t *= 2;
   return t;
