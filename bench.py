@@ -23,7 +23,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -42,6 +41,7 @@ def parse():
     ap.add_argument("--impl", default="sart", choices=["sart", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=8, help="timed oracle decode steps of the cpu_baseline leg")
     ap.add_argument("--T", type=int, default=C2["T"])
     ap.add_argument("--attn-mode", type=int, default=0)
     return ap.parse_args()
@@ -106,66 +106,138 @@ def make_requests(rank: int, world: int, first: int, count: int, shape, cfg):
     return reqs[rank::world]          # round-robin partition by arrival index
 
 
-def request_bytes(r):
-    b = r.prompt.nbytes
-    if r.script is not None:
-        b += r.script.forced_len.nbytes + r.script.scores.nbytes + r.script.final_score.nbytes + r.script.answer.nbytes
-    return b
-
-
 # ------------------------------------------------------------------ oracle (CPU) arm
-def oracle_sample(steps: int, warmup: int, T: int):
-    """The oracle as it stands (fp64 numpy) on a bounded C2 sample: 1 request with N=8
-    branches (1.5B shape, P=64 prompt, scripted lengths), timed per decode step."""
+def _oracle_threads():
+    """BLAS threads pinned to the cores this process may use."""
+    cores = len(os.sched_getaffinity(0))
+    import numpy  # noqa: F401  (load the BLAS first: threadpoolctl acts on loaded libraries only)
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        lim = threadpool_limits(limits=cores)
+        used = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+        return lim, cores, used
+    except Exception:
+        return None, cores, cores
+
+
+def _timing_weights(shape):
+    """Timing input only: the oracle's cost does not depend on the weight values, so the
+    tensors are filled by tiling one seeded 16M-entry normal block (seconds, instead of
+    drawing 1.5B normals)."""
     import numpy as np
+    from synth import weight_names, weight_shapes
+    blk = (np.random.default_rng(0).standard_normal(1 << 24, dtype=np.float32) * 0.02)
+    w = {}
+    for name, shp in weight_shapes(shape).items():
+        n = int(np.prod(shp))
+        a = np.resize(blk, n).reshape(shp)
+        if name.endswith("norm"):
+            a = a + 1.0
+        w[name] = a
+    return w
+
+
+def oracle_c2_slice(timed: int, warmup: int):
+    """BASELINE.md §4 leg 2: a C2 slice -- 1 request, N=8 branches, P=544, 1.5B shape,
+    scripted lengths -- through the oracle engine (fp64 NumPy, model mode).  The first
+    window holds the prefill and is not timed; then `warmup` untimed and `timed` timed decode
+    steps.  Returns per-step seconds."""
     from oracle.engine import Engine as OEngine, EngineConfig, ModelSource
     from oracle.model import Model
     from synth import SHAPES, gen_requests
     shape = SHAPES[C2["shape"]]
     t0 = time.time()
-    # timing input only: plain fp32 normals (the values do not change the oracle's cost)
-    rng = np.random.default_rng(0)
-    w = {}
-    from synth import weight_names, weight_shapes
-    shp = weight_shapes(shape)
-    for name in weight_names(shape):
-        w[name] = (rng.standard_normal(shp[name], dtype=np.float32) * 0.02).astype(np.float32)
-        if name.endswith("norm"):
-            w[name] += 1.0
+    w = _timing_weights(shape)
     gen_s = time.time() - t0
     cfg = EngineConfig(block_size=64, num_blocks=4096, T=1, cap=C2["cap"], eos_id=1)
     eng = OEngine(cfg, ModelSource(Model(shape, w), cfg, prm_scores=False))
-    req = gen_requests(1, shape, C2["N"], C2["M"], C2["alpha"], C2["beta"], C2["cap"], T, eos_id=1,
-                       p_range=(64, 64))[0]
+    req = gen_requests(1, shape, C2["N"], C2["M"], C2["alpha"], C2["beta"], C2["cap"], C2["T"], eos_id=1,
+                       p_range=(544, 544), first_id=0)[0]
     eng.admit(req)
+    t = time.perf_counter()
+    eng.step(1)                                   # prefill (543 tokens) + decode step 1
+    prefill_s = time.perf_counter() - t
     times = []
-    for i in range(warmup + steps):
+    for i in range(warmup + timed):
         t = time.perf_counter()
         eng.step(1)
-        dt = time.perf_counter() - t
         if i >= warmup:
-            times.append(dt)
-    cores = len(os.sched_getaffinity(0))
-    per_step = sum(times) / len(times)
-    return dict(value=C2["N"] / per_step, unit="branch-tokens/s", cores=cores, kind="oracle",
-                sample=f"1 request x N={C2['N']} branches, 1.5B shape fp64 numpy, P=64, {steps} timed decode "
-                       f"steps after {warmup} warm-up (first includes prefill); weight gen {gen_s:.0f}s untimed",
-                step_s=per_step)
+            times.append(time.perf_counter() - t)
+    return dict(times=times, prefill_s=prefill_s, gen_s=gen_s)
+
+
+def oracle_c1_full():
+    """BASELINE.md §4 leg 1: C1 in full -- tiny decoder, 1 request, N=4, M=2, cap 64, T=16,
+    alpha 0.5, beta 2, model mode (sampler + PRM head) -- through the oracle engine."""
+    from oracle.engine import Engine as OEngine, EngineConfig, ModelSource
+    from oracle.model import Model
+    from synth import SHAPES, gen_requests, gen_weights
+    shape = SHAPES["tiny"]
+    cfg = EngineConfig(block_size=16, num_blocks=256, T=16, cap=64, eos_id=1)
+    eng = OEngine(cfg, ModelSource(Model(shape, gen_weights(shape, "bf16", std=0.02)), cfg))
+    req = gen_requests(1, shape, 4, 2, 0.5, 2, 64, 16, eos_id=1, p_range=(16, 16), scripted=False)[0]
+    eng.admit(req)
+    t = time.perf_counter()
+    st = eng.step(1000)
+    el = time.perf_counter() - t
+    return dict(value=st["branch_tokens"] / el, unit="branch-tokens/s", tokens=st["branch_tokens"], s=el)
+
+
+def oracle_control_replay():
+    """BASELINE.md §4 leg 3: control only -- the oracle's Algorithm 1 engine replaying scripted
+    token/score streams (no model) on a C3-shaped slice: 8 requests, N=16, M=4, alpha 0.5,
+    beta 8, cap 8192, T=400 (the GPU's per-rank share of C3 is 32 requests)."""
+    from oracle.engine import Engine as OEngine, EngineConfig, ScriptedSource
+    from synth import SHAPES, gen_requests
+    shape = SHAPES["7B"]
+    cfg = EngineConfig(block_size=64, num_blocks=1 << 20, T=400, cap=8192, eos_id=1)
+    eng = OEngine(cfg, ScriptedSource(1))
+    for r in gen_requests(8, shape, 16, 4, 0.5, 8, 8192, 400, eos_id=1, p_range=(64, 1024)):
+        eng.admit(r)
+    t = time.perf_counter()
+    st = eng.step(1 << 20)
+    el = time.perf_counter() - t
+    return dict(boundaries_per_s=st["windows"] / el, requests_per_s=st["finalized_total"] / el,
+                windows=st["windows"], requests=st["finalized_total"], s=el)
+
+
+def cpu_baseline_legs(timed: int, warmup: int):
+    lim, cores, used = _oracle_threads()
+    c2 = oracle_c2_slice(timed, warmup)
+    med = statistics.median(c2["times"])
+    legs = {"c2_slice": {"value": C2["N"] / med, "unit": "branch-tokens/s", "median_step_s": med,
+                         "min_step_s": min(c2["times"]), "max_step_s": max(c2["times"]),
+                         "prefill_s": c2["prefill_s"], "timed_steps": len(c2["times"])}}
+    try:
+        legs["c1_full"] = oracle_c1_full()
+    except Exception as e:
+        legs["c1_full"] = {"failed": repr(e)}
+    try:
+        legs["control_replay_c3_slice"] = oracle_control_replay()
+    except Exception as e:
+        legs["control_replay_c3_slice"] = {"failed": repr(e)}
+    return dict(value=legs["c2_slice"]["value"], unit="branch-tokens/s", cores=used, kind="oracle",
+                sample=f"C2 slice (BASELINE.md §4): 1 request x N={C2['N']} branches, 1.5B shape, fp64 NumPy, "
+                       f"P=544, model mode; median of {len(c2['times'])} timed decode steps after the prefill "
+                       f"window and {warmup} warm-up steps; weights tiled from one seeded block "
+                       f"({c2['gen_s']:.0f}s, untimed)",
+                legs=legs, step_s=med)
 
 
 def run_reference(args, rank, world):
+    """The base contract's reference arm: the oracle as it stands, on the host cores, rank 0
+    only (other ranks exit without work).  A step = one decode step of the C2 slice."""
     if rank != 0:
         return
-    r = oracle_sample(args.steps, max(1, args.warmup), args.T)
+    r = cpu_baseline_legs(args.steps, max(1, args.warmup))
     line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": r["unit"], "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["step_s"] * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2 oracle sample (BASELINE.json configs[1])", "shape": "1.5B",
-                       "branches": C2["N"], "M": C2["M"], "cap": C2["cap"]},
-            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": {"workload": "C2 (BASELINE.json configs[1]) oracle slice: 1 request, N=8, M=4, cap 4096, "
+                                   "P=544, 1.5B shape", "step": "one decode step of the slice"},
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "legs")},
             "e2e": {"value": r["value"], "unit": r["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
 
 
 def step_roofline(shape, n_avg, attn_bytes_step, ms_step, peaks):
@@ -199,6 +271,80 @@ def step_roofline(shape, n_avg, attn_bytes_step, ms_step, peaks):
 
 
 # ------------------------------------------------------------------ GPU arm
+def relaunch(args) -> int:
+    """`bench.py --gpus N` without a torch.distributed environment: start the N ranks here
+    (one process per GPU, the driver's own torchrun command line) and pass rank 0's line on."""
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def make_engine(shape, cfg, rank, local, stream, attn_mode):
+    from paper_2505_13326_b200 import Engine
+    return Engine(shape, "bf16", weight_seed=1234 + rank, block_size=cfg["block_size"], num_blocks=0,
+                  max_rows=cfg["concurrent"] * cfg["N"], max_requests=256, max_prompt=cfg["p_range"][1] + 1,
+                  T=cfg["T"], cap=cfg["cap"], eos_id=1, temperature=1.0, sampler_seed=7, device=local,
+                  stream=stream.cuda_stream, profile=False, attn_mode=attn_mode)
+
+
+def e2e_leg(shape, cfg, rank, world, local, stream, attn_mode):
+    """End to end through the public C-ABI, from an empty engine: sart_admit one C2 batch (64
+    requests per GPU) from host buffers, sart_step + sart_collect until every one of them is
+    finalized and collected, then the C2 gather of the result records to rank 0 (NCCL).  Wall
+    clock on the host around all of it (max over ranks).  H2D / D2H are the bytes the library
+    itself copied (sart_profile), i.e. prompts, scripts, admission events and prefill token
+    lists up; counter records, finalized records and the selected branches' tokens down."""
+    import torch
+    import torch.distributed as dist
+    from paper_2505_13326_b200 import dist as sdist
+    eng = make_engine(shape, cfg, rank, local, stream, attn_mode)
+    reqs = make_requests(rank, world, 1 << 20, cfg["concurrent"], shape, cfg)
+    want = len(reqs)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    eng.reset_profile()
+    t0 = time.perf_counter()
+    for r in reqs:
+        eng.admit(r)
+    got, windows, tokens = [], 0, 0
+    while len(got) < want:
+        st = eng.step(1)
+        windows += 1
+        got += eng.collect()
+        if st["live_rows"] == 0 and st["queued_requests"] == 0 and st["queued_branches"] == 0 and len(got) < want:
+            raise RuntimeError("engine idle before every admitted request was collected")
+    tokens = st["branch_tokens"]
+    recs = sdist.gather_result_records(got, f"cuda:{local}") if world > 1 else None   # C2 (NCCL)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    prof = eng.profile()
+    eng.close()
+    v = torch.tensor([el, float(tokens), float(len(got)), float(windows), float(prof["h2d_bytes"]),
+                      float(prof["d2h_bytes"])], dtype=torch.float64, device="cuda")
+    if world > 1:
+        mx = v.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(v, op=dist.ReduceOp.SUM)
+        v[0], v[3] = mx[0], mx[3]
+    el_max, tok_all, req_all, win_max, h2d, d2h = (float(x) for x in v)
+    if recs is not None and rank == 0:
+        assert recs.shape[0] == int(req_all), (recs.shape, req_all)
+    return {"value": tok_all / el_max, "unit": "branch-tokens/s", "requests_per_s": req_all / el_max,
+            "requests": int(req_all), "windows": int(win_max), "wall_s": el_max,
+            "h2d_bytes_per_step": int(h2d / max(1.0, win_max * world)),
+            "d2h_bytes_per_step": int(d2h / max(1.0, win_max * world)),
+            "step": "one window (per GPU)",
+            "includes": "sart_admit of one C2 batch from host buffers (64 requests/GPU, empty engine), every "
+                        "window until all are finalized (prefill, decode, boundaries, tail), sart_collect, "
+                        + ("NCCL gather of the result records to rank 0" if world > 1 else "no gather (N=1)")}
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -207,9 +353,10 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     import torch
     import torch.distributed as dist
-    from paper_2505_13326_b200 import Engine
     from synth import SHAPES
 
     torch.cuda.set_device(local)
@@ -219,10 +366,7 @@ def main():
     cfg = dict(C2)
     cfg["T"] = args.T
     stream = torch.cuda.current_stream()
-    eng = Engine(shape, "bf16", weight_seed=1234 + rank, block_size=cfg["block_size"], num_blocks=0,
-                 max_rows=cfg["concurrent"] * cfg["N"], max_requests=256, max_prompt=cfg["p_range"][1] + 1,
-                 T=cfg["T"], cap=cfg["cap"], eos_id=1, temperature=1.0, sampler_seed=7, device=local,
-                 stream=stream.cuda_stream, profile=False, attn_mode=args.attn_mode)
+    eng = make_engine(shape, cfg, rank, local, stream, args.attn_mode)
     windows_needed = args.warmup + args.steps
     # backlog: enough requests that 64 stay resident for every window (~12 finalize per window)
     n_backlog = cfg["concurrent"] + 24 * windows_needed
@@ -235,8 +379,7 @@ def main():
     def window():
         st = eng.step(1)
         if world > 1:     # C1: all-gather of the admission counters
-            eng.export_counters(mine.data_ptr())
-            dist.all_gather_into_tensor(counters, mine)
+            dist.all_gather_into_tensor(counters, eng.counters(mine))
         return st
 
     for _ in range(args.warmup):
@@ -308,43 +451,17 @@ def main():
     # whole decode step vs its roofline; attention bytes per step from the accounted window
     step_rl = step_roofline(shape, tokens / max(1, dec_steps), attn_bytes / max(1, sp1["steps"] - sp0["steps"]),
                             ms_max / max(1, dec_steps), peaks)
+    eng.close()
 
     # ---------------- e2e: the public C-ABI path with host buffers, H2D/D2H inside the timed region
-    e2e = None
-    if not args.no_e2e:
-        extra = make_requests(rank, world, n_backlog + 1000, cfg["concurrent"], shape, cfg)
-        h2d = sum(request_bytes(r) for r in extra)
-        d2h = 0
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e_tok0 = eng.step(0)["branch_tokens"]
-        for r in extra:
-            eng.admit(r)
-        for _ in range(args.steps):
-            eng.step(1)
-            res = eng.collect()
-            d2h += sum(192 + 4 * len(x["tokens"]) for x in res)
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        e_tok = eng.step(0)["branch_tokens"] - e_tok0
-        e2e_v = torch.tensor([el, float(e_tok)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            mx = e2e_v.clone()
-            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-            dist.all_reduce(e2e_v, op=dist.ReduceOp.SUM)
-            e2e_v[0] = mx[0]
-        e2e = {"value": float(e2e_v[1]) / float(e2e_v[0]), "unit": "branch-tokens/s",
-               "windows": args.steps,
-               "h2d_bytes_per_step": h2d // max(1, args.steps), "d2h_bytes_per_step": d2h // max(1, args.steps),
-               "includes": "admit (host prompts/scripts), prefill, decode windows, collect (D2H records+tokens)"}
-    # C2: gather of result records to rank 0 (counts only here)
+    e2e = None if args.no_e2e else e2e_leg(shape, cfg, rank, world, local, stream, args.attn_mode)
     if world > 1:
         dist.barrier()
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
-            r = oracle_sample(2, 1, cfg["T"])
-            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            r = cpu_baseline_legs(args.cpu_steps, 2)
+            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "legs")}
         except Exception as e:  # never let the baseline kill the bench line
             cpu = {"value": None, "unit": "branch-tokens/s", "cores": len(os.sched_getaffinity(0)),
                    "kind": "oracle", "sample": f"failed: {e!r}"}
@@ -363,7 +480,6 @@ def main():
                 "branch_tokens_timed": tok_all, "gpu_launches": launches, "clocks": clocks,
                 "roofline": roofline, "step_roofline": step_rl, "cpu_baseline": cpu, "e2e": e2e}
         print(json.dumps(line), flush=True)
-    eng.close()
     if world > 1:
         dist.destroy_process_group()
 

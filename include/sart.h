@@ -185,8 +185,11 @@ int sart_step(sart_ctx* ctx, int32_t max_windows, sart_stats* out);
 
 /* Write the 16-int32 admission-counter record (live_rows, queued_branches,
  * queued_requests, free_blocks, committed_blocks, finalized_total, windows,
- * steps, branch_tokens lo/hi, 0...) into DEVICE memory dev_int32x16 on the ctx
- * stream, for the multi-GPU all-gather (torch.distributed). */
+ * steps, branch_tokens lo/hi, 0...) into DEVICE memory dev_int32x16 (16 int32 on
+ * this ctx's device, caller-owned), for the multi-GPU all-gather of SURVEY §8(e)
+ * (torch.distributed).  The copy is issued on the ctx stream and completed before
+ * the call returns, so a collective on any stream may read the record.
+ * Errors: EINVAL (null), ESTATE (poisoned ctx), ECUDA. */
 int sart_export_counters(sart_ctx* ctx, void* dev_int32x16);
 
 /* One finalized request (O9 / P:279). */
@@ -295,6 +298,10 @@ typedef struct {
   double prm_ms;           /* GPU time of the f2 PRM passes (CUDA events)         */
   int64_t prm_tokens;      /* suffix entries the PRM model read in those passes   */
   int64_t prm_passes;      /* boundaries with a PRM pass                          */
+  int64_t h2d_bytes;       /* host->device bytes the serving path copied (prompts, scripts,
+                              admission events, prefill token lists, counter exports) */
+  int64_t d2h_bytes;       /* device->host bytes it copied (per-window counter records, live
+                              polls, finalized records, selected branches' tokens)  */
 } sart_profile;
 int sart_get_profile(sart_ctx* ctx, sart_profile* out);
 /* Turn per-launch attention timing on or off.  While on, decode steps are launched eagerly

@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -23,15 +24,33 @@ OBJDIR = os.path.join(HERE, "build") if "SART_LIB_OUT" not in os.environ else LI
 STAMP = os.path.join(OBJDIR, "flags.txt")
 
 
+def fingerprint() -> str:
+    """SHA-256 over the nvcc command line and the CONTENT of every source / header (not their
+    mtimes: a checkout or a copied tree with uniform mtimes must not reuse a stale library)."""
+    h = hashlib.sha256()
+    h.update(" ".join([NVCC] + FLAGS).encode())
+    deps = sorted(sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) +
+                  [os.path.join(HERE, "..", "include", "sart.h")])
+    for d in deps:
+        h.update(os.path.basename(d).encode())
+        with open(d, "rb") as f:
+            h.update(hashlib.sha256(f.read()).digest())
+    return h.hexdigest()
+
+
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+    """The library exists and was built from exactly these sources and flags, and its own
+    bytes are the ones that build wrote (stamp = source fingerprint + library hash)."""
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return False
-    if not os.path.exists(STAMP) or open(STAMP).read() != " ".join(FLAGS):
+    try:
+        fp, lib_hash = open(STAMP).read().split()
+    except ValueError:
         return False
-    t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
-        [os.path.join(HERE, "..", "include", "sart.h")]
-    return all(os.path.getmtime(d) <= t for d in deps)
+    if fp != fingerprint():
+        return False
+    with open(LIB, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest() == lib_hash
 
 
 def build(force: bool = False, verbose: bool = True, jobs: int = 8) -> str:
@@ -63,8 +82,10 @@ def build(force: bool = False, verbose: bool = True, jobs: int = 8) -> str:
            "-o", tmp, "-lcuda"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
+    with open(LIB, "rb") as f:
+        lib_hash = hashlib.sha256(f.read()).hexdigest()
     with open(STAMP, "w") as f:
-        f.write(" ".join(FLAGS))
+        f.write(fingerprint() + " " + lib_hash)
     return LIB
 
 

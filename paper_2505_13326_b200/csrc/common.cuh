@@ -133,6 +133,37 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 #ifdef __CUDACC__
+#include <mutex>
+#include <set>
+#include <utility>
+// SM count of the CURRENT device (engines on different devices in one process each see their
+// own), cached per ordinal
+inline int device_sms() {
+  static int cache[64] = {};
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d < 0 || d >= 64) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    return v;
+  }
+  if (!cache[d]) cudaDeviceGetAttribute(&cache[d], cudaDevAttrMultiProcessorCount, d);
+  return cache[d];
+}
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting of a kernel: set it once
+// per (kernel, device, size)
+template <typename Kern>
+inline void ensure_dyn_smem(Kern kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<std::pair<const void*, int>, int>> done;
+  int d = 0;
+  cudaGetDevice(&d);
+  const auto key = std::make_pair(std::make_pair((const void*)kernel, d), bytes);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(key)) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done.insert(key);
+}
 // launch with the PDL attribute (also captured into CUDA graphs as programmatic edges)
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -640,7 +640,10 @@ __global__ void __launch_bounds__(1024) k_attn_items(Dims D, Rows rows, Reqs req
 // changes at boundaries; tasks whose rows finished mid-window are skipped at run time.
 __global__ void __launch_bounds__(1024) k_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat) {
   const int tid = threadIdx.x;
-  __shared__ int s_rank[1024], s_nrows[1024];
+  // per-row rank inside its request and the request's row count: global scratch sized R, so
+  // any max_rows works (a fixed shared array would overflow above 1024 rows)
+  int* s_rank = pl.row_rank;
+  int* s_nrows = pl.row_nreq;
   const int qr = flat ? 1 : pl.qr_max;
   for (int r = tid; r < n; r += 1024) {
     const int slot = rows.slot[r];
@@ -650,6 +653,7 @@ __global__ void __launch_bounds__(1024) k_attn_plan(Dims D, Rows rows, Reqs reqs
     s_rank[r] = rank;
     s_nrows[r] = tot;
   }
+  __threadfence_block();
   __syncthreads();
   if (tid == 0) {
     int ng = 0, nu = 0;
@@ -737,11 +741,7 @@ template <int HD, bool SUF, int NST>
 static void launch_pf_n(dim3 grid, int threads, const bf16* q, const bf16* pool, bf16* out, Dims D, int layer,
                         Reqs reqs, const int4* blocks, Rows rows, int QT, int HG, cudaStream_t s) {
   const size_t sm = 2 * NST * 64 * (size_t)HD * sizeof(bf16) + 8 * NST;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_attn_prefill_tc<HD, SUF, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
+  ensure_dyn_smem(k_attn_prefill_tc<HD, SUF, NST>, (int)sm);
   k_attn_prefill_tc<HD, SUF, NST><<<grid, threads, sm, s>>>(q, pool, out, D, layer, reqs, blocks, rows, QT, HG);
 }
 // ring depth: 2 stages while two CTAs share an SM (<= 4 warps); 4 stages for the larger
@@ -780,17 +780,12 @@ void launch_attn_account(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, doubl
   launch_pdl(k_attn_account, dim3(1), dim3(1024), 0, s, D, rows, reqs, n, acc);
 }
 
-static int g_sms = 0;
 template <int HD, int NW, int NS, int SW>
 static void launch_cfg(const bf16* q, const bf16* pool, float* part_o, float* part_lse, bf16* out, float* dbg, Dims D,
                        int layer, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s) {
   const size_t sm = sizeof(WarpSmem<HD, NS, SW>) * NW;
-  static bool a = false;
-  if (!a) {
-    cudaFuncSetAttribute(k_attn_cascade<HD, NW, NS, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    a = true;
-  }
-  launch_pdl(k_attn_cascade<HD, NW, NS, SW>, dim3(g_sms), dim3(NW * 32), sm, s, q, pool, part_o, part_lse, out, dbg,
+  ensure_dyn_smem(k_attn_cascade<HD, NW, NS, SW>, (int)sm);
+  launch_pdl(k_attn_cascade<HD, NW, NS, SW>, dim3(device_sms()), dim3(NW * 32), sm, s, q, pool, part_o, part_lse, out, dbg,
              D, layer, rows, reqs, pl);
 }
 static int attn_cfg() {
@@ -801,6 +796,7 @@ static int attn_cfg() {
   }
   return c;
 }
+bool g_attn_skip_merge = false;
 template <int HD>
 static void launch_hd(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse, Dims D,
                       int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s) {
@@ -810,13 +806,13 @@ static void launch_hd(const bf16* q, const bf16* pool, bf16* out, float* dbg, fl
     case 3: launch_cfg<HD, 7, 3, 16>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
     default: launch_cfg<HD, 8, 3, 16>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
   }
+  if (g_attn_skip_merge) return;
   launch_pdl(k_attn_merge<HD>, dim3((n * D.qh * 32 + 255) / 256), dim3(256), 0, s, part_o, part_lse, out, dbg, D,
              rows, reqs, pl, n);
 }
 void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse,
                          Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s) {
   if (n <= 0) return;
-  if (!g_sms) cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0);
   if (D.hd == 128) launch_hd<128>(q, pool, out, dbg, part_o, part_lse, D, layer, rows, reqs, pl, n, s);
   else launch_hd<64>(q, pool, out, dbg, part_o, part_lse, D, layer, rows, reqs, pl, n, s);
 }

@@ -573,7 +573,6 @@ struct MapCache {
   }
 };
 MapCache g_maps;
-int g_num_sms = 0;
 
 template <int BN, int MODE, int MS = 1>
 bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K, int S,
@@ -582,12 +581,8 @@ bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* 
   const CUtensorMap* mb = Bt ? ma : g_maps.get(B, N, K, BN);
   if (!ma || !mb) return false;
   const size_t smem = sizeof(Smem<BN, MS>) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tc<BN, MODE, MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
+  ensure_dyn_smem(k_gemm_tc<BN, MODE, MS>, (int)smem);
+  const int g_num_sms = device_sms();
   const int ntiles = ((M + MS * BM - 1) / (MS * BM)) * ((N + BN - 1) / BN) * S;
   const int grid = ntiles < g_num_sms ? ntiles : g_num_sms;
   QkvEpi e{};
@@ -601,7 +596,7 @@ bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, b
                     int mode, cudaStream_t s, const bf16* Bt) {
   // 256-row tiles (two MMA tiles per weight stage) once they still fill ~3/4 of the SMs:
   // measured 7% faster on the C2 gate/up projection (profiles/r1_gemm_bm256_sweep.txt)
-  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
+  const int g_num_sms = device_sms();
   const int ms = (mode == GEMM_SWIGLU && M > BM && ((M + 2 * BM - 1) / (2 * BM)) * ((N + 255) / 256) >= g_num_sms * 3 / 4)
                      ? 2 : 1;
   return launch_gemm_tc_split(A, B, bias, C, act, M, N, K, mode, 1, 256, ms, s, Bt);
@@ -639,7 +634,7 @@ bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float
 // ties go to fewer splits (less partial traffic).  E.g. t = 32 tiles: S = 4 (128 units, one
 // wave) instead of 5 (160 units = two waves, the second 12 units long).
 static int wave_split(int t, int smax) {
-  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
+  const int g_num_sms = device_sms();
   int best = 1;
   double bc = 1e30;
   for (int S = 1; S <= smax; ++S) {
@@ -655,7 +650,7 @@ bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const Qk
   if (K % 8) return false;
   // split-K so that (m-tiles x heads x splits) covers the SMs; the last split of each tile
   // runs the fused bias + RoPE + KV-append epilogue
-  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
+  const int g_num_sms = device_sms();
   const int mt = (M + BM - 1) / BM, heads = N / epi.D.hd, kb = (K + BK - 1) / BK;
   int S = 1;
   if (epi.parts && epi.cnt && heads * mt * 8 <= epi.cnt_cap && epi.D.hd >= 128) {
@@ -676,7 +671,7 @@ void choose_split(int M, int N, int K, int& S, int& BN, int& MSUB) {
   MSUB = 1;
   // measured on B200 at M = 512 (tools/gemm_sweep.py): long-K projections prefer 256-wide
   // tiles with more splits, short-K ones 128-wide tiles; aim for ~one unit per SM
-  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
+  const int g_num_sms = device_sms();
   const int mt = (M + BM - 1) / BM;
   const int kb = (K + BK - 1) / BK;
   const int t256 = mt * ((N + 255) / 256);

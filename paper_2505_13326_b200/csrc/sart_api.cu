@@ -75,6 +75,7 @@ struct sart_ctx {
   bool poisoned = false;
   bool gemm_failed = false;
   int W = 0;   // workspace rows
+  int ablate = 0;   // SART_ABLATE bit mask (measurement only: skip decode-step kernels, results invalid)
   int PC = 0;  // prefill chunk
 
   // device memory
@@ -136,6 +137,7 @@ struct sart_ctx {
   int ev_used = 0;
   double attn_ms = 0, attn_bytes = 0, attn_bytes_base = 0, prefill_ms = 0;
   long long attn_launches = 0, launches = 0;
+  long long h2d_bytes = 0, d2h_bytes = 0;   // host<->device bytes of the serving path (sart_profile)
 
   // row f2: the separate PRM decoder is a sub-context holding its own dims, weights, KV pool
   // and workspaces; it shares rows / reqs / stream with the policy ctx.
@@ -212,6 +214,14 @@ bool is_norm_tensor(const Dims& D, int idx) {
       return;                                                                              \
     }                                                                                      \
   } while (0)
+
+// Every host<->device copy of the serving path goes through here so that sart_get_profile can
+// report the bytes actually moved (bench.py's e2e h2d / d2h per step).
+cudaError_t xfer(sart_ctx* ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind k, cudaStream_t s) {
+  if (k == cudaMemcpyHostToDevice) ctx->h2d_bytes += (long long)bytes;
+  else if (k == cudaMemcpyDeviceToHost) ctx->d2h_bytes += (long long)bytes;
+  return cudaMemcpyAsync(dst, src, bytes, k, s);
+}
 
 template <typename P>
 cudaError_t dalloc(sart_ctx* ctx, P** p, size_t bytes, bool zero = true) {
@@ -301,8 +311,7 @@ void qkv_rope(sart_ctx* ctx, int l, int n, RopeArgs ra) {
   // HBM rate, so it runs as a wave-split GEMM + the RoPE / append kernel instead
   bool fused = true;
   if constexpr (std::is_same<T, bf16>::value) {
-    static int nsm = 0;
-    if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->cfg.device);
+    const int nsm = device_sms();
     fused = !(D.d >= 4096 && (D.qkv / D.hd) * ((n + 127) / 128) < nsm * 3 / 4);
   }
   if (!fused) {
@@ -365,10 +374,16 @@ void layer_attention(sart_ctx* ctx, int l, int n) {
   if (e1) cudaEventRecord(e1, ctx->st);
 }
 
+// SART_ABLATE bits (measurement only, tools/ablate_c2.py): the in-graph marginal cost of a
+// kernel class is the step time with it minus without it.  Results are meaningless when set.
+enum { AB_RMSNORM = 1, AB_QKV = 2, AB_ATTN = 4, AB_MERGE = 8, AB_OPROJ = 16, AB_GATEUP = 32, AB_DOWN = 64,
+       AB_HEAD = 128, AB_SAMPLE = 256 };
+
 template <typename T>
 void decode_step(sart_ctx* ctx, int n) {
   const Dims& D = ctx->D;
   cudaStream_t s = ctx->st;
+  const int ab = ctx->ablate;
   launch_step_begin(ctx->ctr, s);
   launch_embed<T>(ctx->rows.tok, ctx->W_<T>(t_embed()), ctx->h, n, D.d, s);
   ctx->launches += 2;
@@ -380,24 +395,31 @@ void decode_step(sart_ctx* ctx, int n) {
     launch_attn_items(D, ctx->rows, ctx->reqs, ctx->plan, s);
     ctx->launches++;
   }
+  g_attn_skip_merge = (ab & AB_MERGE) != 0;
   int np_res = 0;   // pending residual partials (previous layer's down projection)
   for (int l = 0; l < D.L; ++l) {
-    launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, n, D.d,
-                      D.eps, s);
-    qkv_rope<T>(ctx, l, n, RopeArgs{nullptr, nullptr});
-    layer_attention<T>(ctx, l, n);
-    int np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), n, D.d, D.qh * D.hd);
-    launch_rmsnorm<T>(ctx->h, ctx->parts, np, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, n, D.d, D.eps,
-                      s);
-    mlp_up<T>(ctx, l, n);
-    np_res = proj<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), n, D.d, D.F);
+    if (!(ab & AB_RMSNORM))
+      launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, n, D.d,
+                        D.eps, s);
+    if (!(ab & AB_QKV)) qkv_rope<T>(ctx, l, n, RopeArgs{nullptr, nullptr});
+    if (!(ab & AB_ATTN)) layer_attention<T>(ctx, l, n);
+    int np = 0;
+    if (!(ab & AB_OPROJ)) np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), n, D.d, D.qh * D.hd);
+    if (!(ab & AB_RMSNORM))
+      launch_rmsnorm<T>(ctx->h, ctx->parts, np, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, n, D.d,
+                        D.eps, s);
+    if (!(ab & AB_GATEUP)) mlp_up<T>(ctx, l, n);
+    np_res = 0;
+    if (!(ab & AB_DOWN)) np_res = proj<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), n, D.d, D.F);
     ctx->launches += 1;
   }
   launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_final(D)), (T*)ctx->zT, ctx->z32, ctx->rows.status, n,
                     D.d, D.eps, s);
-  gemm<T>(ctx, (T*)ctx->zT, ctx->W_<T>(t_lm(D)), nullptr, ctx->logits, n, D.V, D.d, GEMM_STORE);
-  launch_sample(ctx->logits, D, ctx->rows, ctx->reqs, ctx->ctr, n, ctx->dbg_tok, ctx->skey, ctx->sv, s);
+  if (!(ab & AB_HEAD)) gemm<T>(ctx, (T*)ctx->zT, ctx->W_<T>(t_lm(D)), nullptr, ctx->logits, n, D.V, D.d, GEMM_STORE);
+  if (!(ab & AB_SAMPLE))
+    launch_sample(ctx->logits, D, ctx->rows, ctx->reqs, ctx->ctr, n, ctx->dbg_tok, ctx->skey, ctx->sv, s);
   ctx->launches += 2;
+  g_attn_skip_merge = false;
 }
 
 // Batched prefill (Alg. 1 L15): the prompts of every request admitted in this fill
@@ -427,7 +449,7 @@ void prefill_batch(sart_ctx* ctx, sart_ctx* src, int ntok) {
         i = j;
       }
       nqb = (int)qb.size();
-      cudaMemcpyAsync(src->d_pf_blocks, qb.data(), sizeof(int4) * qb.size(), cudaMemcpyHostToDevice, s);
+      xfer(src, src->d_pf_blocks, qb.data(), sizeof(int4) * qb.size(), cudaMemcpyHostToDevice, s);
     }
     launch_embed<T>(src->d_prompt + t0, ctx->W_<T>(t_embed()), ctx->h, c, D.d, s);
     ctx->launches++;
@@ -516,7 +538,7 @@ void prm_model_scores(sart_ctx* ctx, int n) {
   // that `ncu --profile-from-start off` captures exactly one PRM pass
   static const int ncu_pass = getenv("SART_NCU_PRM_PASS") ? atoi(getenv("SART_NCU_PRM_PASS")) : 0;
   const bool ncu_range = ncu_pass > 0 && ctx->prm_passes + 1 == ncu_pass;
-  CK_VOID(cudaMemcpyAsync(m->h_ell, ctx->rows.ell, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+  CK_VOID(xfer(ctx, m->h_ell, ctx->rows.ell, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
   CK_VOID(cudaStreamSynchronize(s));
   if (ncu_range) cudaProfilerStart();
   CK_VOID(cudaEventRecord(m->prm_ev[0], s));
@@ -534,7 +556,7 @@ void prm_model_scores(sart_ctx* ctx, int n) {
   std::copy(seg.begin(), seg.end(), m->h_prm_desc);
   std::copy(qb.begin(), qb.end(), m->h_prm_desc + seg.size());
   std::copy(gat.begin(), gat.end(), m->h_prm_desc + seg.size() + qb.size());
-  if (nd) CK_VOID(cudaMemcpyAsync(m->prm_desc, m->h_prm_desc, sizeof(int4) * nd, cudaMemcpyHostToDevice, s));
+  if (nd) CK_VOID(xfer(ctx, m->prm_desc, m->h_prm_desc, sizeof(int4) * nd, cudaMemcpyHostToDevice, s));
   const int4* dseg = m->prm_desc;
   const int4* dqb = m->prm_desc + seg.size();
   const int4* dgat = m->prm_desc + seg.size() + qb.size();
@@ -588,7 +610,7 @@ void prm_scores(sart_ctx* ctx, int n) {
 int flush_events(sart_ctx* ctx, std::vector<AdmitEvent>& ev, int& pop_off, int& new_rows, int& commit_delta) {
   if (ev.empty()) return SART_OK;
   if ((int)ev.size() > ctx->ev_cap) return set_err(SART_EINVAL, "too many admission events");
-  CK(cudaMemcpyAsync(ctx->d_events, ev.data(), sizeof(AdmitEvent) * ev.size(), cudaMemcpyHostToDevice, ctx->st));
+  CK(xfer(ctx, ctx->d_events, ev.data(), sizeof(AdmitEvent) * ev.size(), cudaMemcpyHostToDevice, ctx->st));
   launch_admit(ctx->d_events, (int)ev.size(), pop_off, new_rows, commit_delta, ctx->D, ctx->rows, ctx->reqs,
                ctx->free_stack, ctx->ctr, ctx->st);
   ctx->launches++;
@@ -605,22 +627,23 @@ int upload_request(sart_ctx* ctx, const HostReq& q, int slot) {
   cudaStream_t s = ctx->st;
   size_t sb = (size_t)slot * SART_MAXN;
   if (!q.sc.forced_len.empty()) {
-    CK(cudaMemcpyAsync(ctx->reqs.sc_len + sb, q.sc.forced_len.data(), sizeof(int) * q.N, cudaMemcpyHostToDevice, s));
+    CK(xfer(ctx, ctx->reqs.sc_len + sb, q.sc.forced_len.data(), sizeof(int) * q.N, cudaMemcpyHostToDevice, s));
   } else {
     std::vector<int> z(q.N, 0);
-    CK(cudaMemcpyAsync(ctx->reqs.sc_len + sb, z.data(), sizeof(int) * q.N, cudaMemcpyHostToDevice, s));
+    CK(xfer(ctx, ctx->reqs.sc_len + sb, z.data(), sizeof(int) * q.N, cudaMemcpyHostToDevice, s));
   }
   if (q.has_script) {
-    CK(cudaMemcpyAsync(ctx->reqs.sc_final + sb, q.sc.final_score.data(), sizeof(float) * q.N,
+    CK(xfer(ctx, ctx->reqs.sc_final + sb, q.sc.final_score.data(), sizeof(float) * q.N,
                        cudaMemcpyHostToDevice, s));
     int nb = std::min(q.sc.n_bnd, D.nbnd_max);
+    ctx->h2d_bytes += (long long)sizeof(float) * nb * q.N;
     CK(cudaMemcpy2DAsync(ctx->reqs.sc_scores + sb * D.nbnd_max, sizeof(float) * D.nbnd_max, q.sc.scores.data(),
                          sizeof(float) * q.sc.n_bnd, sizeof(float) * nb, q.N, cudaMemcpyHostToDevice, s));
   }
   if (!q.sc.answer.empty())
-    CK(cudaMemcpyAsync(ctx->reqs.sc_answer + sb, q.sc.answer.data(), sizeof(int) * q.N, cudaMemcpyHostToDevice, s));
+    CK(xfer(ctx, ctx->reqs.sc_answer + sb, q.sc.answer.data(), sizeof(int) * q.N, cudaMemcpyHostToDevice, s));
   if (!q.sc.forced_tokens.empty())
-    CK(cudaMemcpyAsync(ctx->reqs.forced + sb * D.cap, q.sc.forced_tokens.data(), sizeof(int) * (size_t)q.N * D.cap,
+    CK(xfer(ctx, ctx->reqs.forced + sb * D.cap, q.sc.forced_tokens.data(), sizeof(int) * (size_t)q.N * D.cap,
                        cudaMemcpyHostToDevice, s));
   return SART_OK;
 }
@@ -704,9 +727,9 @@ int fill(sart_ctx* ctx) {
   const int ntok = (int)ctx->pf_tok.size();
   if (ntok > 0) {
     if (ntok > ctx->pf_cap) return set_err(SART_EINVAL, "prefill batch exceeds its buffer");
-    CK(cudaMemcpyAsync(ctx->d_prompt, ctx->pf_tok.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaMemcpyAsync(ctx->d_pf_slot, ctx->pf_slot.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaMemcpyAsync(ctx->d_pf_pos, ctx->pf_pos.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
+    CK(xfer(ctx, ctx->d_prompt, ctx->pf_tok.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
+    CK(xfer(ctx, ctx->d_pf_slot, ctx->pf_slot.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
+    CK(xfer(ctx, ctx->d_pf_pos, ctx->pf_pos.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
     CK(cudaEventRecord(ctx->pf_ev[0], ctx->st));
     ctx->pf_slot_h.swap(ctx->pf_slot);
     ctx->pf_pos_h.swap(ctx->pf_pos);
@@ -732,7 +755,7 @@ int fill(sart_ctx* ctx) {
 // ------------------------------------------------------------------ boundary read-back
 int read_boundary(sart_ctx* ctx) {
   const Dims& D = ctx->D;
-  CK(cudaMemcpyAsync(ctx->h_ctr, ctx->ctr, sizeof(Ctr) + sizeof(int) * D.S, cudaMemcpyDeviceToHost, ctx->st));
+  CK(xfer(ctx, ctx->h_ctr, ctx->ctr, sizeof(Ctr) + sizeof(int) * D.S, cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   Ctr& c = *ctx->h_ctr;
   if (ctx->pf_pending) {   // GPU time of this window's batched prefill
@@ -755,7 +778,7 @@ int read_boundary(sart_ctx* ctx) {
             [&](int a, int b) { return ctx->slots[a].id < ctx->slots[b].id; });
   std::vector<DevResult> dr(nf);
   for (int i = 0; i < nf; ++i)
-    CK(cudaMemcpyAsync(&dr[i], ctx->res + fslots[i], sizeof(DevResult), cudaMemcpyDeviceToHost, ctx->st));
+    CK(xfer(ctx, &dr[i], ctx->res + fslots[i], sizeof(DevResult), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   const int64_t tnow = now_ns();
   for (int i = 0; i < nf; ++i) {
@@ -803,7 +826,7 @@ int read_boundary(sart_ctx* ctx) {
     r.tokens_len = d.branch_len[sel];
     hr.tokens.resize(r.tokens_len);
     if (r.tokens_len > 0)
-      CK(cudaMemcpyAsync(hr.tokens.data(), ctx->reqs.hist + ((size_t)slot * SART_MAXN + sel) * D.cap,
+      CK(xfer(ctx, hr.tokens.data(), ctx->reqs.hist + ((size_t)slot * SART_MAXN + sel) * D.cap,
                          sizeof(int) * r.tokens_len, cudaMemcpyDeviceToHost, ctx->st));
     ctx->results.push_back(std::move(hr));
     si.live = false;
@@ -823,7 +846,7 @@ int run_window(sart_ctx* ctx) {
   launch_window_begin(ctx->ctr, n, ctx->st);
   ctx->launches++;
   if (ctx->prm)   // entries decoded this window = ell(boundary) - ell(now), per row (f2 pass)
-    CK(cudaMemcpyAsync(ctx->prm->h_ell_ws, ctx->rows.ell, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->st));
+    CK(xfer(ctx, ctx->prm->h_ell_ws, ctx->rows.ell, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->st));
   if (ctx->bf16) {   // work units of the cascade attention for this window's batch
     launch_attn_plan(D, ctx->rows, ctx->reqs, ctx->plan, n, ctx->cfg.attn_mode == SART_ATTN_FLAT, ctx->st);
     ctx->launches++;
@@ -864,7 +887,7 @@ int run_window(sart_ctx* ctx) {
         CK(cudaEventSynchronize(ctx->poll_ev[polls & 1]));
         if (ctx->h_live[polls & 1] == 0) break;
       }
-      CK(cudaMemcpyAsync(&ctx->h_live[polls & 1], &ctx->ctr->live, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+      CK(xfer(ctx, &ctx->h_live[polls & 1], &ctx->ctr->live, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
       CK(cudaEventRecord(ctx->poll_ev[polls & 1], ctx->st));
       ++polls;
       if (polls >= 2 && cudaEventQuery(ctx->poll_ev[(polls - 2) & 1]) == cudaSuccess &&
@@ -1209,6 +1232,8 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     IC(dalloc(ctx, &pl.items, sizeof(int4) * 2 * max_units));
     IC(dalloc(ctx, &pl.n_items, sizeof(int)));
     IC(dalloc(ctx, &pl.row_pos, sizeof(int) * D.R));
+    IC(dalloc(ctx, &pl.row_rank, sizeof(int) * D.R));
+    IC(dalloc(ctx, &pl.row_nreq, sizeof(int) * D.R));
 
     IC(dalloc(ctx, &pl.grp_slot, sizeof(int) * D.R));
     IC(dalloc(ctx, &pl.grp_n, sizeof(int) * D.R));
@@ -1223,6 +1248,7 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   IC(cudaEventCreateWithFlags(&ctx->poll_ev[0], cudaEventDisableTiming));
   IC(cudaEventCreateWithFlags(&ctx->poll_ev[1], cudaEventDisableTiming));
   if (getenv("SART_NO_GRAPHS")) ctx->use_graphs = false;
+  if (const char* ev = getenv("SART_ABLATE")) ctx->ablate = atoi(ev);
   // ---- KV pool
   const size_t blk_bytes = (size_t)D.L * 2 * D.kvh * D.bs * D.hd * es;
   // f2: the PRM cache uses the same block ids, so one block costs both decoders' pages
@@ -1305,6 +1331,8 @@ int sart_admit(sart_ctx* ctx, const sart_request* r) {
     if (s->answer) q.sc.answer.assign(s->answer, s->answer + r->N);
     if (s->forced_tokens) {
       if (!ctx->cfg.enable_forced_tokens) return set_err(SART_EINVAL, "forced_tokens needs enable_forced_tokens");
+      for (size_t i = 0; i < (size_t)r->N * D.cap; ++i)   // they become embedding indices and history
+        if (s->forced_tokens[i] < 0 || s->forced_tokens[i] >= D.V) return set_err(SART_EINVAL, "forced token out of range");
       q.sc.forced_tokens.assign(s->forced_tokens, s->forced_tokens + (size_t)r->N * D.cap);
     }
   }
@@ -1354,7 +1382,8 @@ int sart_export_counters(sart_ctx* ctx, void* dev) {
   int32_t c[16] = {ctx->n_rows, (int32_t)ctx->branch_queue.size(), (int32_t)ctx->request_queue.size(),
                    (int32_t)ctx->free_top, (int32_t)ctx->committed, ctx->finalized_total, ctx->windows, ctx->steps,
                    (int32_t)(ctx->branch_tokens & 0xffffffff), (int32_t)(ctx->branch_tokens >> 32), 0, 0, 0, 0, 0, 0};
-  CK(cudaMemcpyAsync(dev, c, sizeof(c), cudaMemcpyHostToDevice, ctx->st));
+  CK(xfer(ctx, dev, c, sizeof(c), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));   // the record is in device memory on return (any stream may read it)
   return SART_OK;
 }
 
@@ -1619,6 +1648,8 @@ int sart_get_profile(sart_ctx* ctx, sart_profile* o) {
   o->prm_ms = ctx->prm_ms;
   o->prm_tokens = ctx->prm_tokens;
   o->prm_passes = ctx->prm_passes;
+  o->h2d_bytes = ctx->h2d_bytes;
+  o->d2h_bytes = ctx->d2h_bytes;
   return SART_OK;
 }
 int sart_set_profile(sart_ctx* ctx, int32_t enable) {
@@ -1638,6 +1669,7 @@ int sart_reset_profile(sart_ctx* ctx) {
   ctx->attn_ms = ctx->attn_bytes = ctx->prefill_ms = ctx->prm_ms = 0;
   ctx->prm_tokens = ctx->prm_passes = 0;
   ctx->attn_launches = ctx->launches = 0;
+  ctx->h2d_bytes = ctx->d2h_bytes = 0;
   return SART_OK;
 }
 

@@ -13,8 +13,9 @@ computed identically on every rank from the gathered counters, so no extra messa
 needed and per-rank replays stay deterministic.
 
 The engine is duck-typed: ``admit(req)``, ``step(n) -> stats dict``, ``collect() -> list``
-and ``counters() -> torch.int32[16]`` (the CUDA engine fills it with
-``sart_export_counters``).
+and ``counters(out) -> torch.int32[16]``: the CUDA engine (``sart.Engine``) fills the device
+tensor ``out`` with ``sart_export_counters``; a host stand-in may ignore ``out`` and return a
+CPU tensor (gloo).
 """
 from __future__ import annotations
 
@@ -76,6 +77,38 @@ def gather_results(results: List[Dict], group=None, dst: int = 0) -> List[Dict]:
     return sorted(merged, key=lambda r: r["request_id"])
 
 
+# C2 with fixed-size records: one int32 row per finalized request, gathered to rank 0 by the
+# backend's own collectives (NCCL over NVLink on GPUs) instead of pickled objects.
+RECORD_FIELDS = ("request_id", "answer_vote", "vote_count", "chosen_max_reward", "answer_max_reward",
+                 "num_completed", "num_pruned", "num_early_stopped", "num_discarded_queued", "finalize_reason",
+                 "phase_at_end", "window_final", "selected_branch", "tokens_len")
+
+
+def gather_result_records(results: List[Dict], device, group=None, dst: int = 0) -> torch.Tensor:
+    """C2: every rank's result records as int32 rows [len(RECORD_FIELDS)] (request_id must
+    fit int32) -> rank dst gets [total, F] ordered by rank then finalization order; other ranks
+    get an empty tensor.  Two all-gathers: the per-rank counts, then the rows padded to the
+    largest count."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    F = len(RECORD_FIELDS)
+    rows = [[int(r[k]) if k != "tokens_len" else int(r.get(k, len(r.get("tokens", ())))) for k in RECORD_FIELDS]
+            for r in results]
+    mine = (torch.tensor(rows, dtype=torch.int32) if rows else torch.zeros((0, F), dtype=torch.int32)).to(device)
+    cnt = torch.tensor([mine.shape[0]], dtype=torch.int32, device=device)
+    cnts = torch.zeros(world, dtype=torch.int32, device=device)
+    dist.all_gather_into_tensor(cnts, cnt, group=group)
+    mx = int(cnts.max().item())
+    pad = torch.zeros((max(mx, 1), F), dtype=torch.int32, device=device)
+    pad[: mine.shape[0]] = mine
+    allr = torch.zeros((world * max(mx, 1), F), dtype=torch.int32, device=device)
+    dist.all_gather_into_tensor(allr, pad, group=group)
+    if rank != dst:
+        return torch.zeros((0, F), dtype=torch.int32)
+    allr = allr.view(world, max(mx, 1), F).cpu()
+    return torch.cat([allr[r, : int(cnts[r])] for r in range(world)], 0)
+
+
 def serve(engine, arrivals: Sequence[Sequence], policy: str = "round_robin", group=None,
           max_windows: int = 1 << 30, on_window: Callable = None) -> List[Dict]:
     """Run a request stream to completion on this rank.
@@ -87,6 +120,10 @@ def serve(engine, arrivals: Sequence[Sequence], policy: str = "round_robin", gro
     """
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     ll = LeastLoaded(world)
+    backend = dist.get_backend(group)
+    # the C1 record lives where the backend's collectives read it: the rank's GPU for NCCL
+    cbuf = torch.zeros(16, dtype=torch.int32,
+                       device=f"cuda:{torch.cuda.current_device()}" if backend == "nccl" else "cpu")
     counters = None
     k = 0
     results: List[Dict] = []
@@ -105,7 +142,7 @@ def serve(engine, arrivals: Sequence[Sequence], policy: str = "round_robin", gro
                 engine.admit(req)
         st = engine.step(1)
         results += engine.collect()
-        counters = all_gather_counters(engine.counters(), group)
+        counters = all_gather_counters(engine.counters(cbuf), group)
         ll.gathered()
         if on_window:
             on_window(w, st, counters)

@@ -96,7 +96,8 @@ class SartState(C.Structure):
 class SartProfile(C.Structure):
     _fields_ = [("attn_ms", C.c_double), ("attn_launches", C.c_int64), ("attn_bytes", C.c_double),
                 ("kernel_launches", C.c_int64), ("prefill_ms", C.c_double), ("prm_ms", C.c_double),
-                ("prm_tokens", C.c_int64), ("prm_passes", C.c_int64)]
+                ("prm_tokens", C.c_int64), ("prm_passes", C.c_int64), ("h2d_bytes", C.c_int64),
+                ("d2h_bytes", C.c_int64)]
 
 
 _lib = None
@@ -294,6 +295,13 @@ class Engine:
 
     def export_counters(self, dev_ptr: int) -> None:
         _check(self.lib.sart_export_counters(self.ctx, C.c_void_p(dev_ptr)))
+
+    def counters(self, out):
+        """The C1 admission-counter record (sart_export_counters) written into ``out`` -- any
+        object exposing ``data_ptr()`` for 16 int32 of device memory on this engine's GPU (a
+        ``torch.int32[16]`` for the NCCL all-gather) -- which is returned."""
+        self.export_counters(out.data_ptr())
+        return out
 
     # ---------------------------------------------------------------- sart_collect
     def collect(self, cap: int = 4096, tokens_cap: int = 1 << 24) -> List[dict]:

@@ -32,7 +32,7 @@ class OracleRankEngine:
     def collect(self):
         return self.e.collect()
 
-    def counters(self):
+    def counters(self, out=None):
         s = self.e.stats()
         c = [s["live_rows"], s["queued_branches"], s["queued_requests"], s["free_blocks"], s["committed_blocks"],
              s["finalized_total"], s["windows"], s["steps"]] + [0] * 8
@@ -61,8 +61,9 @@ def _worker(rank, world, port, policy, q):
     owners = []
     res = sdist.serve(eng, workload(), policy=policy)
     allres = sdist.gather_results(res)
+    recs = sdist.gather_result_records(res, "cpu")     # C2 as fixed-size tensor rows
     mine = sorted(r["request_id"] for r in res)
-    q.put((rank, mine, [{k: r[k] for k in KEYS} for r in allres]))
+    q.put((rank, mine, [{k: r[k] for k in KEYS} for r in allres], recs.tolist()))
     dist.destroy_process_group()
 
 
@@ -76,8 +77,8 @@ def test_two_rank_partition_equals_single_process(policy):
         p.start()
     out = {}
     for _ in range(2):
-        rank, mine, allres = q.get(timeout=120)
-        out[rank] = (mine, allres)
+        rank, mine, allres, recs = q.get(timeout=120)
+        out[rank] = (mine, allres, recs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -100,6 +101,16 @@ def test_two_rank_partition_equals_single_process(policy):
         for k in KEYS:
             assert g[k] == o[k], (k, g["request_id"])
     assert out[1][1] == []
+    # the tensor gather carries the same records (rank 0's rows first, then rank 1's)
+    from paper_2505_13326_b200.dist import RECORD_FIELDS
+    recs = out[0][2]
+    assert sorted(r[0] for r in recs) == list(range(10)) and out[1][2] == []
+    byid = {r["request_id"]: r for r in got}
+    for row in recs:
+        g = byid[row[0]]
+        for k, v in zip(RECORD_FIELDS, row):
+            if k in g:
+                assert g[k] == v, (k, row[0])
 
 
 def test_least_loaded_is_deterministic():

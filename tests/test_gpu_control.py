@@ -137,3 +137,15 @@ def test_policy_presets_match_oracle(policy):
         assert all(r["num_completed"] == 8 and r["num_early_stopped"] == 0 for r in res)
     if policy == "sart_noprune":
         assert all(r["num_pruned"] == 0 and r["num_completed"] >= 2 for r in res)
+
+
+def test_more_than_1024_rows():
+    """B = 1500 rows resident at once (47 requests x N = 32): the window plan (k_attn_plan) keeps
+    its per-row scratch in global memory, so batches above 1024 rows are exact too (ADVICE r1:
+    a fixed __shared__ int[1024] used to overflow); control bit-exact with the oracle."""
+    shape = SHAPES["tiny"]
+    cap, T, bs = 32, 16, 16
+    reqs = gen_requests(47, shape, 32, 16, 0.5, 16, cap, T, eos_id=1, p_range=(2, 60), length="uniform",
+                        len_range=(1, cap), root_seed=31)
+    res = run_pair(shape, reqs, bs, nb=4096, T=T, cap=cap, B=1500, check_every=1)
+    assert len(res) == 47

@@ -43,14 +43,31 @@ def oracle_teacher_forced(model, prompt, forced, steps, layers, prefix=None):
     return out
 
 
-def run_teacher_forced(shape, dtype, prompts, N, steps, bs, tol, std=0.08, seed=0, layers=None, attn_mode=0):
+def run_teacher_forced(shape, dtype, prompts, N, steps, bs, tol, std=0.08, seed=0, layers=None, attn_mode=0, T=1,
+                       attn_ch=None, num_blocks=4096):
+    """Teacher-forced PP1 run.  T > 1: windows of T steps, compared at each window's last step
+    (every row advances exactly T steps per window: forced tokens exclude EOS).  attn_ch: the
+    cascade attention's chunk length (SART_ATTN_CH, read at sart_init), to put many suffix
+    chunks (slots npc_max + c) on the path."""
+    import os
     layers = layers if layers is not None else sorted({0, shape.n_layers // 2, shape.n_layers - 1})
     weights = gen_weights(shape, dtype, std=std, root_seed=seed)
     model = Model(shape, weights)
     rng = np.random.default_rng(seed)
-    g = gpu_engine(shape, dtype, weights, block_size=bs, num_blocks=4096, max_rows=64, max_requests=16,
-                   max_prompt=max(len(p) for p in prompts) + 1, T=1, cap=steps, eos_id=EOS, temperature=1.0,
-                   enable_forced_tokens=True, debug_capture=True, attn_mode=attn_mode)
+    assert steps % T == 0
+    old_ch = os.environ.get("SART_ATTN_CH")
+    if attn_ch is not None:
+        os.environ["SART_ATTN_CH"] = str(attn_ch)
+    try:
+        g = gpu_engine(shape, dtype, weights, block_size=bs, num_blocks=num_blocks, max_rows=64, max_requests=16,
+                       max_prompt=max(len(p) for p in prompts) + 1, T=T, cap=steps, eos_id=EOS, temperature=1.0,
+                       enable_forced_tokens=True, debug_capture=True, attn_mode=attn_mode)
+    finally:
+        if attn_ch is not None:
+            if old_ch is None:
+                os.environ.pop("SART_ATTN_CH", None)
+            else:
+                os.environ["SART_ATTN_CH"] = old_ch
     forced = {}
     for rid, prompt in enumerate(prompts):
         ft = forced_tokens(rng, N, steps, shape.vocab)
@@ -61,7 +78,7 @@ def run_teacher_forced(shape, dtype, prompts, N, steps, bs, tol, std=0.08, seed=
            for rid in range(len(prompts)) for b in range(N)}
     worst = dict(logits=0.0, prm=0.0, attn=0.0)
     step_of = {}
-    for w in range(steps):
+    for w in range(steps // T):
         g.step(1)
         ids = g.debug_fetch(DBG_ROWIDS)
         lg = g.debug_fetch(DBG_LOGITS)
@@ -69,7 +86,7 @@ def run_teacher_forced(shape, dtype, prompts, N, steps, bs, tol, std=0.08, seed=
         at = {l: g.debug_fetch(DBG_ATTN, l) for l in layers}
         for i, key in enumerate(ids):
             rid, b = int(key) >> 8, int(key) & 0xFF
-            s = step_of.get((rid, b), 0) + 1
+            s = step_of.get((rid, b), 0) + T
             step_of[(rid, b)] = s
             r = ref[(rid, b)][s - 1]
             e = rel_err_rows(lg[i], r["logits"])[0]
@@ -213,3 +230,84 @@ def test_long_prefix_many_branches(attn_mode):
     prompts = [gen_prompt(13, shape.vocab, EOS, 1300, 1300)]
     w = run_teacher_forced(shape, "bf16", prompts, N=16, steps=4, bs=64, tol=2e-2, std=0.02, attn_mode=attn_mode)
     print("long prefix worst", attn_mode, w)
+
+
+def test_multi_chunk_suffix_small_ch64():
+    """Cascade attention with many suffix chunks: CH = 64 and 320 teacher-forced steps, so a
+    branch's suffix spans up to 5 chunks (attention slots npc_max + 0..4) next to a prefix of
+    2 chunks -- the slot mapping, per-chunk partials and the fixed-order LSE merge that carry
+    most of C2's attention bytes (l up to 4096 over CH = 512)."""
+    shape = SHAPES["small"]
+    prompts = [gen_prompt(21, shape.vocab, EOS, 100, 100), gen_prompt(22, shape.vocab, EOS, 33, 33)]
+    w = run_teacher_forced(shape, "bf16", prompts, N=4, steps=320, bs=16, tol=2e-2, std=0.02, T=8, attn_ch=64)
+    print("small CH=64 320 steps worst", w)
+
+
+def test_multi_chunk_suffix_1p5b_geometry_ch64():
+    """The C2 attention geometry (1.5B: GQA 12/2, hd 128, full vocab, 64-token blocks) with
+    suffixes over 3+ chunks (CH = 64, 208 steps) and a prefix of several chunks."""
+    shape = SHAPES["1.5B"].with_layers(2)
+    prompts = [gen_prompt(23, shape.vocab, EOS, 300, 300)]
+    w = run_teacher_forced(shape, "bf16", prompts, N=3, steps=208, bs=64, tol=2e-2, std=0.02, T=16, attn_ch=64)
+    print("1.5B-L2 CH=64 208 steps worst", w)
+
+
+def test_multi_chunk_suffix_production_ch():
+    """The production chunk length (CH = 512) with l >= 3 CH: tiny decoder teacher-forced
+    for 1600 steps (suffix chunks 0..3), compared at every 16-step window end."""
+    shape = SHAPES["tiny"]
+    prompts = [gen_prompt(24, shape.vocab, EOS, 40, 40)]
+    w = run_teacher_forced(shape, "bf16", prompts, N=2, steps=1600, bs=64, tol=2e-2, std=0.02, T=16)
+    print("tiny CH=512 1600 steps worst", w)
+
+
+@pytest.mark.parametrize("tau", [1.0, 0.6])
+def test_sampler_full_vocab_1p5b(tau):
+    """PP3 at the full C2 vocabulary (V = 151,936: 10 sampler chunks of 16,384 entries, the
+    pilot-bound pruning across loop iterations, the 10-way final reduction): the oracle
+    sampler applied to the GPU's own fp32 logits must give the GPU's token at >= 500
+    row-steps, except near-ties (top-2 perturbed-key gap < 1e-6 relative, PP3).  Half of the
+    requests carry a script (EOS masked except at the forced step)."""
+    from synth import gen_script
+    shape = SHAPES["1.5B"].with_layers(2)
+    weights = gen_weights(shape, "bf16", std=0.02, root_seed=5)
+    seed = 0x5EED_0000_1234
+    steps = 16
+    g = gpu_engine(shape, "bf16", weights, block_size=64, num_blocks=2048, max_rows=64, max_requests=8,
+                   max_prompt=128, T=1, cap=steps + 4, eos_id=EOS, temperature=tau, sampler_seed=seed,
+                   debug_capture=True)
+    forced_len = {}
+    for rid in range(4):
+        sc = None
+        if rid % 2:
+            sc = gen_script(rid, 8, steps + 4, 1, "uniform", (2, steps + 4))
+            forced_len[rid] = sc.forced_len
+        g.admit(Request(rid, gen_prompt(rid, shape.vocab, EOS, 20, 100), 8, 8, -1.0, 0, sc),
+                use_script_scores=False)
+    n_cmp = n_tie = n_eos = 0
+    step_of = {}
+    for w in range(steps):
+        g.step(1)
+        ids = g.debug_fetch(DBG_ROWIDS)
+        if len(ids) == 0:
+            break
+        lg = g.debug_fetch(DBG_LOGITS)
+        tk = g.debug_fetch(DBG_TOKENS)
+        for i, key in enumerate(ids):
+            rid, b = int(key) >> 8, int(key) & 0xFF
+            s = step_of.get((rid, b), 0) + 1
+            step_of[(rid, b)] = s
+            fl = int(forced_len[rid][b]) if rid in forced_len else 0
+            y = philox.sample(lg[i], s, rid, b, seed, tau, eos_id=EOS, forced_len=fl)
+            n_cmp += 1
+            n_eos += int(y == EOS)
+            if y != tk[i]:
+                keys = lg[i].astype(np.float64) / tau + philox.gumbel_noise(shape.vocab, s, rid, b, seed)
+                if fl:
+                    keys[EOS] = -np.inf
+                top = np.sort(keys)[-2:]
+                assert (top[1] - top[0]) <= 1e-6 * abs(top[1]), (rid, b, s, y, int(tk[i]))
+                n_tie += 1
+    g.close()
+    print(f"PP3 full vocab tau={tau}: {n_cmp} row-steps, {n_tie} near-ties, {n_eos} scripted EOS")
+    assert n_cmp >= 500 and n_tie <= 2 and n_eos >= 4
