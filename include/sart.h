@@ -115,6 +115,22 @@ typedef struct {
   int32_t prm_n_layers, prm_d_model, prm_n_heads, prm_n_kv_heads, prm_head_dim, prm_d_ff;
   uint64_t prm_weight_seed;
   const void* prm_host_weights;
+  /* SURVEY §8(b) additions.
+   * kv_pool / kv_pool_bytes: optional caller-owned DEVICE buffer (e.g. torch-allocated on
+   *   `device`) that holds the policy's paged KV pool [L][NB][2][kvh][bs][hd]; the caller keeps
+   *   it alive until sart_destroy, the ctx never frees it and zeroes it at init.  NB =
+   *   num_blocks if > 0 (must fit: else ENOMEM), otherwise kv_pool_bytes / block bytes.  NULL:
+   *   the ctx allocates the pool.  (The f2 PRM model's pool is always ctx-allocated.)
+   * es_every_step: 0 = paper semantics (early stop is decided at T boundaries, P:300-305,
+   *   reading R8); 1 = variant: once a request has M completed branches, its other running
+   *   branches stop decoding at that step (reading R43); they are EarlyStopped at the boundary.
+   * record_trace: 1 = record, at every boundary, each window row's generated tokens and the
+   *   score the boundary used, plus a 64-bit FNV-1a hash of the control state after the
+   *   boundary (sart_trace_fetch) -- the streams the oracle replays bit-exactly (PP2). */
+  void* kv_pool;
+  size_t kv_pool_bytes;
+  int32_t es_every_step;
+  int32_t record_trace;
 } sart_config;
 
 /* Create an engine.  Errors: EINVAL (shape/range), ENOMEM (allocation failure, or
@@ -215,6 +231,35 @@ typedef struct {
  * written and the rest is kept for the next call. */
 int sart_collect(sart_ctx* ctx, sart_result* out, int32_t cap, int32_t* n_out,
                  int32_t* tokens_out, int64_t tokens_cap);
+
+/*
+ * PP2 trace (record_trace = 1).  One record per row of every window's batch, in window order
+ * then batch-row order:
+ *   window      boundary index (0-based)
+ *   ell_start   tokens the branch had generated before the window
+ *   n_tokens    tokens it generated in the window; they are tokens_out[tokens_offset ..)
+ *   running     1: still running at the boundary (score = its k-th running score, k counting
+ *               the boundaries it was running at); 0: completed in the window (score = final)
+ *   score       the reward the boundary used (PRM head / PRM model / script), fp32
+ * hashes[w]: FNV-1a 64 of the control state after boundary w, over the little-endian bytes of
+ *   for each row in batch order: int64 request_id, int32 branch, int32 ell, int32 nblk,
+ *                                 int32 table[0..nblk)
+ *   int32 n_free, int32 free_stack[0..n_free) (bottom -> top), int64 committed,
+ *   int32 n_live, then per live request in ascending id: int64 id, int32 phase, uint32
+ *   threshold bits, int32 max_num_pruned, int32 num_completed, int32 num_pruned, int32 npre,
+ *   int32 prefix[0..npre).
+ * sart_trace_fetch moves everything recorded so far into the caller's HOST buffers and clears
+ * it.  *n_rows / *n_tokens / *n_hashes always receive the recorded counts; if any buffer is
+ * too small nothing is moved (EFULL).  EINVAL if record_trace is off or a pointer is null.
+ */
+typedef struct {
+  int64_t request_id;
+  int32_t branch, window, ell_start, n_tokens, running;
+  float score;
+  int64_t tokens_offset;
+} sart_trace_row;
+int sart_trace_fetch(sart_ctx* ctx, sart_trace_row* rows, int64_t rows_cap, int64_t* n_rows, int32_t* tokens_out,
+                     int64_t tokens_cap, int64_t* n_tokens, uint64_t* hashes, int64_t hashes_cap, int64_t* n_hashes);
 
 int sart_destroy(sart_ctx* ctx);
 const char* sart_strerror(int code);

@@ -79,6 +79,10 @@ class EngineConfig:
     temperature: float = 1.0
     sampler_seed: int = 0
     select_mode: int = 0          # 0 = vote, 1 = max reward (which branch's tokens are returned)
+    # Reading R43 (variant of R8): once a request has M completed branches,
+    # its other running branches stop decoding at that step; they are EarlyStopped at the
+    # boundary (never pruned).  False = paper semantics: early stop only at T boundaries.
+    es_every_step: bool = False
 
 
 @dataclasses.dataclass
@@ -121,6 +125,7 @@ class Row:
     blocks: List[int] = dataclasses.field(default_factory=list)
     hist: List[int] = dataclasses.field(default_factory=list)
     terminal: int = RUNNING       # state decided at the boundary
+    stopped: bool = False         # R43: stopped mid-window by early stop (incomplete)
 
 
 # ------------------------------------------------------------------ sources
@@ -337,6 +342,10 @@ class Engine:
         cfg = self.cfg
         wstep = 0
         for wstep in range(1, cfg.T + 1):                                          # L22
+            if cfg.es_every_step and wstep > 1:
+                self._es_stop(wstep)
+                if not any(r.running for r in self.rows):                         # R31
+                    break
             run = [r for r in self.rows if r.running]
             ys = self.src.step(run, wstep)
             for r, y in zip(run, ys):
@@ -355,6 +364,17 @@ class Engine:
                 break
         return wstep
 
+    def _es_stop(self, wstep: int) -> None:
+        """R43 (es_every_step): at the start of window step wstep > 1, a running row whose
+        request already has M completed branches (earlier boundaries + this window so far)
+        stops; it keeps its l steps and is EarlyStopped at the boundary.  At the boundary
+        itself Alg. 1's order applies (prune L32-37, then finalize L38-40)."""
+        done_now = collections.Counter(r.rs.rid for r in self.rows if not r.running and not r.stopped)
+        for r in self.rows:
+            if r.running and r.rs.num_completed + done_now[r.rs.rid] >= r.rs.M:
+                r.running, r.stopped = False, True
+                r.done_step, r.done_wstep = r.ell, wstep - 1
+
     def _label(self, rs: ReqState, r: Row) -> int:
         sc = rs.req.script
         if sc is not None and sc.answer is not None:
@@ -368,7 +388,7 @@ class Engine:
         cfg = self.cfg
         # PRM scores (L25/L33): final reward for rows done this window, current otherwise
         for r in self.rows:
-            if r.running:
+            if r.running or r.stopped:                # incomplete: its k-th running score
                 r.score = self.src.score_running(r, r.nbnd)
                 r.nbnd += 1
             else:
@@ -378,7 +398,7 @@ class Engine:
         for rid in involved:
             rs = self.live[rid]
             mine = [r for r in self.rows if r.rs is rs]
-            done = [r for r in mine if not r.running]
+            done = [r for r in mine if not r.running and not r.stopped]
             # L24-27 phase switch (R2, R3, R6)
             if rs.phase == EXPLORE and done:
                 first = min(done, key=lambda r: (r.done_wstep, r.b))
@@ -403,10 +423,12 @@ class Engine:
                         rs.branch_state[r.b] = PRUNED
                         rs.branch_len[r.b] = r.ell
                         rs.branch_score[r.b] = r.score
+            # R43: a request with stopped rows has num_completed >= M, so it finalizes now
+            assert not any(r.stopped for r in mine) or rs.num_completed >= rs.M
             # L38-40 output (R7)
             if rs.num_completed >= rs.M or rs.num_completed + rs.num_pruned == rs.N:
                 for r in mine:
-                    if r.running and r.terminal == RUNNING:
+                    if (r.running or r.stopped) and r.terminal == RUNNING:
                         r.terminal = EARLY_STOPPED
                         rs.num_early_stopped += 1
                         rs.branch_state[r.b] = EARLY_STOPPED

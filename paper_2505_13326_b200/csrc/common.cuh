@@ -14,6 +14,7 @@ typedef __nv_bfloat16 bf16;
 #define ST_CAP 3
 #define ST_PRUNED 4
 #define ST_ES 5
+#define ST_STOP 7             // es_every_step (R43): stopped mid-window by early stop, EarlyStopped at the boundary
 
 template <typename T> __device__ __forceinline__ float to_f(T x);
 template <> __device__ __forceinline__ float to_f<float>(float x) { return x; }
@@ -67,6 +68,7 @@ struct Reqs {
   long long* id;
   int *N, *M, *P, *beta, *prune, *phase, *maxp, *nc, *np, *nes, *npre, *first_tok;
   int *has_script, *has_answer, *has_forced, *nbnd;
+  int* ncw;         // completed branches including this window's so far (es_every_step, R43)
   float *alpha, *thr;
   int* prefix;      // [S][MPB]
   int* br_state;    // [S][32]

@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(NT) k_admit(const AdmitEvent* __restrict__ ev,
       reqs.thr[slot] = E.alpha;
       reqs.maxp[slot] = E.beta;
       reqs.nc[slot] = 0;
+      reqs.ncw[slot] = 0;
       reqs.np[slot] = 0;
       reqs.nes[slot] = 0;
       reqs.final_flag[slot] = 0;
@@ -143,7 +144,8 @@ void launch_admit(const AdmitEvent* ev, int n_ev, int total_pop, int new_rows, i
 // ------------------------------------------------------------------ boundary
 __global__ void __launch_bounds__(NT) k_boundary(Dims D, Rows rows, Rows tmp, Reqs reqs,
                                                   const float* __restrict__ prm, int* __restrict__ fs, Ctr* ctr,
-                                                  DevResult* __restrict__ res, int* __restrict__ slot_row, int n) {
+                                                  DevResult* __restrict__ res, int* __restrict__ slot_row, int n,
+                                                  BoundaryTrace tr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ int s_nlead;
   __shared__ int s_lead[NT];
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(NT) k_boundary(Dims D, Rows rows, Rows tmp, Re
     const int slot = rows.slot[r], b = rows.b[r];
     const long long sb = (long long)slot * SART_MAXN + b;
     float score;
-    if (rows.status[r] == RUNNING_ST) {
+    if (rows.status[r] == RUNNING_ST || rows.status[r] == ST_STOP) {   // incomplete: running score (R43)
       const int k = rows.nbnd[r];
       score = reqs.has_script[slot] ? reqs.sc_scores[sb * D.nbnd_max + min(k, reqs.nbnd[slot] - 1)] : prm[r];
       rows.nbnd[r] = k + 1;
@@ -167,6 +169,11 @@ __global__ void __launch_bounds__(NT) k_boundary(Dims D, Rows rows, Rows tmp, Re
     rows.score[r] = score;
     rows.term[r] = RUNNING_ST;
     slot_row[sb] = r;
+    if (tr.score) {   // record_trace (PP2): the score used and the row's state, in window-row order
+      tr.score[r] = score;
+      tr.state[r] = rows.status[r];
+      tr.ell[r] = rows.ell[r];
+    }
   }
   __syncthreads();
   // involved requests (R19): one leader row per request (its lowest batch row)
@@ -189,7 +196,9 @@ __global__ void __launch_bounds__(NT) k_boundary(Dims D, Rows rows, Rows tmp, Re
     const int r = lane < N ? slot_row[sb] : -1;
     const bool has = r >= 0;
     const int st = has ? rows.status[r] : 0;
-    const bool running = has && st == RUNNING_ST, done = has && st != RUNNING_ST;
+    // stopped (es_every_step, R43): incomplete, not prunable, EarlyStopped by the finalize below
+    const bool stopped = has && st == ST_STOP;
+    const bool running = has && (st == RUNNING_ST || stopped), done = has && (st == ST_EOS || st == ST_CAP);
     const float sc = has ? rows.score[r] : 0.f;
     int phase = reqs.phase[slot], maxp = reqs.maxp[slot], nc = reqs.nc[slot], np = reqs.np[slot];
     float thr = reqs.thr[slot];
@@ -224,7 +233,7 @@ __global__ void __launch_bounds__(NT) k_boundary(Dims D, Rows rows, Rows tmp, Re
     // while num_pruned < max_num_pruned; alpha < 0 disables pruning (R20)
     bool pr = false;
     if (reqs.prune[slot]) {
-      const bool cand = running && sc < thr;
+      const bool cand = running && !stopped && sc < thr;
       const unsigned cm = __ballot_sync(0xffffffffu, cand);
       const int allow = maxp - np;
       const int rank = __popc(cm & ((1u << lane) - 1u));
@@ -305,6 +314,7 @@ __global__ void __launch_bounds__(NT) k_boundary(Dims D, Rows rows, Rows tmp, Re
       reqs.thr[slot] = thr;
       reqs.maxp[slot] = maxp;
       reqs.nc[slot] = nc;
+      reqs.ncw[slot] = nc;
       reqs.np[slot] = np;
       reqs.nes[slot] = nes;
     }
@@ -393,6 +403,6 @@ __global__ void __launch_bounds__(NT) k_boundary(Dims D, Rows rows, Rows tmp, Re
   }
 }
 void launch_boundary(Dims D, Rows rows, Rows tmp, Reqs reqs, const float* prm_score, int* free_stack, Ctr* ctr,
-                     DevResult* res, int* slot_row, int n, cudaStream_t s) {
-  k_boundary<<<1, NT, 0, s>>>(D, rows, tmp, reqs, prm_score, free_stack, ctr, res, slot_row, n);
+                     DevResult* res, int* slot_row, int n, BoundaryTrace tr, cudaStream_t s) {
+  k_boundary<<<1, NT, 0, s>>>(D, rows, tmp, reqs, prm_score, free_stack, ctr, res, slot_row, n, tr);
 }

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(32) k_sample_final(Dims D, Rows rows, Reqs req
   if (y == D.eos) st = ST_EOS;                  // O5 / R17
   else if (s == D.cap) st = ST_CAP;
   if (st != RUNNING_ST) {
+    atomicAdd(&reqs.ncw[slot], 1);              // completions so far (es_every_step, R43)
     rows.status[r] = st;
     rows.done_step[r] = s;
     rows.done_wstep[r] = ctr->wstep;
@@ -127,9 +128,29 @@ void launch_sample(const float* logits, Dims D, Rows rows, Reqs reqs, Ctr* ctr, 
 int sample_chunks(int V) { return (V + SCHUNK - 1) / SCHUNK; }
 
 
-__global__ void k_step_begin(Ctr* ctr) {
+// Start of a decode step.  es_every_step (reading R43): a running row whose request already
+// has M completed branches -- counted at the end of the previous step -- stops here: it keeps
+// the steps it has (done_step = l) and is EarlyStopped at the boundary.
+__global__ void k_step_begin(Ctr* ctr, int es, Dims D, Rows rows, Reqs reqs, int n) {
   pdl_wait();
   pdl_trigger();
-  if (ctr->live > 0) { ctr->wstep += 1; ctr->steps += 1; }
+  if (es) {
+    int stopped = 0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      if (rows.status[r] != RUNNING_ST) continue;
+      const int slot = rows.slot[r];
+      if (reqs.ncw[slot] >= reqs.M[slot]) {
+        rows.status[r] = ST_STOP;
+        rows.done_step[r] = rows.ell[r];
+        rows.done_wstep[r] = ctr->wstep;
+        ++stopped;
+      }
+    }
+    if (stopped) atomicSub(&ctr->live, stopped);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && ctr->live > 0) { ctr->wstep += 1; ctr->steps += 1; }
 }
-void launch_step_begin(Ctr* ctr, cudaStream_t s) { launch_pdl(k_step_begin, dim3(1), dim3(1), 0, s, ctr); }
+void launch_step_begin(Ctr* ctr, int es, Dims D, Rows rows, Reqs reqs, int n, cudaStream_t s) {
+  launch_pdl(k_step_begin, dim3(1), dim3(es ? 1024 : 1), 0, s, ctr, es, D, rows, reqs, n);
+}

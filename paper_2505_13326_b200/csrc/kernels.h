@@ -124,7 +124,7 @@ void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg,
 void launch_sample(const float* logits, Dims D, Rows rows, Reqs reqs, Ctr* ctr, int n, int* dbg_tok, float* pkey,
                    int* pv, cudaStream_t s);
 int sample_chunks(int V);
-void launch_step_begin(Ctr* ctr, cudaStream_t s);
+void launch_step_begin(Ctr* ctr, int es, Dims D, Rows rows, Reqs reqs, int n, cudaStream_t s);
 
 // ---- control (k_ctl.cu)
 // type 0 = prefill (pop the prefix blocks, init meta[i], Alg. 1 L16), 1 = new row (L5)
@@ -136,8 +136,15 @@ struct AdmitEvent {
 };
 void launch_admit(const AdmitEvent* ev, int n_ev, int total_pop, int new_rows, int commit_delta, Dims D,
                   Rows rows, Reqs reqs, int* free_stack, Ctr* ctr, cudaStream_t s);
+// record_trace (PP2): per window row, the score the boundary used, its status at the end of
+// the window (RUNNING, EOS, CAP) and its step count -- before compaction.  All null: off.
+struct BoundaryTrace {
+  float* score;
+  int* state;
+  int* ell;
+};
 void launch_boundary(Dims D, Rows rows, Rows tmp, Reqs reqs, const float* prm_score, int* free_stack,
-                     Ctr* ctr, DevResult* res, int* slot_row, int n, cudaStream_t s);
+                     Ctr* ctr, DevResult* res, int* slot_row, int n, BoundaryTrace tr, cudaStream_t s);
 void launch_window_begin(Ctr* ctr, int n, cudaStream_t s);
 // f2 PRM pass: token list of one chunk from its segments (tok: input token of the entry,
 // row: batch row, ent: suffix entry), and the gather of each row's last-entry state

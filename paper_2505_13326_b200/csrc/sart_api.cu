@@ -138,6 +138,13 @@ struct sart_ctx {
   double attn_ms = 0, attn_bytes = 0, attn_bytes_base = 0, prefill_ms = 0;
   long long attn_launches = 0, launches = 0;
   long long h2d_bytes = 0, d2h_bytes = 0;   // host<->device bytes of the serving path (sart_profile)
+  // record_trace (PP2): per-window streams and per-boundary state hashes for oracle replay
+  std::vector<sart_trace_row> trace_rows;
+  std::vector<int32_t> trace_tokens;
+  std::vector<uint64_t> trace_hashes;
+  std::vector<int> trace_ell0;   // rows.ell at window start
+  BoundaryTrace dtr{nullptr, nullptr, nullptr};
+  bool own_pool = true;          // false: caller-owned kv_pool (never freed here)
 
   // row f2: the separate PRM decoder is a sub-context holding its own dims, weights, KV pool
   // and workspaces; it shares rows / reqs / stream with the policy ctx.
@@ -250,7 +257,7 @@ cudaError_t alloc_reqs(sart_ctx* ctx) {
   cudaError_t e;
   size_t S = D.S, S32 = (size_t)D.S * SART_MAXN;
   if ((e = dalloc(ctx, &q.id, sizeof(long long) * S)) != cudaSuccess) return e;
-  int** ints[] = {&q.N, &q.M, &q.P, &q.beta, &q.prune, &q.phase, &q.maxp, &q.nc, &q.np, &q.nes, &q.npre,
+  int** ints[] = {&q.N, &q.M, &q.P, &q.beta, &q.prune, &q.phase, &q.maxp, &q.nc, &q.ncw, &q.np, &q.nes, &q.npre,
                   &q.first_tok, &q.has_script, &q.has_answer, &q.has_forced, &q.nbnd, &q.final_flag};
   for (auto p : ints)
     if ((e = dalloc(ctx, p, sizeof(int) * S)) != cudaSuccess) return e;
@@ -384,7 +391,7 @@ void decode_step(sart_ctx* ctx, int n) {
   const Dims& D = ctx->D;
   cudaStream_t s = ctx->st;
   const int ab = ctx->ablate;
-  launch_step_begin(ctx->ctr, s);
+  launch_step_begin(ctx->ctr, ctx->cfg.es_every_step, D, ctx->rows, ctx->reqs, n, s);
   launch_embed<T>(ctx->rows.tok, ctx->W_<T>(t_embed()), ctx->h, n, D.d, s);
   ctx->launches += 2;
   if (ctx->cfg.profile) {
@@ -837,6 +844,112 @@ int read_boundary(sart_ctx* ctx) {
   return SART_OK;
 }
 
+// ------------------------------------------------------------------ PP2 trace (record_trace)
+struct Fnv {
+  uint64_t h = 1469598103934665603ull;
+  void bytes(const void* p, size_t n) {
+    const unsigned char* c = (const unsigned char*)p;
+    for (size_t i = 0; i < n; ++i) { h ^= c[i]; h *= 1099511628211ull; }
+  }
+  void i32(int32_t v) { bytes(&v, 4); }
+  void i64(int64_t v) { bytes(&v, 8); }
+};
+
+// FNV-1a 64 of the control state after a boundary (layout: include/sart.h, sart_trace_fetch)
+int state_hash(sart_ctx* ctx, uint64_t* out) {
+  const Dims& D = ctx->D;
+  const int n = ctx->n_rows;
+  std::vector<int> slot(n), b(n), ell(n), nblk(n), tab((size_t)n * D.MBR);
+  if (n) {
+    CK(cudaMemcpy(slot.data(), ctx->rows.slot, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b.data(), ctx->rows.b, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ell.data(), ctx->rows.ell, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(nblk.data(), ctx->rows.nblk, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tab.data(), ctx->rows.table, 4 * tab.size(), cudaMemcpyDeviceToHost));
+  }
+  Fnv f;
+  for (int r = 0; r < n; ++r) {
+    f.i64(ctx->slots[slot[r]].id);
+    f.i32(b[r]);
+    f.i32(ell[r]);
+    f.i32(nblk[r]);
+    for (int j = 0; j < nblk[r]; ++j) f.i32(tab[(size_t)r * D.MBR + j]);
+  }
+  std::vector<int> fs((size_t)ctx->free_top);
+  if (!fs.empty()) CK(cudaMemcpy(fs.data(), ctx->free_stack, 4 * fs.size(), cudaMemcpyDeviceToHost));
+  f.i32((int32_t)fs.size());
+  for (int x : fs) f.i32(x);
+  f.i64(ctx->committed);
+  std::vector<std::pair<int64_t, int>> live;
+  for (int s = 0; s < D.S; ++s)
+    if (ctx->slots[s].live) live.emplace_back(ctx->slots[s].id, s);
+  std::sort(live.begin(), live.end());
+  f.i32((int32_t)live.size());
+  for (auto& [id, s] : live) {
+    int v[5];
+    float thr;
+    CK(cudaMemcpy(&v[0], ctx->reqs.phase + s, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&thr, ctx->reqs.thr + s, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&v[1], ctx->reqs.maxp + s, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&v[2], ctx->reqs.nc + s, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&v[3], ctx->reqs.np + s, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&v[4], ctx->reqs.npre + s, 4, cudaMemcpyDeviceToHost));
+    uint32_t tb;
+    memcpy(&tb, &thr, 4);
+    f.i64(id);
+    f.i32(v[0]);
+    f.i32((int32_t)tb);
+    f.i32(v[1]);
+    f.i32(v[2]);
+    f.i32(v[3]);
+    f.i32(v[4]);
+    std::vector<int> pre(v[4]);
+    if (v[4]) CK(cudaMemcpy(pre.data(), ctx->reqs.prefix + (size_t)s * D.MPB, 4 * (size_t)v[4], cudaMemcpyDeviceToHost));
+    for (int x : pre) f.i32(x);
+  }
+  *out = f.h;
+  return SART_OK;
+}
+
+// After the boundary of a window of n rows: each row's new tokens (reqs.hist [ell_start, ell))
+// and the score the boundary used, then the state hash.  The finalized requests' slots were
+// released by read_boundary, but nothing has overwritten their history yet (the next fill
+// runs after this).
+int record_trace_window(sart_ctx* ctx, int n) {
+  const Dims& D = ctx->D;
+  std::vector<int> slot(n), b(n), st(n), ell(n);
+  std::vector<float> sc(n);
+  if (n) {
+    CK(cudaMemcpy(slot.data(), ctx->dbg_slot, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b.data(), ctx->dbg_b, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(st.data(), ctx->dtr.state, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ell.data(), ctx->dtr.ell, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sc.data(), ctx->dtr.score, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+  }
+  for (int r = 0; r < n; ++r) {
+    sart_trace_row t{};
+    t.request_id = ctx->last_slot_id[slot[r]];
+    t.branch = b[r];
+    t.window = ctx->windows - 1;
+    t.ell_start = ctx->trace_ell0[r];
+    t.n_tokens = ell[r] - t.ell_start;
+    t.running = st[r] == RUNNING_ST ? 1 : 0;
+    t.score = sc[r];
+    t.tokens_offset = (int64_t)ctx->trace_tokens.size();
+    ctx->trace_tokens.resize(ctx->trace_tokens.size() + t.n_tokens);
+    if (t.n_tokens > 0)
+      CK(cudaMemcpy(ctx->trace_tokens.data() + t.tokens_offset,
+                    ctx->reqs.hist + ((size_t)slot[r] * SART_MAXN + b[r]) * D.cap + t.ell_start,
+                    4 * (size_t)t.n_tokens, cudaMemcpyDeviceToHost));
+    ctx->trace_rows.push_back(t);
+  }
+  uint64_t h = 0;
+  const int rc = state_hash(ctx, &h);
+  if (rc) return rc;
+  ctx->trace_hashes.push_back(h);
+  return SART_OK;
+}
+
 template <typename T>
 int run_window(sart_ctx* ctx) {
   const Dims& D = ctx->D;
@@ -845,6 +958,11 @@ int run_window(sart_ctx* ctx) {
   ctx->ev_used = 0;
   launch_window_begin(ctx->ctr, n, ctx->st);
   ctx->launches++;
+  if (ctx->cfg.record_trace) {   // PP2: steps each row had before this window
+    ctx->trace_ell0.resize(n);
+    if (n) CK(cudaMemcpyAsync(ctx->trace_ell0.data(), ctx->rows.ell, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+  }
   if (ctx->prm)   // entries decoded this window = ell(boundary) - ell(now), per row (f2 pass)
     CK(xfer(ctx, ctx->prm->h_ell_ws, ctx->rows.ell, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->st));
   if (ctx->bf16) {   // work units of the cascade attention for this window's batch
@@ -914,11 +1032,12 @@ int run_window(sart_ctx* ctx) {
     prm_scores<T>(ctx, n);
   }
   launch_boundary(D, ctx->rows, ctx->tmp, ctx->reqs, ctx->prm ? ctx->prm->prm_score : ctx->prm_score, ctx->free_stack, ctx->ctr, ctx->res,
-                  ctx->slot_row, n, ctx->st);
+                  ctx->slot_row, n, ctx->dtr, ctx->st);
   ctx->launches++;
   CK(cudaGetLastError());
   int rc = read_boundary(ctx);
   if (rc) return rc;
+  if (ctx->cfg.record_trace && (rc = record_trace_window(ctx, n)) != SART_OK) return rc;
   if (ctx->prm) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ctx->prm->prm_ev[0], ctx->prm->prm_ev[1]) == cudaSuccess) ctx->prm_ms += ms;
@@ -1098,6 +1217,9 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   if (cfg.select_mode != 0 && cfg.select_mode != 1) return set_err(SART_EINVAL, "select_mode");
   if (cfg.attn_mode != 0 && cfg.attn_mode != 1) return set_err(SART_EINVAL, "attn_mode");
   if (cfg.prm_n_layers < 0) return set_err(SART_EINVAL, "prm_n_layers < 0");
+  if (cfg.es_every_step != 0 && cfg.es_every_step != 1) return set_err(SART_EINVAL, "es_every_step must be 0 or 1");
+  if (cfg.record_trace != 0 && cfg.record_trace != 1) return set_err(SART_EINVAL, "record_trace must be 0 or 1");
+  if (cfg.kv_pool && cfg.kv_pool_bytes == 0) return set_err(SART_EINVAL, "kv_pool given with kv_pool_bytes == 0");
   if (cfg.prm_n_layers > 0) {   // row f2: separate PRM decoder
     if (cfg.prm_d_model < 1 || cfg.prm_n_heads < 1 || cfg.prm_n_kv_heads < 1 || cfg.prm_d_ff < 1)
       return set_err(SART_EINVAL, "PRM model dims must be positive");
@@ -1215,6 +1337,11 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   ctx->ev_cap = D.R + D.S + 64;
   IC(dalloc(ctx, &ctx->d_events, sizeof(AdmitEvent) * ctx->ev_cap));
   if (cfg.debug_capture) IC(dalloc(ctx, &ctx->dbg_attn, (size_t)D.L * D.R * D.qh * D.hd * 4));
+  if (cfg.record_trace) {
+    IC(dalloc(ctx, &ctx->dtr.score, sizeof(float) * D.R));
+    IC(dalloc(ctx, &ctx->dtr.state, sizeof(int) * D.R));
+    IC(dalloc(ctx, &ctx->dtr.ell, sizeof(int) * D.R));
+  }
   {  // cascade attention plan and partial outputs
     AttnPlan& pl = ctx->plan;
     pl.CH = 512;   // tokens per attention chunk (SART_ATTN_CH overrides; multiple of 64)
@@ -1255,7 +1382,15 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   const size_t prm_blk_bytes =
       ctx->prm ? (size_t)ctx->prm->D.L * 2 * ctx->prm->D.kvh * D.bs * ctx->prm->D.hd * es : 0;
   long long NB = cfg.num_blocks;
-  if (NB <= 0) {
+  if (cfg.kv_pool) {   // caller-owned pool: it bounds NB
+    const long long fit = (long long)(cfg.kv_pool_bytes / blk_bytes);
+    if (NB <= 0) NB = fit;
+    if (NB > fit) {
+      set_err(SART_ENOMEM, "kv_pool_bytes smaller than num_blocks x block bytes");
+      sart_destroy(ctx);
+      return SART_ENOMEM;
+    }
+  } else if (NB <= 0) {
     size_t fr = 0, tot = 0;
     IC(cudaMemGetInfo(&fr, &tot));
     const size_t reserve = (size_t)3 << 30;
@@ -1267,7 +1402,15 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     return SART_ENOMEM;
   }
   D.NB = NB;
-  IC(dalloc(ctx, &ctx->pool, (size_t)NB * blk_bytes));
+  if (cfg.kv_pool) {
+    // never-written slots of a partially filled stage are multiplied by p = 0 in the attention
+    // kernels: they must be finite, so the borrowed pool is zeroed like an allocated one
+    ctx->pool = cfg.kv_pool;
+    ctx->own_pool = false;
+    IC(cudaMemsetAsync(ctx->pool, 0, (size_t)NB * blk_bytes, ctx->st));
+  } else {
+    IC(dalloc(ctx, &ctx->pool, (size_t)NB * blk_bytes));
+  }
   if (ctx->prm) {
     ctx->prm->D.NB = NB;
     IC(dalloc(ctx->prm, &ctx->prm->pool, (size_t)NB * prm_blk_bytes));
@@ -1635,6 +1778,26 @@ int sart_debug_prm_plan(const int32_t* ell_ws, const int32_t* ell, int32_t n, in
     const PrmPlan::Chunk& k = P.chunks[c];
     chunks[4 * c] = k.ntok; chunks[4 * c + 1] = k.nseg; chunks[4 * c + 2] = k.nqb; chunks[4 * c + 3] = k.ngat;
   }
+  return SART_OK;
+}
+
+int sart_trace_fetch(sart_ctx* ctx, sart_trace_row* rows, int64_t rows_cap, int64_t* n_rows, int32_t* tokens_out,
+                     int64_t tokens_cap, int64_t* n_tokens, uint64_t* hashes, int64_t hashes_cap, int64_t* n_hashes) {
+  if (!ctx || !n_rows || !n_tokens || !n_hashes) return set_err(SART_EINVAL, "null argument");
+  if (!ctx->cfg.record_trace) return set_err(SART_EINVAL, "record_trace is off");
+  *n_rows = (int64_t)ctx->trace_rows.size();
+  *n_tokens = (int64_t)ctx->trace_tokens.size();
+  *n_hashes = (int64_t)ctx->trace_hashes.size();
+  if (*n_rows > rows_cap || *n_tokens > tokens_cap || *n_hashes > hashes_cap)
+    return set_err(SART_EFULL, "trace buffers too small (counts written, nothing moved)");
+  if ((*n_rows && !rows) || (*n_tokens && !tokens_out) || (*n_hashes && !hashes))
+    return set_err(SART_EINVAL, "null buffer");
+  if (*n_rows) memcpy(rows, ctx->trace_rows.data(), sizeof(sart_trace_row) * (size_t)*n_rows);
+  if (*n_tokens) memcpy(tokens_out, ctx->trace_tokens.data(), sizeof(int32_t) * (size_t)*n_tokens);
+  if (*n_hashes) memcpy(hashes, ctx->trace_hashes.data(), sizeof(uint64_t) * (size_t)*n_hashes);
+  ctx->trace_rows.clear();
+  ctx->trace_tokens.clear();
+  ctx->trace_hashes.clear();
   return SART_OK;
 }
 

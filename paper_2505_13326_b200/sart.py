@@ -44,6 +44,8 @@ class SartConfig(C.Structure):
         ("prm_n_layers", C.c_int32), ("prm_d_model", C.c_int32), ("prm_n_heads", C.c_int32),
         ("prm_n_kv_heads", C.c_int32), ("prm_head_dim", C.c_int32), ("prm_d_ff", C.c_int32),
         ("prm_weight_seed", C.c_uint64), ("prm_host_weights", C.c_void_p),
+        ("kv_pool", C.c_void_p), ("kv_pool_bytes", C.c_size_t), ("es_every_step", C.c_int32),
+        ("record_trace", C.c_int32),
     ]
 
 
@@ -76,6 +78,11 @@ class SartResult(C.Structure):
                 ("branch_score", C.c_float * 32), ("t_arrival_ns", C.c_int64), ("t_prefill_ns", C.c_int64),
                 ("t_final_ns", C.c_int64), ("window_final", C.c_int32), ("selected_branch", C.c_int32),
                 ("tokens_offset", C.c_int64), ("tokens_len", C.c_int32)]
+
+
+class SartTraceRow(C.Structure):
+    _fields_ = [("request_id", C.c_int64), ("branch", C.c_int32), ("window", C.c_int32), ("ell_start", C.c_int32),
+                ("n_tokens", C.c_int32), ("running", C.c_int32), ("score", C.c_float), ("tokens_offset", C.c_int64)]
 
 
 P32 = C.POINTER(C.c_int32)
@@ -130,7 +137,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                     C.c_int32, C.c_int32, C.c_int32, C.c_int32]
     lib.sart_debug_prm_plan.argtypes = [P32, P32, C.c_int32, C.c_int32, C.c_int32, P32, C.c_int32, P32, P32, P32,
                                         P32, C.c_int32, P32]
-    for f in ("sart_debug_prm_plan", "sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
+    lib.sart_trace_fetch.argtypes = [C.c_void_p, C.POINTER(SartTraceRow), C.c_int64, P64, P32, C.c_int64, P64,
+                                     C.POINTER(C.c_uint64), C.c_int64, P64]
+    for f in ("sart_trace_fetch", "sart_debug_prm_plan", "sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
               "sart_get_state", "sart_debug_fetch", "sart_get_profile", "sart_reset_profile", "sart_debug_gemm", "sart_set_profile"):
         getattr(lib, f).restype = C.c_int
     _lib = lib
@@ -139,7 +148,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 
 EXPORTED = ["sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
             "sart_strerror", "sart_last_error", "sart_get_state", "sart_debug_fetch", "sart_get_profile",
-            "sart_reset_profile", "sart_debug_gemm", "sart_set_profile", "sart_debug_prm_plan"]
+            "sart_reset_profile", "sart_debug_gemm", "sart_set_profile", "sart_debug_prm_plan", "sart_trace_fetch"]
 
 
 def debug_prm_plan(ell_ws, ell, chunk: int, qp: int):
@@ -201,9 +210,12 @@ class Engine:
                  eos_id: int = 1, temperature: float = 1.0, sampler_seed: int = 0, select_mode: int = 0,
                  attn_mode: int = SART_ATTN_CASCADE, device: int = 0, stream: int = 0,
                  enable_forced_tokens: bool = False, debug_capture: bool = False, profile: bool = False,
-                 prm_shape=None, prm_host_weights: Optional[np.ndarray] = None, prm_weight_seed: int = 0):
+                 prm_shape=None, prm_host_weights: Optional[np.ndarray] = None, prm_weight_seed: int = 0,
+                 kv_pool=None, es_every_step: bool = False, record_trace: bool = False):
         """prm_shape (a synth.ModelShape, vocab = the policy's): the separate PRM decoder of
-        row f2; None -> the PRM head on the policy's hidden state."""
+        row f2; None -> the PRM head on the policy's hidden state.  kv_pool: (device address,
+        bytes) of a caller-owned KV pool buffer (e.g. a torch tensor's data_ptr() and nbytes;
+        the caller keeps it alive until close())."""
         self.lib = load_library()
         self.shape = shape
         self.cap, self.T = cap, T
@@ -224,6 +236,9 @@ class Engine:
         cfg.device, cfg.stream = device, stream or None
         cfg.enable_forced_tokens, cfg.debug_capture = int(enable_forced_tokens), int(debug_capture)
         cfg.profile = int(profile)
+        if kv_pool is not None:
+            cfg.kv_pool, cfg.kv_pool_bytes = int(kv_pool[0]), int(kv_pool[1])
+        cfg.es_every_step, cfg.record_trace = int(es_every_step), int(record_trace)
         self._prm_weights = None
         if prm_shape is not None:
             if prm_shape.vocab != shape.vocab:
@@ -325,6 +340,28 @@ class Engine:
                 out.append(d)
             if rc == SART_OK:
                 return out
+
+    # ---------------------------------------------------------------- PP2 trace
+    def trace_fetch(self):
+        """sart_trace_fetch: (rows, hashes) recorded since the last call.  rows: dicts with
+        request_id, branch, window, ell_start, running, score (fp32) and tokens (this window's)."""
+        nr, nt, nh = C.c_int64(), C.c_int64(), C.c_int64()
+        rc = self.lib.sart_trace_fetch(self.ctx, None, 0, C.byref(nr), None, 0, C.byref(nt), None, 0, C.byref(nh))
+        if rc not in (SART_OK, SART_EFULL):
+            _check(rc)
+        rows = (SartTraceRow * max(1, nr.value))()
+        toks = np.zeros(max(1, nt.value), np.int32)
+        hs = np.zeros(max(1, nh.value), np.uint64)
+        _check(self.lib.sart_trace_fetch(self.ctx, rows, nr.value, C.byref(nr), toks.ctypes.data_as(P32), nt.value,
+                                         C.byref(nt), hs.ctypes.data_as(C.POINTER(C.c_uint64)), nh.value,
+                                         C.byref(nh)))
+        out = []
+        for i in range(nr.value):
+            r = rows[i]
+            out.append(dict(request_id=r.request_id, branch=r.branch, window=r.window, ell_start=r.ell_start,
+                            running=r.running, score=r.score,
+                            tokens=toks[r.tokens_offset:r.tokens_offset + r.n_tokens].tolist()))
+        return out, [int(h) for h in hs[: nh.value]]
 
     # ---------------------------------------------------------------- test hooks
     def state(self, rows_cap: int = 4096, table_cap: int = 512, free_cap: int = 1 << 22,

@@ -11,8 +11,9 @@ def gpu_engine(shape, dtype="bf16", weights=None, **kw):
     return Engine(shape, dtype, host_weights=blob, **kw)
 
 
-def oracle_engine(bs, nb, T, cap, B=1 << 30, eos=1, select=0, source=None):
-    cfg = EngineConfig(block_size=bs, num_blocks=nb, max_rows=B, T=T, cap=cap, eos_id=eos, select_mode=select)
+def oracle_engine(bs, nb, T, cap, B=1 << 30, eos=1, select=0, source=None, es=False):
+    cfg = EngineConfig(block_size=bs, num_blocks=nb, max_rows=B, T=T, cap=cap, eos_id=eos, select_mode=select,
+                       es_every_step=es)
     return OEngine(cfg, source if source is not None else ScriptedSource(eos))
 
 
@@ -58,3 +59,24 @@ def rel_err_rows(gpu, ref):
     gpu = np.atleast_2d(np.asarray(gpu, np.float64))
     ref = np.atleast_2d(np.asarray(ref, np.float64))
     return np.max(np.abs(gpu - ref), axis=1) / np.maximum(np.max(np.abs(ref), axis=1), 1e-30)
+
+
+def fnv_state_hash(snap) -> int:
+    """FNV-1a 64 of an oracle snapshot in the byte layout include/sart.h documents for
+    sart_trace_fetch (written from that description; shares nothing with the library)."""
+    import struct
+    h = 1469598103934665603
+    buf = bytearray()
+    for (rid, b, ell, _nbnd), blocks in zip(snap["rows"], snap["tables"]):
+        buf += struct.pack("<qiii", rid, b, ell, len(blocks)) + struct.pack(f"<{len(blocks)}i", *blocks)
+    buf += struct.pack("<i", len(snap["free"])) + struct.pack(f"<{len(snap['free'])}i", *snap["free"])
+    buf += struct.pack("<q", snap["committed"])
+    buf += struct.pack("<i", len(snap["meta"]))
+    for rid in sorted(snap["meta"]):
+        phase, thr, maxp, nc, np_, pre = snap["meta"][rid]
+        buf += struct.pack("<qi", rid, phase) + struct.pack("<f", thr) + struct.pack("<iiii", maxp, nc, np_, len(pre))
+        buf += struct.pack(f"<{len(pre)}i", *pre)
+    for c in bytes(buf):
+        h ^= c
+        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h

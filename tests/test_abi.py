@@ -44,7 +44,7 @@ def test_struct_layout_matches_header():
     from paper_2505_13326_b200 import sart as S
     structs = {"sart_config": S.SartConfig, "sart_script": S.SartScript, "sart_request": S.SartRequest,
                "sart_stats": S.SartStats, "sart_result": S.SartResult, "sart_state": S.SartState,
-               "sart_profile": S.SartProfile}
+               "sart_profile": S.SartProfile, "sart_trace_row": S.SartTraceRow}
     lines = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{HEADER}"', "int main(void){"]
     for cname, py in structs.items():
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')

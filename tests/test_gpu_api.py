@@ -121,3 +121,65 @@ def test_collect_partial_buffers_and_counters():
     assert len(rest) == 3
     assert sorted([res[0].request_id, res[1].request_id] + [r["request_id"] for r in rest]) == [0, 1, 2, 3, 4]
     g.close()
+
+
+def test_forced_token_out_of_range_rejected():
+    """forced tokens become embedding indices -- out-of-range ids are EINVAL."""
+    from paper_2505_13326_b200.sart import SartError, SART_EINVAL
+    g = eng(enable_forced_tokens=True)
+    p = gen_prompt(0, 512, EOS, 5, 5)
+    ft = np.full((2, 32), 7, np.int32)
+    ft[1, 5] = 512
+    with pytest.raises(SartError) as e:
+        g.admit(Request(0, p, 2, 1, -1.0, 0, None), forced_tokens=ft)
+    assert e.value.code == SART_EINVAL
+    ft[1, 5] = -1
+    with pytest.raises(SartError) as e:
+        g.admit(Request(0, p, 2, 1, -1.0, 0, None), forced_tokens=ft)
+    assert e.value.code == SART_EINVAL
+    ft[1, 5] = 511
+    g.admit(Request(0, p, 2, 1, -1.0, 0, None), forced_tokens=ft)
+    assert g.step(100)["finalized_total"] == 1
+
+
+def test_dist_serve_with_cuda_engine_world1():
+    """SURVEY §8(e) on the real engine: dist.serve drives sart_admit / sart_step / sart_collect
+    and the C1 counter all-gather over NCCL (world size 1 on this one-GPU box); the result
+    records then go through the C2 tensor gather.  Equal to running the engine directly."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2505_13326_b200 import dist as sdist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        shape = SHAPES["tiny"]
+        reqs = gen_requests(9, shape, 4, 2, 0.5, 2, 32, 8, eos_id=EOS, p_range=(2, 40), length="uniform",
+                            len_range=(1, 32), root_seed=17)
+        arrivals = [reqs[0:3], [], reqs[3:7], reqs[7:9]]
+        seen = []
+        res = sdist.serve(eng(), arrivals, policy="least_loaded", on_window=lambda w, st, c: seen.append(c.clone()))
+        assert all(c.is_cuda and c.shape == (1, 16) for c in seen)
+        assert int(seen[-1][0, sdist.FINALIZED]) == 9
+        recs = sdist.gather_result_records(res, "cuda:0")
+        ref_eng = eng()
+        for r in reqs:
+            ref_eng.admit(r)
+        ref_eng.step(1000)
+        ref = {r["request_id"]: r for r in ref_eng.collect()}
+        assert sorted(r["request_id"] for r in res) == sorted(ref)
+        for r in res:
+            o = ref[r["request_id"]]
+            for k in ("answer_vote", "num_completed", "num_pruned", "num_early_stopped", "branch_len",
+                      "branch_state"):
+                assert r[k] == o[k], k
+        assert recs.shape == (9, len(sdist.RECORD_FIELDS))
+        assert sorted(recs[:, 0].tolist()) == sorted(ref)
+    finally:
+        dist.destroy_process_group()

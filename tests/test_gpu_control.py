@@ -17,10 +17,10 @@ from synth import SHAPES, gen_requests, gen_weights
 pytestmark = pytest.mark.gpu
 
 
-def run_pair(shape, reqs, bs, nb, T, cap, B, select=0, windows=100000, check_every=1):
+def run_pair(shape, reqs, bs, nb, T, cap, B, select=0, windows=100000, check_every=1, es=False):
     g = gpu_engine(shape, "bf16", None, block_size=bs, num_blocks=nb, max_rows=B, max_requests=64, max_prompt=2048,
-                   T=T, cap=cap, eos_id=1, select_mode=select, weight_seed=3)
-    o = oracle_engine(bs, nb, T, cap, B=B, select=select)
+                   T=T, cap=cap, eos_id=1, select_mode=select, weight_seed=3, es_every_step=es)
+    o = oracle_engine(bs, nb, T, cap, B=B, select=select, es=es)
     for r in reqs:
         g.admit(r)
         o.admit(r)
@@ -149,3 +149,24 @@ def test_more_than_1024_rows():
                         len_range=(1, cap), root_seed=31)
     res = run_pair(shape, reqs, bs, nb=4096, T=T, cap=cap, B=1500, check_every=1)
     assert len(res) == 47
+
+
+def test_es_every_step_trace_B_on_gpu():
+    """Reading R43 on the device (k_step_begin stops the rows, k_boundary early-stops them):
+    trace B under es_every_step, bit-exact with the oracle every window."""
+    from tests_traces import trace_B_request
+    res = run_pair(SHAPES["tiny"], [trace_B_request()], bs=16, nb=17, T=16, cap=64, B=1 << 20, es=True)
+    assert res[0]["branch_len"][:4] == [25, 10, 25, 25] and res[0]["window_final"] == 1
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_es_every_step_random_workloads(seed):
+    """es_every_step with pruning on, mixed N / M / alpha / beta, tight pools: bit-exact."""
+    rng = np.random.default_rng(500 + seed)
+    shape = SHAPES["tiny"]
+    bs = int(rng.choice([16, 64]))
+    T = int(rng.choice([4, 16, 40]))
+    cap = int(rng.integers(16, 120))
+    reqs = _mixed_requests(rng, shape, 40, cap, T, 0, 70 + seed)
+    need = max(-(-(len(r.prompt) - 1) // bs) for r in reqs) + -(-cap // bs)
+    run_pair(shape, reqs, bs, int(need * 5), T, cap, B=int(rng.integers(8, 96)), es=True)

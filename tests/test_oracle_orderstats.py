@@ -130,3 +130,63 @@ def test_engine_early_stop_with_boundaries():
         assert r["num_completed"] >= M
         assert r["num_completed"] == sum(1 for x in lens if x <= expect)
         assert r["num_early_stopped"] == N - r["num_completed"]
+
+
+def _run_es(lens, M, T, cap):
+    """Like _run_scripted, with es_every_step (reading R43)."""
+    N = len(lens)
+    sc = Script(np.asarray(lens, np.int32), np.zeros((N, 1), np.float32), np.zeros(N, np.float32),
+                np.zeros(N, np.int32))
+    eng = Engine(EngineConfig(block_size=16, num_blocks=4096, T=T, cap=cap, eos_id=1, es_every_step=True),
+                 ScriptedSource(1))
+    eng.admit(Request(0, np.array([5, 6], np.int32), N, M, -1.0, 0, sc))
+    eng.step(1000)
+    res = eng.collect()
+    assert len(res) == 1
+    return eng, res[0]
+
+
+@pytest.mark.parametrize("T", [1, 3, 4, 16])
+@pytest.mark.parametrize("M,expect", [(1, Fraction(177, 128)), (2, Fraction(269, 128)),
+                                      (4, Fraction(463, 128))])
+def test_es_every_step_stop_is_order_statistic(M, expect, T):
+    """Reading R43 (es_every_step): whatever T, the unfinished branches stop at X_(M), the
+    M-th smallest of the N lengths -- per instance exactly -- so over all 4^4
+    scripts the mean stop step is E[X_(M)] of Lemma 1, and the decoded tokens are
+    sum_{j<M} E[X_(j)] + (N-M+1) E[X_(M)]."""
+    N, k = 4, 4
+    pmf = [Fraction(0)] + [Fraction(1, k)] * k
+    total = tokens = 0
+    for lens in itertools.product(range(1, k + 1), repeat=N):
+        eng, r = _run_es(list(lens), M, T=T, cap=8)
+        xm = sorted(lens)[M - 1]
+        for b in range(N):
+            if lens[b] <= xm:
+                assert r["branch_state"][b] == 2 and r["branch_len"][b] == lens[b]
+            else:
+                assert r["branch_state"][b] == 5 and r["branch_len"][b] == xm, (lens, b, r["branch_len"])
+        assert r["num_completed"] == sum(1 for x in lens if x <= xm)
+        total += xm
+        tokens += eng.branch_tokens
+    n = k ** N
+    assert Fraction(total, n) == expect
+    Ej = [os_.expected_order_stat(j, N, pmf) for j in range(1, M + 1)]
+    assert Fraction(tokens, n) == sum(Ej[:-1], Fraction(0)) + (N - M + 1) * Ej[-1]
+
+
+def test_es_every_step_trace_B():
+    """SURVEY §8(c) trace B under es_every_step: b1 completes at 10, b3 at 25 -> M = 2 is
+    reached at step 25, so b0 and b2 stop at l = 25; the request finalizes at the boundary
+    of window 1 (step 32) with completions {b1, b3} (vote over those two)."""
+    from tests_traces import trace_B_request
+    eng = Engine(EngineConfig(block_size=16, num_blocks=17, T=16, cap=64, eos_id=1, es_every_step=True),
+                 ScriptedSource(1))
+    eng.admit(trace_B_request())
+    eng.step(100)
+    r = eng.collect()[0]
+    assert r["window_final"] == 1
+    assert r["branch_state"] == [5, 2, 5, 2]
+    assert r["branch_len"] == [25, 10, 25, 25]
+    assert (r["num_completed"], r["num_early_stopped"]) == (2, 2)
+    assert eng.steps == 25                     # window 1 ends early: nothing live after step 25
+    assert sorted(eng.free) == list(range(17))
