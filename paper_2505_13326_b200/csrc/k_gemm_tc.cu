@@ -261,8 +261,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // weights: pre-tiled (Bt: [n-tile][k-block] images of the swizzled shared tile, one
       // contiguous bulk copy each) or row-major through the 2-D tensor map
       auto load_b = [&](int st, int kbi, int n0_) {
-        if (Bt) bulk_load(sm.b[st], Bt + ((size_t)(n0_ / BN) * kb_all + kbi) * (BN * BK), BN * BK * 2, &sm.full[st]);
-        else tma_load_2d(sm.b[st], &tmB, &sm.full[st], kbi * BK, n0_);
+        if constexpr (MODE == GEMM_QKV_HALF) {
+          // half-head tile: weight rows [32p, 32p + 32) and [64 + 32p, ...) of head n0_ / 128
+          // as two 32-row boxes (four whole 8-row swizzle atoms each, so the 64-row smem tile
+          // keeps the layout one 64-row box would have)
+          const int hb = (n0_ / 128) * 128 + ((n0_ / 64) & 1) * 32;
+          tma_load_2d(sm.b[st], &tmB, &sm.full[st], kbi * BK, hb);
+          tma_load_2d(sm.b[st] + 32 * BK, &tmB, &sm.full[st], kbi * BK, hb + 64);
+        } else if (Bt) {
+          bulk_load(sm.b[st], Bt + ((size_t)(n0_ / BN) * kb_all + kbi) * (BN * BK), BN * BK * 2, &sm.full[st]);
+        } else {
+          tma_load_2d(sm.b[st], &tmB, &sm.full[st], kbi * BK, n0_);
+        }
       };
       auto load_a = [&](int st, int j, int kbi, int m0_) {
         tma_load_2d(sm.a[st] + j * BM * BK, &tmA, &sm.full[st], kbi * BK, m0_ + j * BM);
@@ -369,16 +379,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int m0 = m0_ + ms * BM;
       const int gm = m0 + row;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (as * MS + ms) * BN;
-      if (MODE == GEMM_QKV) {
-        // tile = one head (BN == head_dim): q / k heads are rotated (pairs i, i + hd/2), k and v
-        // are appended to the paged pool at the row's slot (common.cuh layout and swizzle).
-        // Split-K (S > 1): every unit publishes its fp32 partial tile (C + split * M * N); the
-        // last of the S units of a (m-tile, head, lane quarter) -- an atomic arrival count --
-        // sums the S partials in split order (deterministic) and runs the epilogue.
+      if (MODE == GEMM_QKV || MODE == GEMM_QKV_HALF) {
+        // tile = one head (GEMM_QKV, BN == head_dim) or half a head (GEMM_QKV_HALF, hd = 128):
+        // q / k heads are rotated (pairs i, i + hd/2), k and v are appended to the paged pool
+        // at the row's slot (common.cuh layout and swizzle).  Tile column c < HALF is head dim
+        // i0 + c and column HALF + c is dim hd/2 + i0 + c.
+        // Split-K (S > 1, GEMM_QKV only): every unit publishes its fp32 partial tile (C + split
+        // * M * N); the last of the S units of a (m-tile, head, lane quarter) -- an atomic
+        // arrival count -- sums the S partials in split order (deterministic) and runs the
+        // epilogue.
         const Dims& D = epi.D;
-        const int head = n0 / BN;
-        constexpr int HALF = BN / 2;
-        if (S > 1) {
+        constexpr int HD = MODE == GEMM_QKV_HALF ? 128 : BN;
+        constexpr int HALF = BN / 2, HHD = HD / 2;
+        const int head = n0 / HD;
+        const int i0 = MODE == GEMM_QKV_HALF ? ((n0 / 64) & 1) * 32 : 0;
+        if (MODE == GEMM_QKV && S > 1) {
           store_tile_f32<BN, GEMM_STORE>(tbase, Cs, m0 + q * 32, n0, M, N, nullptr, smem_u32(sm.slab[warp - 2]), lane, half * 32, CSTEP);
           __threadfence();
           __syncwarp();
@@ -420,7 +435,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
         const bool rot = head < D.qh + D.kvh;
-        const float* cs = epi.rope_cs + (long long)pos * BN;   // [cos(half) | sin(half)]
+        const float* cs = epi.rope_cs + (long long)pos * HD;   // [cos(hd/2) | sin(hd/2)]
 #pragma unroll 1
         for (int c = half * 32; c < HALF; c += CSTEP) {
           float x1[32], x2[32];
@@ -442,13 +457,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
           }
           if (gm < M) {
+            const float* bh = epi.bias + head * HD + i0 + c;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) { x1[j] += epi.bias[n0 + c + j]; x2[j] += epi.bias[n0 + HALF + c + j]; }
+            for (int j = 0; j < 32; ++j) { x1[j] += bh[j]; x2[j] += bh[HHD + j]; }
             if (rot) {
 #pragma unroll
               for (int j4 = 0; j4 < 8; ++j4) {
-                const float4 co = *reinterpret_cast<const float4*>(cs + c + 4 * j4);
-                const float4 sn = *reinterpret_cast<const float4*>(cs + HALF + c + 4 * j4);
+                const float4 co = *reinterpret_cast<const float4*>(cs + i0 + c + 4 * j4);
+                const float4 sn = *reinterpret_cast<const float4*>(cs + HHD + i0 + c + 4 * j4);
                 const float cv[4] = {co.x, co.y, co.z, co.w}, sv[4] = {sn.x, sn.y, sn.z, sn.w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -460,14 +476,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             }
             if (head < D.qh) {
-              bf16* qd = epi.qout + ((long long)gm * D.qh + head) * BN;
+              bf16* qd = epi.qout + ((long long)gm * D.qh + head) * HD + i0;
 #pragma unroll
               for (int j = 0; j < 32; j += 8) {
                 __align__(16) bf16 o1[8], o2[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) { o1[e] = __float2bfloat16_rn(x1[j + e]); o2[e] = __float2bfloat16_rn(x2[j + e]); }
                 *reinterpret_cast<uint4*>(qd + c + j) = *reinterpret_cast<uint4*>(o1);
-                *reinterpret_cast<uint4*>(qd + HALF + c + j) = *reinterpret_cast<uint4*>(o2);
+                *reinterpret_cast<uint4*>(qd + HHD + c + j) = *reinterpret_cast<uint4*>(o2);
               }
             } else if (kv_ok) {
               const int kv = head < D.qh + D.kvh ? 0 : 1;
@@ -478,8 +494,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 __align__(16) bf16 o1[8], o2[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) { o1[e] = __float2bfloat16_rn(x1[j + e]); o2[e] = __float2bfloat16_rn(x2[j + e]); }
-                *reinterpret_cast<uint4*>(tile + kv_swz<bf16>(sib, c + j, BN)) = *reinterpret_cast<uint4*>(o1);
-                *reinterpret_cast<uint4*>(tile + kv_swz<bf16>(sib, HALF + c + j, BN)) = *reinterpret_cast<uint4*>(o2);
+                *reinterpret_cast<uint4*>(tile + kv_swz<bf16>(sib, i0 + c + j, HD)) = *reinterpret_cast<uint4*>(o1);
+                *reinterpret_cast<uint4*>(tile + kv_swz<bf16>(sib, HHD + i0 + c + j, HD)) = *reinterpret_cast<uint4*>(o2);
               }
             }
           }
@@ -578,7 +594,7 @@ template <int BN, int MODE, int MS = 1>
 bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K, int S,
                cudaStream_t s, const QkvEpi* epi = nullptr, const bf16* Bt = nullptr) {
   const CUtensorMap* ma = g_maps.get(A, M, K, BM);
-  const CUtensorMap* mb = Bt ? ma : g_maps.get(B, N, K, BN);
+  const CUtensorMap* mb = Bt ? ma : g_maps.get(B, N, K, MODE == GEMM_QKV_HALF ? 32 : BN);
   if (!ma || !mb) return false;
   const size_t smem = sizeof(Smem<BN, MS>) + 1024;
   ensure_dyn_smem(k_gemm_tc<BN, MODE, MS>, (int)smem);
@@ -661,6 +677,11 @@ bool launch_gemm_qkv(const bf16* A, const bf16* B, int M, int N, int K, const Qk
     const int smax = smax_env ? smax_env : 1;
     S = wave_split(heads * mt, std::max(1, std::min(smax, std::min(8, kb / 2))));
   }
+  // half-head tiles (2 CTAs per head) when the doubled tile count still fits one wave: C2's
+  // 16 heads x 4 m-tiles = 64 one-head CTAs leave 84 SMs idle.  SART_QKV_HALF=0 disables.
+  static const int half_env = getenv("SART_QKV_HALF") ? atoi(getenv("SART_QKV_HALF")) : 1;
+  if (epi.D.hd == 128 && S == 1 && !Bt && half_env && 2 * heads * mt <= g_num_sms)
+    return launch_bn<64, GEMM_QKV_HALF>(A, B, nullptr, epi.parts, nullptr, M, N, K, 1, s, &epi);
   if (epi.D.hd == 128) return launch_bn<128, GEMM_QKV>(A, B, nullptr, epi.parts, nullptr, M, N, K, S, s, &epi, Bt);
   if (epi.D.hd == 64) return launch_bn<64, GEMM_QKV>(A, B, nullptr, epi.parts, nullptr, M, N, K, S, s, &epi, Bt);
   return false;

@@ -37,7 +37,11 @@ template <typename T> void launch_convert(const float* in, T* out, long long n, 
 template <typename T> void launch_to_f32(const T* in, float* out, long long n, cudaStream_t s);
 
 // ---- GEMM (k_gemm.cu): C[m][n] (+)= A[m][k] . B[n][k]^T (+ bias[n]); fp32 accumulate.
-enum { GEMM_STORE = 0, GEMM_ACCUM = 1, GEMM_SWIGLU = 2, GEMM_QKV = 3 };
+enum { GEMM_STORE = 0, GEMM_ACCUM = 1, GEMM_SWIGLU = 2, GEMM_QKV = 3,
+       // QKV epilogue on half-head tiles (hd = 128, BN = 64): tile (head, p) holds head dims
+       // [32p, 32p + 32) and [64 + 32p, 64 + 32p + 32) -- the rotate-half pairs stay in one tile,
+       // so a head is split over 2 CTAs (2x the CTAs of the one-head tiling at small M)
+       GEMM_QKV_HALF = 4 };
 // QKV epilogue: bias, rotate-half RoPE, q -> qout (bf16), k/v -> paged pool (decode: running
 // rows only; prefill: prefix positions p0 + row)
 struct QkvEpi {

@@ -272,7 +272,7 @@ def test_sampler_full_vocab_1p5b(tau):
     shape = SHAPES["1.5B"].with_layers(2)
     weights = gen_weights(shape, "bf16", std=0.02, root_seed=5)
     seed = 0x5EED_0000_1234
-    steps = 16
+    steps = 24
     g = gpu_engine(shape, "bf16", weights, block_size=64, num_blocks=2048, max_rows=64, max_requests=8,
                    max_prompt=128, T=1, cap=steps + 4, eos_id=EOS, temperature=tau, sampler_seed=seed,
                    debug_capture=True)
