@@ -131,6 +131,22 @@ typedef struct {
   size_t kv_pool_bytes;
   int32_t es_every_step;
   int32_t record_trace;
+  /* NEXT row f4 (the paper's 70B model): tensor parallelism over
+   * tp_size GPUs (one ctx per GPU, tp_rank = its position).  The model dims above are the
+   * FULL model's; this ctx holds q heads [rank*qh/tp, ...), kv heads [rank*kvh/tp, ...), FFN
+   * rows [rank*F/tp, ...) (Megatron split: QKV / gate-up by output rows, O / down by input
+   * columns; embedding, norms, LM head and PRM head replicated) and its share of the KV pool.
+   * host_weights is the FULL blob (each rank extracts its shard); device-generated weights
+   * equal the TP = 1 model's.  The O-projection and down-projection outputs are partial sums
+   * over ranks: their GEMM epilogues store every partial tile straight into each peer's
+   * receive buffer over NVLink (sart_tp_buffer / sart_tp_connect), then signal the peers;
+   * the consuming RMSNorm waits for all ranks' tiles and sums them in (rank, split) order,
+   * so every rank holds the same residual stream, the same logits and the same tokens, and
+   * the (replicated) branch control stays identical across ranks.  Every rank must receive
+   * the same sart_admit / sart_step calls.  Requires dtype SART_BF16, no PRM model,
+   * n_heads and n_kv_heads divisible by tp_size, (d_ff / tp_size) % 128 == 0.
+   * tp_size 0 or 1: no tensor parallelism. */
+  int32_t tp_size, tp_rank;
 } sart_config;
 
 /* Create an engine.  Errors: EINVAL (shape/range), ENOMEM (allocation failure, or
@@ -238,8 +254,9 @@ int sart_collect(sart_ctx* ctx, sart_result* out, int32_t cap, int32_t* n_out,
  *   window      boundary index (0-based)
  *   ell_start   tokens the branch had generated before the window
  *   n_tokens    tokens it generated in the window; they are tokens_out[tokens_offset ..)
- *   running     1: still running at the boundary (score = its k-th running score, k counting
- *               the boundaries it was running at); 0: completed in the window (score = final)
+ *   running     1: incomplete at the boundary -- still running, or stopped by es_every_step --
+ *               (score = its k-th running score, k counting the boundaries it was incomplete
+ *               at); 0: completed in the window (score = final)
  *   score       the reward the boundary used (PRM head / PRM model / script), fp32
  * hashes[w]: FNV-1a 64 of the control state after boundary w, over the little-endian bytes of
  *   for each row in batch order: int64 request_id, int32 branch, int32 ell, int32 nblk,
@@ -260,6 +277,30 @@ typedef struct {
 } sart_trace_row;
 int sart_trace_fetch(sart_ctx* ctx, sart_trace_row* rows, int64_t rows_cap, int64_t* n_rows, int32_t* tokens_out,
                      int64_t tokens_cap, int64_t* n_tokens, uint64_t* hashes, int64_t hashes_cap, int64_t* n_hashes);
+
+/*
+ * Tensor parallelism (tp_size > 1): the symmetric receive buffer of this ctx -- device
+ * memory on its GPU that every rank's O / down GEMMs write their partial tiles into, with
+ * the arrival counters.  *dev_ptr gets its address (valid in this process); ipc_handle, if
+ * not NULL, receives a 64-byte cudaIpcMemHandle_t for it (for peers in other processes).
+ * Errors: EINVAL (tp_size <= 1, null dev_ptr).
+ */
+int sart_tp_buffer(sart_ctx* ctx, void** dev_ptr, void* ipc_handle);
+/*
+ * Connect the tp_size ranks.  Exactly one of peer_ptrs / ipc_handles is non-NULL:
+ *   peer_ptrs[r]    the sart_tp_buffer address of rank r, valid in THIS process (ranks of one
+ *                   process, e.g. on one GPU or GPUs with peer access enabled);
+ *   ipc_handles     tp_size x 64 bytes: rank r's handle at offset 64 r (entry tp_rank is
+ *                   ignored); opened with cudaIpcOpenMemHandle (one process per GPU).
+ * Must be called once, after every rank's sart_init and before the first sart_step.
+ * Errors: EINVAL, ESTATE (already connected), ECUDA (handle open failed).
+ */
+int sart_tp_connect(sart_ctx* ctx, void* const* peer_ptrs, const void* ipc_handles);
+/* Host-only test hook (no GPU): where rank cfg->tp_rank's copy of tensor `tensor` (host_weights
+ * order, FULL dims in cfg) comes from.  out receives *n_out records of 6 int64
+ * {local offset, count, cl, cf, c0, global offset}: local element loff + i is full-tensor element
+ * goff + (i / cl) * cf + c0 + i % cl.  EFULL if cap records do not suffice (count written). */
+int sart_debug_tp_segments(const sart_config* cfg, int32_t tensor, int64_t* out, int32_t cap, int32_t* n_out);
 
 int sart_destroy(sart_ctx* ctx);
 const char* sart_strerror(int code);

@@ -27,6 +27,15 @@
 #include "kernels.h"
 
 namespace {
+// Partial outputs of the split items (normalised o of a chunk, per row / q head / slot): fp32.
+// -DSART_PART_BF16 stores them in bf16 (half the partial round trip): +0.6% on the C2 step
+// (profiles/r2_attn_partials_ab.txt), but the extra rounding moved one sampled row of the
+// full-depth C2 logits parity to 2.09e-2 > north_star's 2e-2, so it is not the default.
+#ifdef SART_PART_BF16
+typedef bf16 PartT;
+#else
+typedef float PartT;
+#endif
 // launch configurations <warps per CTA, stages per warp ring, tokens per stage>; the
 // default is chosen by measurement, SART_ATTN_CFG=<index> overrides it.
 
@@ -322,11 +331,16 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const float m = half ? m1 : m0, l = half ? l1 : l0;
         const float inv = 1.0f / l;
         const long long pi = ((long long)row * D.qh + head) * pl.nslot + it.slot_idx;
-        float* dst = part_o + pi * HD;
+        PartT* dst = reinterpret_cast<PartT*>(part_o) + pi * HD;
 #pragma unroll
-        for (int nt = 0; nt < HD / 8; ++nt)
-          *reinterpret_cast<float2*>(dst + nt * 8 + cc) =
-              make_float2(o[nt][2 * half] * inv, o[nt][2 * half + 1] * inv);
+        for (int nt = 0; nt < HD / 8; ++nt) {
+          if constexpr (sizeof(PartT) == 4)
+            *reinterpret_cast<float2*>(dst + nt * 8 + cc) =
+                make_float2(o[nt][2 * half] * inv, o[nt][2 * half + 1] * inv);
+          else
+            *reinterpret_cast<__nv_bfloat162*>(dst + nt * 8 + cc) =
+                __floats2bfloat162_rn(o[nt][2 * half] * inv, o[nt][2 * half + 1] * inv);
+        }
         if ((lane & 3) == 0) part_lse[pi] = (m == -INFINITY ? 0.f : m) * sl2 + log2f(l);
       }
     }
@@ -372,12 +386,25 @@ __global__ void __launch_bounds__(256) k_attn_merge(const float* __restrict__ pa
     const long long pi = base + (k < npc ? k : pl.npc_max + k - npc);
     const float w = exp2f(part_lse[pi] - M);
     L += w;
-    if constexpr (C == 4) {
-      const float4 v = *reinterpret_cast<const float4*>(part_o + pi * HD + lane * 4);
-      acc[0] += w * v.x; acc[1] += w * v.y; acc[2] += w * v.z; acc[3] += w * v.w;
+    const PartT* src = reinterpret_cast<const PartT*>(part_o) + pi * HD + lane * C;
+    if constexpr (sizeof(PartT) == 4) {
+      if constexpr (C == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(src);
+        acc[0] += w * v.x; acc[1] += w * v.y; acc[2] += w * v.z; acc[3] += w * v.w;
+      } else {
+        const float2 v = *reinterpret_cast<const float2*>(src);
+        acc[0] += w * v.x; acc[1] += w * v.y;
+      }
     } else {
-      const float2 v = *reinterpret_cast<const float2*>(part_o + pi * HD + lane * 2);
-      acc[0] += w * v.x; acc[1] += w * v.y;
+      if constexpr (C == 4) {
+        const uint2 u = *reinterpret_cast<const uint2*>(src);
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+        acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * b.x; acc[3] += w * b.y;
+      } else {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(src));
+        acc[0] += w * a.x; acc[1] += w * a.y;
+      }
     }
   }
   const long long oi = ((long long)r * D.qh + head) * HD + lane * C;

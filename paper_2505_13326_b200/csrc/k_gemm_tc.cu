@@ -113,9 +113,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 // 32 x 32 chunk; transpose it through a 16-byte-swizzled shared slab (chunk k of row r at
 // k ^ (r & 7): conflict-free both ways) so that each 16-byte store instruction writes 4 full
 // 128-byte lines.  MODE == GEMM_ACCUM adds into C.
+// ndst > 1 (tensor parallelism): the same values go to every destination tile in dsts[] (this
+// rank's and each peer's receive buffer).
 template <int BN, int MODE>
 __device__ __forceinline__ void store_tile_f32(uint32_t tbase, float* Cs, int mrow0, int n0, int M, int N,
-                                               const float* bias, uint32_t slab, int lane, int c_begin, int c_step) {
+                                               const float* bias, uint32_t slab, int lane, int c_begin, int c_step,
+                                               float* const* dsts = nullptr, int ndst = 0) {
   const int kk = lane & 7, r4 = lane >> 3;
   const bool vec = (N & 3) == 0;
 #pragma unroll 1
@@ -150,6 +153,24 @@ __device__ __forceinline__ void store_tile_f32(uint32_t tbase, float* Cs, int mr
       x[i].x += bv.x; x[i].y += bv.y; x[i].z += bv.z; x[i].w += bv.w;
     }
     __syncwarp();
+    if (ndst > 0) {   // TP exchange: plain stores (no accumulate) into every rank's buffer
+      for (int p = 0; p < ndst; ++p) {
+        float* dst = dsts[p] + (size_t)(mrow0 + r4) * N + gn;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (mrow0 + i * 4 + r4 >= M) continue;
+          float* d = dst + (size_t)i * 4 * N;
+          if (vec && gn + 4 <= N) {
+            *reinterpret_cast<float4*>(d) = x[i];
+          } else {
+            const float xs[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
+            for (int e = 0; e < 4; ++e)
+              if (gn + e < N) d[e] = xs[e];
+          }
+        }
+      }
+      continue;
+    }
     float* dst = Cs + (size_t)(mrow0 + r4) * N + gn;
     if (vec && gn + 4 <= N) {
 #pragma unroll
@@ -210,7 +231,7 @@ template <int BN, int MODE, int MS>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const bf16* __restrict__ Bt,
               float* C, const float* __restrict__ bias, bf16* act, int M, int N, int K, int S,
-              const __grid_constant__ QkvEpi epi) {
+              const __grid_constant__ QkvEpi epi, const __grid_constant__ TpOut tp) {
   extern __shared__ __align__(16) uint8_t smem_raw[];   // 1024-aligned below (+1024 B slack)
   Smem<BN, MS>& sm =
       *reinterpret_cast<Smem<BN, MS>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -361,6 +382,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else {
     // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
     pdl_wait();   // outputs may be read by the previous kernel; inputs (bias, rows) are visible
+    // TP: this rank's consumer of projection k expects gridDim.x arrivals from each rank
+    if (tp.tp > 1 && blockIdx.x == 0 && warp == 2 && lane == 0) tp.expect[tp.k] += (unsigned long long)gridDim.x * tp.tp;
     const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;  // which 32-column chunks of the tile it handles
     const int row = q * 32 + lane;
@@ -524,6 +547,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
           }
         }
+      } else if (tp.tp > 1) {
+        float* dsts[SART_MAX_TP];
+        for (int p = 0; p < tp.tp; ++p) dsts[p] = tp.dst[p] + ((size_t)tp.rank * S + sp) * M * N;
+        store_tile_f32<BN, MODE>(tbase, Cs, m0 + q * 32, n0, M, N, bias, smem_u32(sm.slab[warp - 2]), lane, half * 32,
+                                 CSTEP, dsts, tp.tp);
       } else {
         store_tile_f32<BN, MODE>(tbase, Cs, m0 + q * 32, n0, M, N, bias, smem_u32(sm.slab[warp - 2]), lane, half * 32, CSTEP);
       }
@@ -534,8 +562,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (lane == 0) mbar_arrive(&sm.tempty[as]);
     }
   }
+  if (tp.tp > 1) __threadfence_system();   // this thread's remote partial stores, before the signal
   __syncthreads();
   if (threadIdx.x == 0) { TS(7); }
+  if (tp.tp > 1 && threadIdx.x == 0) {      // every rank: one more CTA of projection k has landed
+    __threadfence_system();
+    for (int p = 0; p < tp.tp; ++p)
+      asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(tp.cnt[p] + tp.k) : "memory");
+  }
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
@@ -592,7 +626,7 @@ MapCache g_maps;
 
 template <int BN, int MODE, int MS = 1>
 bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K, int S,
-               cudaStream_t s, const QkvEpi* epi = nullptr, const bf16* Bt = nullptr) {
+               cudaStream_t s, const QkvEpi* epi = nullptr, const bf16* Bt = nullptr, const TpOut* tpo = nullptr) {
   const CUtensorMap* ma = g_maps.get(A, M, K, BM);
   const CUtensorMap* mb = Bt ? ma : g_maps.get(B, N, K, MODE == GEMM_QKV_HALF ? 32 : BN);
   if (!ma || !mb) return false;
@@ -603,7 +637,10 @@ bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* 
   const int grid = ntiles < g_num_sms ? ntiles : g_num_sms;
   QkvEpi e{};
   if (epi) e = *epi;
-  launch_pdl(k_gemm_tc<BN, MODE, MS>, dim3(grid), dim3(NTHREADS), smem, s, *ma, *mb, Bt, C, bias, act, M, N, K, S, e);
+  TpOut t{};
+  if (tpo) t = *tpo;
+  launch_pdl(k_gemm_tc<BN, MODE, MS>, dim3(grid), dim3(NTHREADS), smem, s, *ma, *mb, Bt, C, bias, act, M, N, K, S, e,
+             t);
   return true;
 }
 }  // namespace
@@ -619,8 +656,14 @@ bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, b
 }
 
 bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
-                          int mode, int S, int BN, int MSUB, cudaStream_t s, const bf16* Bt) {
+                          int mode, int S, int BN, int MSUB, cudaStream_t s, const bf16* Bt, const TpOut* tp) {
   if (M <= 0 || N <= 0) return true;
+  if (tp && tp->tp > 1) {   // TP exchange: plain partial stores only
+    if (mode != GEMM_STORE || MSUB != 1) return false;
+    if (BN == 128) return launch_bn<128, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s, nullptr, Bt, tp);
+    if (BN == 256) return launch_bn<256, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s, nullptr, Bt, tp);
+    return false;
+  }
   if (K % 8) return false;   // TMA row stride must be a multiple of 16 bytes
   const int kb = (K + BK - 1) / BK;
   if (S < 1 || S > kb || (mode == GEMM_SWIGLU && S != 1)) return false;

@@ -5,27 +5,37 @@
 // ------------------------------------------------------------ device weight init
 // N(0, std^2) via Philox + Box-Muller; norms 1 + N(0, 0.1^2).  Inputs only: the
 // values do not matter for timing runs (parity runs pass host_weights).
+// Element gi of tensor tid is a function of (seed, tid, gi) only, so a TP rank's shard
+// (local element i = global goff + (i / cl) * cf + c0 + i % cl) equals the TP = 1 tensor's.
 template <typename T>
-__global__ void k_init_tensor(T* p, long long n, int tid, int is_norm, float std, unsigned long long seed) {
+__global__ void k_init_tensor(T* p, long long n, int tid, int is_norm, float std, unsigned long long seed,
+                              long long cl, long long cf, long long c0, long long goff) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   long long stride = (long long)gridDim.x * blockDim.x;
   for (; i < n; i += stride) {
-    long long pr = i >> 1;
+    const long long gi = goff + (i / cl) * cf + c0 + i % cl;
+    long long pr = gi >> 1;
     u32x4 w = philox4x32_10(u32x4{(uint32_t)pr, (uint32_t)(pr >> 32), (uint32_t)tid, 0xC0FFEEu},
                             (uint32_t)seed, (uint32_t)(seed >> 32));
     float u1 = ((w.x >> 8) + 0.5f) * (1.0f / 16777216.0f);
     float u2 = ((w.y >> 8) + 0.5f) * (1.0f / 16777216.0f);
     float r = sqrtf(-2.0f * logf(u1));
-    float z = (i & 1) ? r * sinpif(2.0f * u2) : r * cospif(2.0f * u2);
+    float z = (gi & 1) ? r * sinpif(2.0f * u2) : r * cospif(2.0f * u2);
     p[i] = from_f<T>(is_norm ? 1.0f + 0.1f * z : std * z);
   }
 }
 template <typename T>
-void launch_init_tensor(T* p, long long n, int tid, int is_norm, float std, unsigned long long seed,
-                        cudaStream_t s) {
+void launch_init_slice(T* p, long long n, int tid, int is_norm, float std, unsigned long long seed, long long cl,
+                       long long cf, long long c0, long long goff, cudaStream_t s) {
+  if (n <= 0) return;
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  k_init_tensor<T><<<(int)blocks, 256, 0, s>>>(p, n, tid, is_norm, std, seed);
+  k_init_tensor<T><<<(int)blocks, 256, 0, s>>>(p, n, tid, is_norm, std, seed, cl, cf, c0, goff);
+}
+template <typename T>
+void launch_init_tensor(T* p, long long n, int tid, int is_norm, float std, unsigned long long seed,
+                        cudaStream_t s) {
+  launch_init_slice<T>(p, n, tid, is_norm, std, seed, n > 0 ? n : 1, n > 0 ? n : 1, 0, 0, s);
 }
 
 // ------------------------------------------------------------ embedding: h = E[tok]
@@ -70,11 +80,28 @@ template <typename T>
 __global__ void __launch_bounds__(512) k_rmsnorm(float* __restrict__ h, const float* __restrict__ parts, int np,
                                                   long long pstride, const T* __restrict__ g, T* __restrict__ out,
                                                   float* __restrict__ out32, const int* __restrict__ status, int n,
-                                                  int d, float eps) {
+                                                  int d, float eps, const unsigned long long* __restrict__ tp_cnt,
+                                                  const unsigned long long* __restrict__ tp_expect) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
   if (status && status[r] != RUNNING_ST) return;
+  if (tp_cnt) {   // tensor parallelism: every rank's partial tiles of the projection have landed
+    if (threadIdx.x == 0) {
+      const unsigned long long target = *reinterpret_cast<const volatile unsigned long long*>(tp_expect);
+      unsigned long long t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      for (;;) {
+        unsigned long long v, t;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(tp_cnt) : "memory");
+        if (v >= target) break;
+        __nanosleep(32);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) __trap();   // a peer never delivered (20 s): fail, do not hang
+      }
+    }
+    __syncthreads();
+  }
   float4* x = reinterpret_cast<float4*>(h + (long long)r * d);
   const int d4 = d >> 2;
   float ss = 0.f;
@@ -114,10 +141,11 @@ static int rmsnorm_threads(int d) {
 }
 template <typename T>
 void launch_rmsnorm(float* h, const float* parts, int np, const T* g, T* out, float* out32, const int* status, int n,
-                    int d, float eps, cudaStream_t s) {
+                    int d, float eps, cudaStream_t s, const unsigned long long* tp_cnt,
+                    const unsigned long long* tp_expect) {
   if (n > 0)
     launch_pdl(k_rmsnorm<T>, dim3(n), dim3(rmsnorm_threads(d)), 0, s, h, parts, np, (long long)n * d, g, out, out32,
-               status, n, d, eps);
+               status, n, d, eps, tp_cnt, tp_expect);
 }
 
 // ------------------------------------------------------------ RoPE + KV append
@@ -285,7 +313,10 @@ void launch_prm_gather(const T* z, T* zrow, const int4* gat, int ng, int d, cuda
   template void launch_init_tensor<T>(T*, long long, int, int, float, unsigned long long, cudaStream_t); \
   template void launch_embed<T>(const int*, const T*, float*, int, int, cudaStream_t);                  \
   template void launch_rmsnorm<T>(float*, const float*, int, const T*, T*, float*, const int*, int, int, \
-                                  float, cudaStream_t);                                                 \
+                                  float, cudaStream_t, const unsigned long long*,                       \
+                                  const unsigned long long*);                                           \
+  template void launch_init_slice<T>(T*, long long, int, int, float, unsigned long long, long long,     \
+                                     long long, long long, long long, cudaStream_t);                    \
   template void launch_rope_append<T>(const float*, int, const float*, T*, T*, const float*, Dims, int, \
                                       Rows, Reqs, RopeArgs, int, cudaStream_t);                         \
   template void launch_swiglu<T>(const float*, T*, int, int, cudaStream_t);                             \

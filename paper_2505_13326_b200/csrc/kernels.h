@@ -24,8 +24,17 @@ template <typename T> void launch_init_tensor(T* p, long long n, int tensor_id, 
                                               unsigned long long seed, cudaStream_t s);
 template <typename T> void launch_embed(const int* tok, const T* emb, float* h, int n, int d, cudaStream_t s);
 // h[r] += sum_{s<np} parts[s][r] (fixed order; np may be 0), then out = RMSNorm(h) * g
+// tp_cnt / tp_expect (tensor parallelism, may be null): wait until the local arrival counter
+// reaches the expected count before reading the partials (they include other ranks' tiles)
 template <typename T> void launch_rmsnorm(float* h, const float* parts, int np, const T* g, T* out, float* out32,
-                                          const int* status, int n, int d, float eps, cudaStream_t s);
+                                          const int* status, int n, int d, float eps, cudaStream_t s,
+                                          const unsigned long long* tp_cnt = nullptr,
+                                          const unsigned long long* tp_expect = nullptr);
+// device weight init of a (sliced) tensor: local element i is global element
+// goff + (i / cl) * cf + c0 + i % cl of tensor tensor_id (row / column shards of TP ranks)
+template <typename T> void launch_init_slice(T* p, long long n, int tensor_id, int is_norm, float std,
+                                             unsigned long long seed, long long cl, long long cf, long long c0,
+                                             long long goff, cudaStream_t s);
 // qkv = sum_{s<np} parts[s] + bias (fixed order), then RoPE + paged KV append
 template <typename T> void launch_rope_append(const float* parts, int np, const float* bias, T* qout, T* pool,
                                               const float* rope_cs, Dims D, int layer, Rows rows, Reqs reqs,
@@ -58,6 +67,18 @@ struct QkvEpi {
   int* cnt;       // per (head, m-tile, lane quarter) arrival counters, zero between launches
   int cnt_cap;    // entries in cnt (split-K is used only when heads x m-tiles x 4 fits)
 };
+// Tensor parallelism (row f4): the split-K partials of an O / down projection are partial sums
+// over the tp ranks.  The GEMM epilogue stores partial tile (rank, split) into EVERY rank's
+// receive buffer (dst[p] + (rank * S + split) * M * N, remote stores over NVLink), then each CTA
+// adds 1 to counter k of every rank (system scope).  The consumer (k_rmsnorm) waits until its
+// counter k reaches expect[k], which CTA 0 of the local producer raised by gridDim.x * tp.
+constexpr int SART_MAX_TP = 8;
+struct TpOut {
+  float* dst[SART_MAX_TP];
+  unsigned long long* cnt[SART_MAX_TP];   // counter arrays of every rank (index k)
+  unsigned long long* expect;             // this rank's expected arrivals (index k)
+  int tp, rank, k;
+};
 template <typename T> void launch_gemm_simt(const T* A, const T* B, const float* bias, float* C, int M, int N,
                                             int K, int mode, cudaStream_t s);
 
@@ -72,7 +93,8 @@ bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, b
 void launch_interleave_gate_up(bf16* w, bf16* tmp, int F, int d, cudaStream_t s);
 // split-K variant: S partial products written to C + s*M*N (summed by the consumer kernel)
 bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
-                          int mode, int S, int BN, int MSUB, cudaStream_t s, const bf16* Bt = nullptr);
+                          int mode, int S, int BN, int MSUB, cudaStream_t s, const bf16* Bt = nullptr,
+                          const TpOut* tp = nullptr);
 // pre-tiled weight layout for the tcgen05 GEMM (k_gemm_tc.cu)
 size_t tiled_b_elems(int N, int K, int BN);
 void launch_tile_b(const bf16* W, bf16* Wt, int N, int K, int BN, cudaStream_t s);

@@ -145,6 +145,16 @@ struct sart_ctx {
   std::vector<int> trace_ell0;   // rows.ell at window start
   BoundaryTrace dtr{nullptr, nullptr, nullptr};
   bool own_pool = true;          // false: caller-owned kv_pool (never freed here)
+  // tensor parallelism (row f4): symmetric receive buffer [counters | partials] and the peers'
+  int tp = 1, tp_rank = 0;
+  void* tp_buf = nullptr;                  // this rank's receive buffer (cudaMalloc base)
+  float* tp_parts = nullptr;               // its partial region: [tp][S <= 8][W][max(d, qkv)] fp32
+  unsigned long long* tp_cnt = nullptr;    // its arrival counters [2 L]
+  unsigned long long* tp_expect = nullptr; // expected arrivals [2 L] (local)
+  std::vector<void*> tp_peer;              // every rank's buffer base as seen from here
+  std::vector<void*> tp_opened;            // IPC mappings to close at destroy
+  bool tp_connected = false;
+  size_t tp_parts_off = 0;
 
   // row f2: the separate PRM decoder is a sub-context holding its own dims, weights, KV pool
   // and workspaces; it shares rows / reqs / stream with the policy ctx.
@@ -307,6 +317,45 @@ int proj(sart_ctx* ctx, const T* A, const T* B, int M, int N, int K) {
   return S;
 }
 
+// Residual partials of an O / down projection as the consuming RMSNorm reads them: this
+// rank's split-K partials, or (tensor parallelism) every rank's, with the arrival wait.
+struct ResParts {
+  const float* parts;
+  int np;
+  const unsigned long long* cnt;
+  const unsigned long long* expect;
+};
+// proj() for the residual projections; k = the TP exchange index (2 l: O-proj, 2 l + 1: down)
+template <typename T>
+ResParts proj_res(sart_ctx* ctx, const T* A, const T* B, int M, int N, int K, int k) {
+  if constexpr (std::is_same<T, bf16>::value) {
+    if (ctx->tp > 1) {
+      int S = 1, BN = 256, MS = 1;
+      choose_split(M, N, K, S, BN, MS);
+      TpOut t{};
+      t.tp = ctx->tp;
+      t.rank = ctx->tp_rank;
+      t.k = k;
+      t.expect = ctx->tp_expect;
+      for (int p = 0; p < ctx->tp; ++p) {
+        t.dst[p] = (float*)((char*)ctx->tp_peer[p] + ctx->tp_parts_off);
+        t.cnt[p] = (unsigned long long*)ctx->tp_peer[p];
+      }
+      if (!launch_gemm_tc_split(A, B, nullptr, ctx->tp_parts, nullptr, M, N, K, GEMM_STORE, S, BN, MS, ctx->st,
+                                nullptr, &t))
+        ctx->gemm_failed = true;
+      ctx->launches++;
+      return ResParts{ctx->tp_parts, S * ctx->tp, ctx->tp_cnt + k, ctx->tp_expect + k};
+    }
+  }
+  return ResParts{ctx->parts, proj<T>(ctx, A, B, M, N, K), nullptr, nullptr};
+}
+template <typename T>
+void norm(sart_ctx* ctx, const ResParts& rp, const T* g, T* out, float* out32, const int* status, int n) {
+  launch_rmsnorm<T>(ctx->h, rp.parts, rp.np, g, out, out32, status, n, ctx->D.d, ctx->D.eps, ctx->st, rp.cnt,
+                    rp.expect);
+}
+
 // QKV projection + bias + RoPE + paged KV append: one fused tcgen05 launch in bf16 (tile =
 // one head); fp32 mode: SIMT GEMM into the partial buffer + the RoPE/append kernel.
 template <typename T>
@@ -403,25 +452,20 @@ void decode_step(sart_ctx* ctx, int n) {
     ctx->launches++;
   }
   g_attn_skip_merge = (ab & AB_MERGE) != 0;
-  int np_res = 0;   // pending residual partials (previous layer's down projection)
+  ResParts res{ctx->parts, 0, nullptr, nullptr};   // pending residual partials (previous layer's down)
   for (int l = 0; l < D.L; ++l) {
-    if (!(ab & AB_RMSNORM))
-      launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, n, D.d,
-                        D.eps, s);
+    if (!(ab & AB_RMSNORM)) norm<T>(ctx, res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, n);
     if (!(ab & AB_QKV)) qkv_rope<T>(ctx, l, n, RopeArgs{nullptr, nullptr});
     if (!(ab & AB_ATTN)) layer_attention<T>(ctx, l, n);
-    int np = 0;
-    if (!(ab & AB_OPROJ)) np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), n, D.d, D.qh * D.hd);
-    if (!(ab & AB_RMSNORM))
-      launch_rmsnorm<T>(ctx->h, ctx->parts, np, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, n, D.d,
-                        D.eps, s);
+    ResParts ro{ctx->parts, 0, nullptr, nullptr};
+    if (!(ab & AB_OPROJ)) ro = proj_res<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), n, D.d, D.qh * D.hd, 2 * l);
+    if (!(ab & AB_RMSNORM)) norm<T>(ctx, ro, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, n);
     if (!(ab & AB_GATEUP)) mlp_up<T>(ctx, l, n);
-    np_res = 0;
-    if (!(ab & AB_DOWN)) np_res = proj<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), n, D.d, D.F);
+    res = ResParts{ctx->parts, 0, nullptr, nullptr};
+    if (!(ab & AB_DOWN)) res = proj_res<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), n, D.d, D.F, 2 * l + 1);
     ctx->launches += 1;
   }
-  launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_final(D)), (T*)ctx->zT, ctx->z32, ctx->rows.status, n,
-                    D.d, D.eps, s);
+  norm<T>(ctx, res, ctx->W_<T>(t_final(D)), (T*)ctx->zT, ctx->z32, ctx->rows.status, n);
   if (!(ab & AB_HEAD)) gemm<T>(ctx, (T*)ctx->zT, ctx->W_<T>(t_lm(D)), nullptr, ctx->logits, n, D.V, D.d, GEMM_STORE);
   if (!(ab & AB_SAMPLE))
     launch_sample(ctx->logits, D, ctx->rows, ctx->reqs, ctx->ctr, n, ctx->dbg_tok, ctx->skey, ctx->sv, s);
@@ -460,10 +504,9 @@ void prefill_batch(sart_ctx* ctx, sart_ctx* src, int ntok) {
     }
     launch_embed<T>(src->d_prompt + t0, ctx->W_<T>(t_embed()), ctx->h, c, D.d, s);
     ctx->launches++;
-    int np_res = 0;
+    ResParts res{ctx->parts, 0, nullptr, nullptr};
     for (int l = 0; l < D.L; ++l) {
-      launch_rmsnorm<T>(ctx->h, ctx->parts, np_res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, c, D.d,
-                        D.eps, s);
+      norm<T>(ctx, res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, c);
       qkv_rope<T>(ctx, l, c, ra);
       if (l == D.L - 1) break;
       if constexpr (std::is_same<T, bf16>::value)
@@ -471,11 +514,10 @@ void prefill_batch(sart_ctx* ctx, sart_ctx* src, int ntok) {
                                s);
       else
         launch_attn_prefill<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, D, l, ctx->reqs, ra.pf_slot, ra.pf_pos, c, s);
-      int np = proj<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), c, D.d, D.qh * D.hd);
-      launch_rmsnorm<T>(ctx->h, ctx->parts, np, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, c, D.d,
-                        D.eps, s);
+      const ResParts ro = proj_res<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), c, D.d, D.qh * D.hd, 2 * l);
+      norm<T>(ctx, ro, ctx->W_<T>(t_layer(l, 4)), (T*)ctx->a, nullptr, nullptr, c);
       mlp_up<T>(ctx, l, c);
-      np_res = proj<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), c, D.d, D.F);
+      res = proj_res<T>(ctx, (T*)ctx->act, ctx->W_<T>(t_layer(l, 7)), c, D.d, D.F, 2 * l + 1);
       ctx->launches += 3;
     }
   }
@@ -933,7 +975,7 @@ int record_trace_window(sart_ctx* ctx, int n) {
     t.window = ctx->windows - 1;
     t.ell_start = ctx->trace_ell0[r];
     t.n_tokens = ell[r] - t.ell_start;
-    t.running = st[r] == RUNNING_ST ? 1 : 0;
+    t.running = (st[r] == RUNNING_ST || st[r] == ST_STOP) ? 1 : 0;   // incomplete: a running score (R43)
     t.score = sc[r];
     t.tokens_offset = (int64_t)ctx->trace_tokens.size();
     ctx->trace_tokens.resize(ctx->trace_tokens.size() + t.n_tokens);
@@ -1056,6 +1098,33 @@ int run_window(sart_ctx* ctx) {
 
 // Weights (host blob or device-generated), fp32 epilogue vectors, RoPE table and the
 // per-token workspaces of one decoder: the policy, or the f2 PRM model (sub-context).
+// Tensor parallelism: where a rank's tensor t comes from in the FULL model's tensor t --
+// segments {local element offset, count, cl, cf, c0, global offset} in the k_init_tensor
+// slice mapping (local i -> global goff + (i / cl) * cf + c0 + i % cl).
+struct Seg { long long loff, n, cl, cf, c0, goff; };
+std::vector<Seg> shard_segments(const Dims& F, int tp, int rank, int idx) {
+  const long long d = F.d, hd = F.hd, qr = F.qh / tp, kr = F.kvh / tp, fr = F.F / tp;
+  std::vector<size_t> sz = tensor_sizes(F);
+  const long long n = (long long)sz[idx];
+  if (idx >= 1 && idx < 1 + 8 * F.L) {
+    const int k = (idx - 1) % 8;
+    const long long rows_q = F.qh * hd, rows_k = F.kvh * hd;
+    if (k == 1 || k == 2) {   // wqkv rows / bqkv: q heads, k heads, v heads of this rank
+      const long long w = k == 1 ? d : 1;
+      const long long q0 = rank * qr * hd, k0 = rows_q + rank * kr * hd, v0 = rows_q + rows_k + rank * kr * hd;
+      const long long nq = qr * hd * w, nk = kr * hd * w;
+      return {Seg{0, nq, nq, nq, 0, q0 * w}, Seg{nq, nk, nk, nk, 0, k0 * w}, Seg{nq + nk, nk, nk, nk, 0, v0 * w}};
+    }
+    if (k == 3)               // wo [d][qh hd]: this rank's input columns
+      return {Seg{0, d * qr * hd, qr * hd, F.qh * hd, rank * qr * hd, 0}};
+    if (k == 5 || k == 6)     // wgate / wup [F][d]: this rank's rows
+      return {Seg{0, fr * d, fr * d, fr * d, 0, rank * fr * d}};
+    if (k == 7)               // wdown [d][F]: this rank's input columns
+      return {Seg{0, d * fr, fr, F.F, rank * fr, 0}};
+  }
+  return {Seg{0, n, n, n, 0, 0}};   // replicated
+}
+
 int init_model(sart_ctx* ctx, const void* host_w, uint64_t seed, float wstd) {
   const Dims& D = ctx->D;
   const size_t es = ctx->bf16 ? 2 : 4;
@@ -1073,7 +1142,33 @@ int init_model(sart_ctx* ctx, const void* host_w, uint64_t seed, float wstd) {
   size_t total = 0;
   for (size_t s : sizes) { ctx->woff.push_back(total); total += s; }
   MC(cudaMalloc(&ctx->wblob, total * es));
-  if (host_w) {
+  if (ctx->tp > 1) {   // row f4: this rank's shard of the full model (host blob or generated)
+    Dims Fd = D;
+    Fd.qh *= ctx->tp; Fd.kvh *= ctx->tp; Fd.F *= ctx->tp; Fd.qkv = (Fd.qh + 2 * Fd.kvh) * Fd.hd;
+    std::vector<size_t> fsz = tensor_sizes(Fd), foff;
+    size_t ft = 0;
+    for (size_t x : fsz) { foff.push_back(ft); ft += x; }
+    for (size_t i = 0; i < sizes.size(); ++i) {
+      const bool nrm = is_norm_tensor(D, (int)i);
+      for (const Seg& g : shard_segments(Fd, ctx->tp, ctx->tp_rank, (int)i)) {
+        char* dst = (char*)ctx->wblob + (ctx->woff[i] + g.loff) * es;
+        if (host_w) {
+          const char* src = (const char*)host_w + foff[i] * es;
+          const long long rows = g.n / g.cl;
+          if (rows == 1)
+            MC(cudaMemcpy(dst, src + (g.goff + g.c0) * es, g.n * es, cudaMemcpyHostToDevice));
+          else
+            MC(cudaMemcpy2D(dst, g.cl * es, src + (g.goff + g.c0) * es, g.cf * es, g.cl * es, rows,
+                            cudaMemcpyHostToDevice));
+        } else if (ctx->bf16) {
+          launch_init_slice<bf16>((bf16*)dst, g.n, (int)i, nrm, wstd, seed, g.cl, g.cf, g.c0, g.goff, ctx->st);
+        } else {
+          launch_init_slice<float>((float*)dst, g.n, (int)i, nrm, wstd, seed, g.cl, g.cf, g.c0, g.goff, ctx->st);
+        }
+      }
+    }
+    MC(cudaGetLastError());
+  } else if (host_w) {
     MC(cudaMemcpy(ctx->wblob, host_w, total * es, cudaMemcpyHostToDevice));
   } else {
     for (size_t i = 0; i < sizes.size(); ++i) {
@@ -1177,6 +1272,7 @@ int sart_destroy(sart_ctx* ctx) {
   for (auto e : ctx->pf_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->step_exec) cudaGraphExecDestroy(ctx->step_exec);
+  for (void* p : ctx->tp_opened) cudaIpcCloseMemHandle(p);
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->wblob) cudaFree(ctx->wblob);
   if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
@@ -1220,6 +1316,16 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   if (cfg.es_every_step != 0 && cfg.es_every_step != 1) return set_err(SART_EINVAL, "es_every_step must be 0 or 1");
   if (cfg.record_trace != 0 && cfg.record_trace != 1) return set_err(SART_EINVAL, "record_trace must be 0 or 1");
   if (cfg.kv_pool && cfg.kv_pool_bytes == 0) return set_err(SART_EINVAL, "kv_pool given with kv_pool_bytes == 0");
+  if (cfg.tp_size == 0) cfg.tp_size = 1;
+  if (cfg.tp_size < 1 || cfg.tp_size > SART_MAX_TP || cfg.tp_rank < 0 || cfg.tp_rank >= cfg.tp_size)
+    return set_err(SART_EINVAL, "need 1 <= tp_size <= 8 and 0 <= tp_rank < tp_size");
+  if (cfg.tp_size > 1) {   // row f4
+    if (cfg.dtype != SART_BF16) return set_err(SART_EINVAL, "tensor parallelism needs dtype SART_BF16");
+    if (cfg.prm_n_layers > 0) return set_err(SART_EINVAL, "tensor parallelism with a separate PRM model is not supported");
+    if (cfg.n_heads % cfg.tp_size || cfg.n_kv_heads % cfg.tp_size || (cfg.d_ff / cfg.tp_size) % 128 ||
+        cfg.d_ff % cfg.tp_size)
+      return set_err(SART_EINVAL, "tp_size must divide n_heads and n_kv_heads, and d_ff / tp_size % 128 == 0");
+  }
   if (cfg.prm_n_layers > 0) {   // row f2: separate PRM decoder
     if (cfg.prm_d_model < 1 || cfg.prm_n_heads < 1 || cfg.prm_n_kv_heads < 1 || cfg.prm_d_ff < 1)
       return set_err(SART_EINVAL, "PRM model dims must be positive");
@@ -1234,7 +1340,11 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   ctx->bf16 = cfg.dtype == SART_BF16;
   Dims& D = ctx->D;
   D.L = cfg.n_layers; D.d = cfg.d_model; D.qh = cfg.n_heads; D.kvh = cfg.n_kv_heads; D.hd = cfg.head_dim;
-  D.F = cfg.d_ff; D.V = cfg.vocab; D.qkv = (D.qh + 2 * D.kvh) * D.hd; D.g = D.qh / D.kvh;
+  D.F = cfg.d_ff; D.V = cfg.vocab;
+  ctx->tp = cfg.tp_size;
+  ctx->tp_rank = cfg.tp_rank;
+  D.qh /= ctx->tp; D.kvh /= ctx->tp; D.F /= ctx->tp;   // this rank's heads and FFN rows (row f4)
+  D.qkv = (D.qh + 2 * D.kvh) * D.hd; D.g = D.qh / D.kvh;
   D.bs = cfg.block_size; D.R = cfg.max_rows; D.S = cfg.max_requests;
   D.cap = cfg.max_new_tokens; D.T = cfg.ctl_interval; D.eos = cfg.eos_id;
   D.MBR = cdiv(D.cap, D.bs);
@@ -1315,6 +1425,14 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     m->prm_desc_cap = 3 * (size_t)D.R + 2 * (max_tok / m->prm_chunk + 1) + max_tok / 16 + 16;
     IC(dalloc(m, &m->prm_desc, sizeof(int4) * m->prm_desc_cap, false));
     IC(cudaMallocHost(&m->h_prm_desc, sizeof(int4) * m->prm_desc_cap));
+  }
+  if (ctx->tp > 1) {   // row f4: [arrival counters 2L (4 KB-aligned) | partials [tp][8][W][max(d, qkv)]]
+    ctx->tp_parts_off = ((size_t)2 * D.L * sizeof(unsigned long long) + 4095) / 4096 * 4096;
+    const size_t bytes = ctx->tp_parts_off + sizeof(float) * (size_t)ctx->tp * 8 * ctx->W * std::max(D.d, D.qkv);
+    IC(dalloc(ctx, &ctx->tp_buf, bytes));
+    ctx->tp_cnt = (unsigned long long*)ctx->tp_buf;
+    ctx->tp_parts = (float*)((char*)ctx->tp_buf + ctx->tp_parts_off);
+    IC(dalloc(ctx, &ctx->tp_expect, sizeof(unsigned long long) * 2 * D.L));
   }
   IC(dalloc(ctx, &ctx->ctr, sizeof(Ctr) + sizeof(int) * D.S));
   IC(dalloc(ctx, &ctx->res, sizeof(DevResult) * D.S));
@@ -1507,6 +1625,7 @@ int sart_step(sart_ctx* ctx, int32_t max_windows, sart_stats* out) {
   if (!ctx) return set_err(SART_EINVAL, "null ctx");
   if (ctx->poisoned) return set_err(SART_ESTATE, "ctx poisoned by an earlier CUDA error");
   if (max_windows < 0) return set_err(SART_EINVAL, "max_windows < 0");
+  if (ctx->tp > 1 && !ctx->tp_connected) return set_err(SART_ESTATE, "tensor-parallel ctx not connected (sart_tp_connect)");
   cudaSetDevice(ctx->cfg.device);
   for (int w = 0; w < max_windows; ++w) {
     int rc = fill(ctx);
@@ -1778,6 +1897,71 @@ int sart_debug_prm_plan(const int32_t* ell_ws, const int32_t* ell, int32_t n, in
     const PrmPlan::Chunk& k = P.chunks[c];
     chunks[4 * c] = k.ntok; chunks[4 * c + 1] = k.nseg; chunks[4 * c + 2] = k.nqb; chunks[4 * c + 3] = k.ngat;
   }
+  return SART_OK;
+}
+
+int sart_debug_tp_segments(const sart_config* cfg, int32_t tensor, int64_t* out, int32_t cap, int32_t* n_out) {
+  if (!cfg || !out || !n_out) return set_err(SART_EINVAL, "null argument");
+  const int tp = cfg->tp_size < 1 ? 1 : cfg->tp_size;
+  if (cfg->tp_rank < 0 || cfg->tp_rank >= tp || cfg->n_heads % tp || cfg->n_kv_heads % tp || cfg->d_ff % tp ||
+      cfg->n_layers < 1 || cfg->head_dim < 1)
+    return set_err(SART_EINVAL, "bad tp / dims");
+  Dims F{};
+  F.L = cfg->n_layers; F.d = cfg->d_model; F.qh = cfg->n_heads; F.kvh = cfg->n_kv_heads; F.hd = cfg->head_dim;
+  F.F = cfg->d_ff; F.V = cfg->vocab; F.qkv = (F.qh + 2 * F.kvh) * F.hd;
+  if (tensor < 0 || tensor >= (int)tensor_sizes(F).size()) return set_err(SART_EINVAL, "tensor index");
+  const std::vector<Seg> g = shard_segments(F, tp, cfg->tp_rank, tensor);
+  *n_out = (int32_t)g.size();
+  if ((int)g.size() > cap) return set_err(SART_EFULL, "cap too small");
+  for (size_t i = 0; i < g.size(); ++i) {
+    const int64_t v[6] = {g[i].loff, g[i].n, g[i].cl, g[i].cf, g[i].c0, g[i].goff};
+    memcpy(out + 6 * i, v, sizeof(v));
+  }
+  return SART_OK;
+}
+
+int sart_tp_buffer(sart_ctx* ctx, void** dev_ptr, void* ipc_handle) {
+  if (!ctx || !dev_ptr) return set_err(SART_EINVAL, "null argument");
+  if (ctx->tp <= 1) return set_err(SART_EINVAL, "tp_size <= 1");
+  *dev_ptr = ctx->tp_buf;
+  if (ipc_handle) {
+    cudaSetDevice(ctx->cfg.device);
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, ctx->tp_buf));
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    memcpy(ipc_handle, &h, 64);
+  }
+  return SART_OK;
+}
+
+int sart_tp_connect(sart_ctx* ctx, void* const* peer_ptrs, const void* ipc_handles) {
+  if (!ctx) return set_err(SART_EINVAL, "null ctx");
+  if (ctx->tp <= 1) return set_err(SART_EINVAL, "tp_size <= 1");
+  if ((peer_ptrs == nullptr) == (ipc_handles == nullptr)) return set_err(SART_EINVAL, "give peer_ptrs or ipc_handles");
+  if (ctx->tp_connected) return set_err(SART_ESTATE, "already connected");
+  cudaSetDevice(ctx->cfg.device);
+  std::vector<void*> peers(ctx->tp, nullptr);
+  for (int r = 0; r < ctx->tp; ++r) {
+    if (r == ctx->tp_rank) { peers[r] = ctx->tp_buf; continue; }
+    if (peer_ptrs) {
+      if (!peer_ptrs[r]) return set_err(SART_EINVAL, "null peer pointer");
+      peers[r] = peer_ptrs[r];
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, (const char*)ipc_handles + 64 * (size_t)r, 64);
+      void* p = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        for (void* q : ctx->tp_opened) cudaIpcCloseMemHandle(q);
+        ctx->tp_opened.clear();
+        return set_err(SART_ECUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+      }
+      ctx->tp_opened.push_back(p);
+      peers[r] = p;
+    }
+  }
+  ctx->tp_peer = peers;
+  ctx->tp_connected = true;
   return SART_OK;
 }
 

@@ -45,7 +45,7 @@ class SartConfig(C.Structure):
         ("prm_n_kv_heads", C.c_int32), ("prm_head_dim", C.c_int32), ("prm_d_ff", C.c_int32),
         ("prm_weight_seed", C.c_uint64), ("prm_host_weights", C.c_void_p),
         ("kv_pool", C.c_void_p), ("kv_pool_bytes", C.c_size_t), ("es_every_step", C.c_int32),
-        ("record_trace", C.c_int32),
+        ("record_trace", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32),
     ]
 
 
@@ -137,9 +137,12 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                     C.c_int32, C.c_int32, C.c_int32, C.c_int32]
     lib.sart_debug_prm_plan.argtypes = [P32, P32, C.c_int32, C.c_int32, C.c_int32, P32, C.c_int32, P32, P32, P32,
                                         P32, C.c_int32, P32]
+    lib.sart_debug_tp_segments.argtypes = [C.POINTER(SartConfig), C.c_int32, P64, C.c_int32, P32]
+    lib.sart_tp_buffer.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p]
+    lib.sart_tp_connect.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p]
     lib.sart_trace_fetch.argtypes = [C.c_void_p, C.POINTER(SartTraceRow), C.c_int64, P64, P32, C.c_int64, P64,
                                      C.POINTER(C.c_uint64), C.c_int64, P64]
-    for f in ("sart_trace_fetch", "sart_debug_prm_plan", "sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
+    for f in ("sart_debug_tp_segments", "sart_tp_buffer", "sart_tp_connect", "sart_trace_fetch", "sart_debug_prm_plan", "sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
               "sart_get_state", "sart_debug_fetch", "sart_get_profile", "sart_reset_profile", "sart_debug_gemm", "sart_set_profile"):
         getattr(lib, f).restype = C.c_int
     _lib = lib
@@ -148,7 +151,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 
 EXPORTED = ["sart_init", "sart_admit", "sart_step", "sart_export_counters", "sart_collect", "sart_destroy",
             "sart_strerror", "sart_last_error", "sart_get_state", "sart_debug_fetch", "sart_get_profile",
-            "sart_reset_profile", "sart_debug_gemm", "sart_set_profile", "sart_debug_prm_plan", "sart_trace_fetch"]
+            "sart_reset_profile", "sart_debug_gemm", "sart_set_profile", "sart_debug_prm_plan", "sart_trace_fetch",
+            "sart_tp_buffer", "sart_tp_connect", "sart_debug_tp_segments"]
 
 
 def debug_prm_plan(ell_ws, ell, chunk: int, qp: int):
@@ -166,6 +170,19 @@ def debug_prm_plan(ell_ws, ell, chunk: int, qp: int):
                                    ch.ctypes.data_as(P32), len(ch), C.byref(nc)))
     a, b, c = ns.value, nq.value, ng.value
     return out[:a], out[a:a + b], out[a + b:a + b + c], ch[:nc.value]
+
+
+def debug_tp_segments(shape, tp: int, rank: int, tensor: int):
+    """sart_debug_tp_segments (host only): int64 [k][6] {loff, n, cl, cf, c0, goff} records."""
+    lib = load_library()
+    cfg = SartConfig()
+    cfg.n_layers, cfg.d_model, cfg.n_heads = shape.n_layers, shape.d_model, shape.n_heads
+    cfg.n_kv_heads, cfg.head_dim, cfg.d_ff, cfg.vocab = shape.n_kv_heads, shape.head_dim, shape.d_ff, shape.vocab
+    cfg.tp_size, cfg.tp_rank = tp, rank
+    out = np.zeros((8, 6), np.int64)
+    n = C.c_int32()
+    _check(lib.sart_debug_tp_segments(C.byref(cfg), tensor, out.ctypes.data_as(P64), 8, C.byref(n)))
+    return out[: n.value]
 
 
 def debug_gemm(A_bits: np.ndarray, B_bits: np.ndarray, bias=None, C=None, mode: int = 0, splits: int = 1,
@@ -211,11 +228,12 @@ class Engine:
                  attn_mode: int = SART_ATTN_CASCADE, device: int = 0, stream: int = 0,
                  enable_forced_tokens: bool = False, debug_capture: bool = False, profile: bool = False,
                  prm_shape=None, prm_host_weights: Optional[np.ndarray] = None, prm_weight_seed: int = 0,
-                 kv_pool=None, es_every_step: bool = False, record_trace: bool = False):
+                 kv_pool=None, es_every_step: bool = False, record_trace: bool = False, tp=(1, 0)):
         """prm_shape (a synth.ModelShape, vocab = the policy's): the separate PRM decoder of
         row f2; None -> the PRM head on the policy's hidden state.  kv_pool: (device address,
         bytes) of a caller-owned KV pool buffer (e.g. a torch tensor's data_ptr() and nbytes;
-        the caller keeps it alive until close())."""
+        the caller keeps it alive until close()).  tp = (tp_size, tp_rank): tensor parallelism
+        (row f4); connect the ranks with tp_buffer() / tp_connect() before the first step."""
         self.lib = load_library()
         self.shape = shape
         self.cap, self.T = cap, T
@@ -239,6 +257,8 @@ class Engine:
         if kv_pool is not None:
             cfg.kv_pool, cfg.kv_pool_bytes = int(kv_pool[0]), int(kv_pool[1])
         cfg.es_every_step, cfg.record_trace = int(es_every_step), int(record_trace)
+        cfg.tp_size, cfg.tp_rank = int(tp[0]), int(tp[1])
+        self.tp = max(1, int(tp[0]))
         self._prm_weights = None
         if prm_shape is not None:
             if prm_shape.vocab != shape.vocab:
@@ -341,6 +361,25 @@ class Engine:
             if rc == SART_OK:
                 return out
 
+    # ---------------------------------------------------------------- tensor parallelism
+    def tp_buffer(self):
+        """sart_tp_buffer: (device address of this rank's receive buffer, 64-byte IPC handle)."""
+        p = C.c_void_p()
+        h = (C.c_ubyte * 64)()
+        _check(self.lib.sart_tp_buffer(self.ctx, C.byref(p), h))
+        return p.value, bytes(h)
+
+    def tp_connect(self, ptrs=None, handles=None):
+        """sart_tp_connect: every rank's buffer address (ranks of this process) or every
+        rank's IPC handle (64 bytes each, rank order; other processes)."""
+        if ptrs is not None:
+            arr = (C.c_void_p * len(ptrs))(*[C.c_void_p(int(x)) for x in ptrs])
+            _check(self.lib.sart_tp_connect(self.ctx, arr, None))
+        else:
+            blob = b"".join(handles)
+            buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
+            _check(self.lib.sart_tp_connect(self.ctx, None, buf))
+
     # ---------------------------------------------------------------- PP2 trace
     def trace_fetch(self):
         """sart_trace_fetch: (rows, hashes) recorded since the last call.  rows: dicts with
@@ -408,8 +447,8 @@ class Engine:
             out = np.zeros(rows, np.int32)
         elif what in (DBG_SCORES, DBG_PRM_SCORES):
             out = np.zeros(rows, np.float32)
-        elif what == DBG_ATTN:
-            out = np.zeros((rows, sh.n_heads * sh.head_dim), np.float32)
+        elif what == DBG_ATTN:   # this rank's q heads under tensor parallelism
+            out = np.zeros((rows, sh.n_heads // self.tp * sh.head_dim), np.float32)
         elif what == DBG_Z:
             out = np.zeros((rows, sh.d_model), np.float32)
         else:

@@ -12,10 +12,14 @@ SAMPLED: three requests (shortest prompt, longest prompt, one in the middle) x t
 branches.  For each sampled row the oracle computes, one by one, the logits at the last
 step of each window, the PRM-head score at the boundary and the attention output of
 layers {0, 14, 27}; the row-relative error (reading R30) must be <= 2e-2 (bf16,
-north_star) -- for the 28-layer logits, or within 1.25x of the intrinsic bf16 drift that a
-rounding-only emulation shows on the same row (reading R41).  For every row (all 512)
-properties that hold at any size are checked: the logits are finite, and the row order /
-step counts match the teacher-forced schedule.
+north_star) for every one of them, logits included -- no allowance.  A second, diagnostic
+reference (tests/bf16_emulation.py: fp64 with bf16 rounding at the points any bf16 decode
+must round) measures the intrinsic bf16 drift on the same rows; the GPU's mean logits error
+must not exceed 1.2x the emulation's (the CUDA path adds no error beyond bf16 storage; two
+bf16 paths decorrelate through 28 layers, so a per-row GPU-vs-emulation bound is not a
+meaningful check: DESIGN.md R41, profiles/r2_bf16_sensitivity.txt).  For every row (all
+512) properties that hold at any size are checked: the logits are finite, and the row order
+/ step counts match the teacher-forced schedule.
 """
 import numpy as np
 import pytest
@@ -105,9 +109,10 @@ def test_c2_full_size_sampled_rows():
     worst_attn = max(max(e["attn"].values()) for e in errs)
     assert worst_attn <= TOL, worst_attn
     assert max(e["prm"] for e in errs) <= TOL
-    # Reading R41: at full depth the 2e-2 logits bound is the size of the intrinsic
-    # bf16 drift itself -- the NumPy emulation that rounds at the GPU's bf16 storage points
-    # and has no other error is 1.3-1.9e-2 from the fp64 oracle on these rows.  A row passes
-    # at 2e-2, or within 1.25x of that intrinsic bf16 error on the same row.
-    bad = [e for e in errs if e["logits"] > max(TOL, 1.25 * e["emu_vs_oracle"])]
+    bad = [e for e in errs if e["logits"] > TOL]
     assert not bad, bad
+    g_mean = float(np.mean([e["logits"] for e in errs]))
+    e_mean = float(np.mean([e["emu_vs_oracle"] for e in errs]))
+    print(f"logits row error vs fp64 oracle: GPU mean {g_mean:.4f} max {max(e['logits'] for e in errs):.4f}; "
+          f"bf16 emulation mean {e_mean:.4f} max {max(e['emu_vs_oracle'] for e in errs):.4f}")
+    assert g_mean <= 1.2 * e_mean, (g_mean, e_mean)
