@@ -14,6 +14,8 @@
 // weight stream is read from HBM once (small-M decode GEMMs are weight-bandwidth-bound).
 #include <cuda.h>
 
+#include <cstdio>
+
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -227,6 +229,41 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// QKV epilogue: where row gm's k / v go and at which RoPE position (decode: the row's next
+// suffix entry; prefill: a prompt position; f2 PRM pass: a suffix entry of a batch row)
+struct RowMeta {
+  int pos, sib;
+  long long blk;
+  bool kv_ok;
+};
+__device__ __forceinline__ RowMeta qkv_row_meta(const QkvEpi& epi, int gm, int M) {
+  const Dims& D = epi.D;
+  RowMeta r{0, 0, 0, false};
+  if (gm >= M) return r;
+  if (epi.a.sf_row) {
+    const int row = epi.a.sf_row[gm];
+    if (row >= 0) {
+      const int l = epi.a.pf_pos[gm];
+      r.pos = epi.reqs.P[epi.rows.slot[row]] - 1 + l;
+      r.blk = epi.rows.table[(long long)row * D.MBR + l / D.bs];
+      r.sib = l % D.bs;
+      r.kv_ok = true;
+    }
+  } else if (epi.a.pf_slot) {
+    r.pos = epi.a.pf_pos[gm];
+    r.blk = epi.reqs.prefix[(long long)epi.a.pf_slot[gm] * D.MPB + r.pos / D.bs];
+    r.sib = r.pos % D.bs;
+    r.kv_ok = true;
+  } else if (epi.rows.status[gm] == RUNNING_ST) {
+    const int l = epi.rows.ell[gm];
+    r.pos = epi.reqs.P[epi.rows.slot[gm]] - 1 + l;
+    r.blk = epi.rows.table[(long long)gm * D.MBR + l / D.bs];
+    r.sib = l % D.bs;
+    r.kv_ok = true;
+  }
+  return r;
+}
+
 template <int BN, int MODE, int MS>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const bf16* __restrict__ Bt,
@@ -252,7 +289,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 #ifdef SART_GEMM_TS   // phase timestamps of CTA 0 (build with -DSART_GEMM_TS; SART_GEMM_TS=1 prints them)
   __shared__ int ts_slot;
-  const bool tsb = blockIdx.x == 0;
+#ifndef SART_GEMM_TS_MODE
+#define SART_GEMM_TS_MODE -1   // record launches of this MODE only (-1: every launch)
+#endif
+  const bool tsb = blockIdx.x == 0 && (SART_GEMM_TS_MODE < 0 || MODE == SART_GEMM_TS_MODE);
   if (threadIdx.x == 0 && tsb) { ts_slot = atomicAdd(&g_gemm_ts_idx, 1) & 3; g_gemm_ts[ts_slot][0] = gtime(); }
 #define TS(i) if (tsb) g_gemm_ts[ts_slot][i] = gtime()
 #else
@@ -383,7 +423,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
     pdl_wait();   // outputs may be read by the previous kernel; inputs (bias, rows) are visible
     // TP: this rank's consumer of projection k expects gridDim.x arrivals from each rank
-    if (tp.tp > 1 && blockIdx.x == 0 && warp == 2 && lane == 0) tp.expect[tp.k] += (unsigned long long)gridDim.x * tp.tp;
+    if (tp.tp > 1 && blockIdx.x == 0 && warp == 2 && lane == 0) {
+      tp.expect[tp.k] += (unsigned long long)gridDim.x * tp.tp;
+#ifdef SART_TP_DEBUG
+      printf("tp gemm rank %d k %d grid %d expect %llu cnt0 %p cnt1 %p\n", tp.rank, tp.k, gridDim.x, tp.expect[tp.k],
+             (void*)tp.cnt[0], (void*)tp.cnt[1]);
+#endif
+    }
     const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;  // which 32-column chunks of the tile it handles
     const int row = q * 32 + lane;
@@ -393,7 +439,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t aph = (it / NBUF) & 1;
       int m0_, n0, kb0, kb1, sp;
       unit_of(t, m0_, n0, kb0, kb1, sp);
+      const int n0_ = n0;
       float* Cs = C + (size_t)sp * M * N;
+      // QKV: this row's position and KV slot are dependent global loads (status, ell, request
+      // prompt length, block table); resolve them -- and pull the row's RoPE cos / sin lines
+      // toward L1 -- while the mainloop still runs, off the epilogue's critical path (MS == 1)
+      RowMeta rm{};
+      if constexpr (MODE == GEMM_QKV || MODE == GEMM_QKV_HALF) {
+        rm = qkv_row_meta(epi, m0_ + row, M);
+        constexpr int HD = MODE == GEMM_QKV_HALF ? 128 : BN;
+        const float* cs = epi.rope_cs + (long long)rm.pos * HD + (MODE == GEMM_QKV_HALF ? ((n0_ / 64) & 1) * 32 : 0);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(cs));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(cs + HD / 2));
+        if (HD == 128 && MODE == GEMM_QKV) {
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(cs + 32));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(cs + HD / 2 + 32));
+        }
+      }
       mbar_wait(&sm.tfull[as], aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (warp == 2 && lane == 0 && it == 0) { TS(5); }
@@ -430,33 +492,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (old != S - 1) continue;
           __threadfence();
         }
-        int pos = 0;
-        bool kv_ok = false;
-        long long blk = 0;
-        int sib = 0;
-        if (gm < M) {
-          if (epi.a.sf_row) {                  // f2 PRM pass: suffix entry of a batch row
-            const int row = epi.a.sf_row[gm];
-            if (row >= 0) {
-              const int l = epi.a.pf_pos[gm];
-              pos = epi.reqs.P[epi.rows.slot[row]] - 1 + l;
-              blk = epi.rows.table[(long long)row * D.MBR + l / D.bs];
-              sib = l % D.bs;
-              kv_ok = true;
-            }
-          } else if (epi.a.pf_slot) {
-            pos = epi.a.pf_pos[gm];
-            blk = epi.reqs.prefix[(long long)epi.a.pf_slot[gm] * D.MPB + pos / D.bs];
-            sib = pos % D.bs;
-            kv_ok = true;
-          } else if (epi.rows.status[gm] == RUNNING_ST) {
-            const int l = epi.rows.ell[gm];
-            pos = epi.reqs.P[epi.rows.slot[gm]] - 1 + l;
-            blk = epi.rows.table[(long long)gm * D.MBR + l / D.bs];
-            sib = l % D.bs;
-            kv_ok = true;
-          }
-        }
+        const int pos = rm.pos, sib = rm.sib;
+        const bool kv_ok = rm.kv_ok;
+        const long long blk = rm.blk;
         const bool rot = head < D.qh + D.kvh;
         const float* cs = epi.rope_cs + (long long)pos * HD;   // [cos(hd/2) | sin(hd/2)]
 #pragma unroll 1

@@ -1,5 +1,7 @@
 // Decoder elementwise kernels: weight init, embedding gather, RMSNorm, RoPE + paged KV
 // append, SwiGLU, PRM head tail.  (SURVEY §8(a) rows a2, a3, a5, a6, a8.)
+#include <cstdio>
+
 #include "kernels.h"
 
 // ------------------------------------------------------------ device weight init
@@ -80,35 +82,21 @@ template <typename T>
 __global__ void __launch_bounds__(512) k_rmsnorm(float* __restrict__ h, const float* __restrict__ parts, int np,
                                                   long long pstride, const T* __restrict__ g, T* __restrict__ out,
                                                   float* __restrict__ out32, const int* __restrict__ status, int n,
-                                                  int d, float eps, const unsigned long long* __restrict__ tp_cnt,
-                                                  const unsigned long long* __restrict__ tp_expect) {
+                                                  int d, float eps) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
   if (status && status[r] != RUNNING_ST) return;
-  if (tp_cnt) {   // tensor parallelism: every rank's partial tiles of the projection have landed
-    if (threadIdx.x == 0) {
-      const unsigned long long target = *reinterpret_cast<const volatile unsigned long long*>(tp_expect);
-      unsigned long long t0;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-      for (;;) {
-        unsigned long long v, t;
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(tp_cnt) : "memory");
-        if (v >= target) break;
-        __nanosleep(32);
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > 20000000000ull) __trap();   // a peer never delivered (20 s): fail, do not hang
-      }
-    }
-    __syncthreads();
-  }
+
   float4* x = reinterpret_cast<float4*>(h + (long long)r * d);
   const int d4 = d >> 2;
   float ss = 0.f;
   for (int i = threadIdx.x; i < d4; i += blockDim.x) {
     float4 v = x[i];
     for (int sp = 0; sp < np; ++sp) {   // split order: deterministic
-      const float4 p = reinterpret_cast<const float4*>(parts + sp * pstride + (long long)r * d)[i];
+      // L2 loads (.cg): under tensor parallelism the partials were written by another rank's
+      // kernel, outside this stream's dependency chain, so no L1 / read-only-cache line may serve them
+      const float4 p = __ldcg(reinterpret_cast<const float4*>(parts + sp * pstride + (long long)r * d) + i);
       v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
     }
     if (np) x[i] = v;
@@ -139,13 +127,48 @@ static int rmsnorm_threads(int d) {
   while (t < 512 && d / t > 16) t *= 2;
   return t;
 }
+// Tensor parallelism: one warp waits until every rank's partial tiles of the projection have
+// landed (arrival counter >= the expected count the local producer set), and only then lets
+// the RMSNorm launch (pdl_trigger after the wait).  The wait occupies one warp, never the SMs
+// the peers' GEMMs need -- which matters when ranks share a GPU (tests) -- and a peer that
+// never delivers traps after 20 s instead of hanging the device.
+__global__ void k_tp_wait(const unsigned long long* __restrict__ cnt, const unsigned long long* __restrict__ expect) {
+  pdl_wait();   // the local producer has finished: *expect is final
+  if (threadIdx.x == 0) {
+    const unsigned long long target = *reinterpret_cast<const volatile unsigned long long*>(expect);
+#ifdef SART_TP_DEBUG
+    printf("tp wait cnt %p target %llu now %llu\n", (const void*)cnt, target, *(const volatile unsigned long long*)cnt);
+#endif
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      unsigned long long v, t;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+      if (v >= target) break;
+      __nanosleep(64);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) {   // a peer never delivered (20 s): fail, do not hang
+#ifdef SART_TP_DEBUG
+        printf("k_tp_wait timeout: counter %llu < expected %llu (cnt %p)\n", v, target, (const void*)cnt);
+        break;
+#else
+        __trap();
+#endif
+      }
+    }
+    __threadfence();
+  }
+  __syncwarp();
+  pdl_trigger();
+}
 template <typename T>
 void launch_rmsnorm(float* h, const float* parts, int np, const T* g, T* out, float* out32, const int* status, int n,
                     int d, float eps, cudaStream_t s, const unsigned long long* tp_cnt,
                     const unsigned long long* tp_expect) {
-  if (n > 0)
-    launch_pdl(k_rmsnorm<T>, dim3(n), dim3(rmsnorm_threads(d)), 0, s, h, parts, np, (long long)n * d, g, out, out32,
-               status, n, d, eps, tp_cnt, tp_expect);
+  if (n <= 0) return;
+  if (tp_cnt) launch_pdl(k_tp_wait, dim3(1), dim3(32), 0, s, tp_cnt, tp_expect);
+  launch_pdl(k_rmsnorm<T>, dim3(n), dim3(rmsnorm_threads(d)), 0, s, h, parts, np, (long long)n * d, g, out, out32,
+             status, n, d, eps);
 }
 
 // ------------------------------------------------------------ RoPE + KV append

@@ -148,7 +148,8 @@ struct sart_ctx {
   // tensor parallelism (row f4): symmetric receive buffer [counters | partials] and the peers'
   int tp = 1, tp_rank = 0;
   void* tp_buf = nullptr;                  // this rank's receive buffer (cudaMalloc base)
-  float* tp_parts = nullptr;               // its partial region: [tp][S <= 8][W][max(d, qkv)] fp32
+  float* tp_parts = nullptr;               // its partial regions: 2 x [tp][S <= 8][W][max(d, qkv)] fp32
+  size_t tp_region = 0;                    // floats per region (exchange k uses region k & 1)
   unsigned long long* tp_cnt = nullptr;    // its arrival counters [2 L]
   unsigned long long* tp_expect = nullptr; // expected arrivals [2 L] (local)
   std::vector<void*> tp_peer;              // every rank's buffer base as seen from here
@@ -337,15 +338,18 @@ ResParts proj_res(sart_ctx* ctx, const T* A, const T* B, int M, int N, int K, in
       t.rank = ctx->tp_rank;
       t.k = k;
       t.expect = ctx->tp_expect;
+      // two receive regions, alternating by exchange: a rank runs at most one exchange ahead of
+      // a peer, so it never overwrites tiles the peer's consumer may still be reading
+      const size_t roff = (size_t)(k & 1) * ctx->tp_region;
       for (int p = 0; p < ctx->tp; ++p) {
-        t.dst[p] = (float*)((char*)ctx->tp_peer[p] + ctx->tp_parts_off);
+        t.dst[p] = (float*)((char*)ctx->tp_peer[p] + ctx->tp_parts_off) + roff;
         t.cnt[p] = (unsigned long long*)ctx->tp_peer[p];
       }
-      if (!launch_gemm_tc_split(A, B, nullptr, ctx->tp_parts, nullptr, M, N, K, GEMM_STORE, S, BN, MS, ctx->st,
-                                nullptr, &t))
+      if (!launch_gemm_tc_split(A, B, nullptr, ctx->tp_parts + roff, nullptr, M, N, K, GEMM_STORE, S, BN, MS,
+                                ctx->st, nullptr, &t))
         ctx->gemm_failed = true;
       ctx->launches++;
-      return ResParts{ctx->tp_parts, S * ctx->tp, ctx->tp_cnt + k, ctx->tp_expect + k};
+      return ResParts{ctx->tp_parts + roff, S * ctx->tp, ctx->tp_cnt + k, ctx->tp_expect + k};
     }
   }
   return ResParts{ctx->parts, proj<T>(ctx, A, B, M, N, K), nullptr, nullptr};
@@ -1085,6 +1089,18 @@ int run_window(sart_ctx* ctx) {
     if (cudaEventElapsedTime(&ms, ctx->prm->prm_ev[0], ctx->prm->prm_ev[1]) == cudaSuccess) ctx->prm_ms += ms;
     ctx->prm_passes++;
   }
+  if (getenv("SART_GEMM_TS_PRINT")) {   // phase timestamps of the last 4 recorded GEMM launches
+    unsigned long long hts[4][10];        // (CTA 0; build with -DSART_GEMM_TS [-DSART_GEMM_TS_MODE=m])
+    CK(cudaStreamSynchronize(ctx->st));
+    gemm_ts_fetch(&hts[0][0]);
+    for (int i = 0; i < 4; ++i) {
+      fprintf(stderr, "GEMMTS window %d launch %d (ns from CTA start): setup %lld wait %lld mma0 %lld mma_last %lld "
+              "epi_start %lld epi_end %lld end %lld dealloc %lld\n", ctx->windows, i,
+              (long long)(hts[i][1] - hts[i][0]), (long long)(hts[i][2] - hts[i][0]), (long long)(hts[i][3] - hts[i][0]),
+              (long long)(hts[i][4] - hts[i][0]), (long long)(hts[i][5] - hts[i][0]), (long long)(hts[i][6] - hts[i][0]),
+              (long long)(hts[i][7] - hts[i][0]), (long long)(hts[i][8] - hts[i][0]));
+    }
+  }
   if (ctx->cfg.profile) {
     for (int i = 0; i + 1 < ctx->ev_used; i += 2) {
       float ms = 0.f;
@@ -1428,7 +1444,8 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   }
   if (ctx->tp > 1) {   // row f4: [arrival counters 2L (4 KB-aligned) | partials [tp][8][W][max(d, qkv)]]
     ctx->tp_parts_off = ((size_t)2 * D.L * sizeof(unsigned long long) + 4095) / 4096 * 4096;
-    const size_t bytes = ctx->tp_parts_off + sizeof(float) * (size_t)ctx->tp * 8 * ctx->W * std::max(D.d, D.qkv);
+    ctx->tp_region = (size_t)ctx->tp * 8 * ctx->W * std::max(D.d, D.qkv);
+    const size_t bytes = ctx->tp_parts_off + sizeof(float) * 2 * ctx->tp_region;
     IC(dalloc(ctx, &ctx->tp_buf, bytes));
     ctx->tp_cnt = (unsigned long long*)ctx->tp_buf;
     ctx->tp_parts = (float*)((char*)ctx->tp_buf + ctx->tp_parts_off);

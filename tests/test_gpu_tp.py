@@ -129,7 +129,12 @@ def test_tp2_geometry_teacher_forced(name):
     32/4, d 8192, F 28672 -> 14336): one layer, small vocab."""
     shape = _slice(name)
     prompts = [gen_prompt(43, shape.vocab, EOS, 70, 70)]
-    w = teacher_forced_tp(shape, 2, prompts, N=3, steps=16, T=8, bs=64)
+    # reading R39: the bf16 bound is stated at the O1 logit scale; at d = 8192 the q.k logits of
+    # std-0.02 weights are ~2.3x C2's and the attention output error of ANY bf16 path sits at
+    # the bound (TP = 1 on the same rows: 1.8e-2, tools/check_70b_geometry.py) -- the 70B
+    # geometry runs at std 0.01, where TP = 1 gives 0.44e-2
+    std = 0.01 if shape.d_model >= 8192 else 0.02
+    w = teacher_forced_tp(shape, 2, prompts, N=3, steps=16, T=8, bs=64, std=std)
     print(f"TP=2 {name}-L1 worst", w)
 
 
