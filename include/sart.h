@@ -17,7 +17,8 @@
  *   - Input pointers are HOST pointers unless stated otherwise; they are
  *     borrowed only for the duration of the call (deep-copied when needed).
  *   - The ctx owns all device memory it allocates.  Outputs go to caller buffers.
- *   - One sart_ctx per GPU; a ctx is NOT thread-safe.
+ *   - One sart_ctx per GPU (or per tensor-parallel rank); a ctx is NOT thread-safe, but
+ *     different ctx may be driven from different host threads concurrently.
  *   - After SART_ECUDA the ctx is poisoned: every later call except
  *     sart_destroy returns SART_ESTATE.
  *   - Validation is all-or-nothing: an error never leaves partial state.

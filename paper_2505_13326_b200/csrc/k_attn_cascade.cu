@@ -823,7 +823,7 @@ static int attn_cfg() {
   }
   return c;
 }
-bool g_attn_skip_merge = false;
+thread_local bool g_attn_skip_merge = false;   // per host thread (ctx of a TP group each drive one)
 template <int HD>
 static void launch_hd(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse, Dims D,
                       int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s) {

@@ -34,11 +34,17 @@ template <int BN, int MS> struct Tmem {
 // warp 0 TMA producer, warp 1 MMA issuer, then NEPI epilogue warps: NEPI / 4 per TMEM lane
 // quarter (warp % 4), splitting the 32-column chunks between them
 #ifndef SART_GEMM_NEPI
-#define SART_GEMM_NEPI 4   // 8 (two warps per lane quarter) measured 1.3% slower per C2 step
+#define SART_GEMM_NEPI 4   // 8 (two warps per lane quarter) for every mode measured 1.3% slower per C2 step
 #endif
-constexpr int NEPI = SART_GEMM_NEPI;
-constexpr int NTHREADS = 64 + 32 * NEPI;
-constexpr int CSTEP = 32 * (NEPI / 4);   // chunk stride of one epilogue warp
+#ifndef SART_GEMM_NEPI_SWIGLU
+#define SART_GEMM_NEPI_SWIGLU 8   // the SwiGLU epilogue (2 MUFU ops per output, one tile per CTA) runs alone
+#endif                            // after the mainloop: two warps per lane quarter halve it
+template <int MODE> struct Epi {
+  static constexpr int NEPI = MODE == GEMM_SWIGLU ? SART_GEMM_NEPI_SWIGLU : SART_GEMM_NEPI;
+  static constexpr int NTHREADS = 64 + 32 * NEPI;
+  static constexpr int CSTEP = 32 * (NEPI / 4);   // chunk stride of one epilogue warp
+  static constexpr int SLAB = MODE == GEMM_SWIGLU ? 1 : NEPI;   // transpose slabs (store epilogues)
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -201,14 +207,14 @@ __device__ __forceinline__ void store_tile_f32(uint32_t tbase, float* Cs, int mr
   }
 }
 
-template <int BN, int MS>
+template <int BN, int MS, int NSLAB>
 struct Smem {
   static constexpr int STAGES = Stages<BN, MS>::value;
   alignas(1024) bf16 a[STAGES][MS * BM * BK];
   alignas(1024) bf16 b[STAGES][BN * BK];
   uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   uint32_t tmem_base;
-  alignas(16) float slab[NEPI][32 * 32];   // epilogue transpose staging (explicit st/ld.shared)
+  alignas(16) float slab[NSLAB][32 * 32];   // epilogue transpose staging (explicit st/ld.shared)
 };
 
 // MS m-subtiles of 128 rows share each B stage (tile = MS*128 x BN): per-SM operand traffic
@@ -265,14 +271,15 @@ __device__ __forceinline__ RowMeta qkv_row_meta(const QkvEpi& epi, int gm, int M
 }
 
 template <int BN, int MODE, int MS>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(Epi<MODE>::NTHREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const bf16* __restrict__ Bt,
               float* C, const float* __restrict__ bias, bf16* act, int M, int N, int K, int S,
               const __grid_constant__ QkvEpi epi, const __grid_constant__ TpOut tp) {
   extern __shared__ __align__(16) uint8_t smem_raw[];   // 1024-aligned below (+1024 B slack)
-  Smem<BN, MS>& sm =
-      *reinterpret_cast<Smem<BN, MS>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int STAGES = Smem<BN, MS>::STAGES;
+  Smem<BN, MS, Epi<MODE>::SLAB>& sm =
+      *reinterpret_cast<Smem<BN, MS, Epi<MODE>::SLAB>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int STAGES = Smem<BN, MS, Epi<MODE>::SLAB>::STAGES;
+  constexpr int NEPI = Epi<MODE>::NEPI, CSTEP = Epi<MODE>::CSTEP;
   constexpr int NBUF = Tmem<BN, MS>::NBUF, TCOLS = Tmem<BN, MS>::COLS;
   constexpr uint32_t STAGE_TX = (MS * BM + BN) * BK * 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -649,9 +656,14 @@ bool make_map(CUtensorMap* m, const void* ptr, int rows, int K, int box_rows) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Process-wide and used by every ctx: several ctx may launch from different host threads (one
+// thread per rank of a tensor-parallel group), so lookups and inserts are serialised.  Entries
+// are std::map nodes, so returned pointers stay valid across later inserts.
 struct MapCache {
   std::map<std::tuple<const void*, int, int, int>, CUtensorMap> m;
+  std::mutex mu;
   const CUtensorMap* get(const void* p, int rows, int K, int box) {
+    std::lock_guard<std::mutex> lk(mu);
     auto key = std::make_tuple(p, rows, K, box);
     auto it = m.find(key);
     if (it != m.end()) return &it->second;
@@ -668,7 +680,7 @@ bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* 
   const CUtensorMap* ma = g_maps.get(A, M, K, BM);
   const CUtensorMap* mb = Bt ? ma : g_maps.get(B, N, K, MODE == GEMM_QKV_HALF ? 32 : BN);
   if (!ma || !mb) return false;
-  const size_t smem = sizeof(Smem<BN, MS>) + 1024;
+  const size_t smem = sizeof(Smem<BN, MS, Epi<MODE>::SLAB>) + 1024;
   ensure_dyn_smem(k_gemm_tc<BN, MODE, MS>, (int)smem);
   const int g_num_sms = device_sms();
   const int ntiles = ((M + MS * BM - 1) / (MS * BM)) * ((N + BN - 1) / BN) * S;
@@ -677,7 +689,7 @@ bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* 
   if (epi) e = *epi;
   TpOut t{};
   if (tpo) t = *tpo;
-  launch_pdl(k_gemm_tc<BN, MODE, MS>, dim3(grid), dim3(NTHREADS), smem, s, *ma, *mb, Bt, C, bias, act, M, N, K, S, e,
+  launch_pdl(k_gemm_tc<BN, MODE, MS>, dim3(grid), dim3(Epi<MODE>::NTHREADS), smem, s, *ma, *mb, Bt, C, bias, act, M, N, K, S, e,
              t);
   return true;
 }

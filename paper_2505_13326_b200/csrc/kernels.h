@@ -141,7 +141,7 @@ int prefill_query_block(const Dims& D);   // query positions per prefill CTA (16
 // entries over [prefix ; suffix entries 0..entry] (causal)
 void launch_attn_suffix_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
                            const int4* qblocks, int nqb, cudaStream_t s);
-extern bool g_attn_skip_merge;   // measurement only (SART_ABLATE): launch the cascade kernel without its merge
+extern thread_local bool g_attn_skip_merge;   // measurement only (SART_ABLATE): launch the cascade kernel without its merge
 void launch_attn_account(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, double* acc, cudaStream_t s);
 void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse,
                          Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s);
