@@ -148,6 +148,13 @@ typedef struct {
    * n_heads and n_kv_heads divisible by tp_size, (d_ff / tp_size) % 128 == 0.
    * tp_size 0 or 1: no tensor parallelism. */
   int32_t tp_size, tp_rank;
+  /* NEXT row f1: chunked prefill interleaved with decode (reading
+   * R44).  0: each fill's prompts are prefilled before the window's first decode step (Alg. 1
+   * L7 inline).  C in [1, 2048]: they are prefilled in C-token chunks, chunk c right before
+   * window step min(c + 1, T), so resident rows keep decoding while long prompts are
+   * prefilled; the rows of a request prefilled in this window start decoding at the step
+   * whose chunk completes its prefix (ST_WAIT until then), every other row at step 1. */
+  int32_t prefill_chunk;
 } sart_config;
 
 /* Create an engine.  Errors: EINVAL (shape/range), ENOMEM (allocation failure, or
@@ -389,6 +396,10 @@ typedef struct {
                               admission events, prefill token lists, counter exports) */
   int64_t d2h_bytes;       /* device->host bytes it copied (per-window counter records, live
                               polls, finalized records, selected branches' tokens)  */
+  double first_step_ms_max; /* profile mode: longest time from a window's start to its first
+                              decode step's completion (includes an inline prefill)  */
+  double step_ms_max;       /* profile mode: longest single decode step (incl. an interleaved
+                              prefill chunk), both over the windows since the last reset */
 } sart_profile;
 int sart_get_profile(sart_ctx* ctx, sart_profile* out);
 /* Turn per-launch attention timing on or off.  While on, decode steps are launched eagerly

@@ -83,6 +83,12 @@ class EngineConfig:
     # its other running branches stop decoding at that step; they are EarlyStopped at the
     # boundary (never pruned).  False = paper semantics: early stop only at T boundaries.
     es_every_step: bool = False
+    # Reading R44 (row f1): 0 = each fill's prefill runs before the window's first decode step
+    # (Alg. 1 L7 inline).  C > 0 = chunked prefill interleaved with decode: the fill's prompts
+    # (prefix tokens, FCFS order, concatenated) are processed in C-token chunks, chunk c right
+    # before window step min(c + 1, T); the rows of a request prefilled in this fill start
+    # decoding at the step whose chunk completes its prefix, the other rows at step 1.
+    prefill_chunk: int = 0
 
 
 @dataclasses.dataclass
@@ -109,6 +115,7 @@ class ReqState:
     branch_label: List[int] = dataclasses.field(default_factory=list)
     branch_tokens: Dict[int, List[int]] = dataclasses.field(default_factory=dict)
     window_prefill: int = -1
+    ready_wstep: int = 1          # R44: window step at which its prefix is complete (window_prefill)
 
 
 @dataclasses.dataclass
@@ -126,6 +133,7 @@ class Row:
     hist: List[int] = dataclasses.field(default_factory=list)
     terminal: int = RUNNING       # state decided at the boundary
     stopped: bool = False         # R43: stopped mid-window by early stop (incomplete)
+    start: int = 1                # R44: first window step this row decodes in its first window
 
 
 # ------------------------------------------------------------------ sources
@@ -316,6 +324,7 @@ class Engine:
     # -------------------------------------------------------------- fill loop (L3-11)
     def _fill(self) -> None:
         cfg = self.cfg
+        pf_tok = 0                      # prefix tokens prefilled so far in this fill (R44)
         while len(self.rows) < cfg.max_rows:                                       # L3
             if self.branch_queue:                                                  # L4
                 rs, j = self.branch_queue[0]
@@ -324,6 +333,8 @@ class Engine:
                 self.branch_queue.popleft()                                        # L5
                 self.committed += self.row_commit()
                 row = Row(rs=rs, b=j)
+                if rs.window_prefill == self.window:          # R44: after its prefix is complete
+                    row.start = rs.ready_wstep
                 row.blocks = self._pop(cdiv(min(cfg.T, cfg.cap), cfg.block_size))
                 rs.branch_state[j] = RUNNING
                 self.rows.append(row)
@@ -334,6 +345,10 @@ class Engine:
                     break
                 self.request_queue.popleft()
                 self._prefill(req)                                                 # L7
+                P = len(req.prompt)
+                pf_tok += P - 1
+                if cfg.prefill_chunk > 0 and P > 1:   # R44: the chunk holding its last prefix token
+                    self.live[req.request_id].ready_wstep = min((pf_tok - 1) // cfg.prefill_chunk + 1, cfg.T)
             else:
                 break                                                              # L8-9
 
@@ -346,7 +361,7 @@ class Engine:
                 self._es_stop(wstep)
                 if not any(r.running for r in self.rows):                         # R31
                     break
-            run = [r for r in self.rows if r.running]
+            run = [r for r in self.rows if r.running and r.start <= wstep]
             ys = self.src.step(run, wstep)
             for r, y in zip(run, ys):
                 s = r.ell + 1
@@ -362,6 +377,8 @@ class Engine:
             self.steps += 1
             if not any(r.running for r in self.rows):                             # R31
                 break
+        for r in self.rows:          # R44: later windows start every row at step 1
+            r.start = 1
         return wstep
 
     def _es_stop(self, wstep: int) -> None:

@@ -15,6 +15,7 @@ typedef __nv_bfloat16 bf16;
 #define ST_PRUNED 4
 #define ST_ES 5
 #define ST_STOP 7             // es_every_step (R43): stopped mid-window by early stop, EarlyStopped at the boundary
+#define ST_WAIT 8             // R44: admitted, waiting for its interleaved prefill (starts at rows.start)
 
 template <typename T> __device__ __forceinline__ float to_f(T x);
 template <> __device__ __forceinline__ float to_f<float>(float x) { return x; }
@@ -59,6 +60,7 @@ struct Rows {
   int* tok;       // next input token
   int* term;      // terminal state decided at the boundary
   int* nblk;      // blocks owned
+  int* start;     // R44: first window step it decodes in its first window (status ST_WAIT until then)
   float* score;
   int* table;     // [R][MBR]
 };

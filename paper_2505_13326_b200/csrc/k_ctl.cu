@@ -52,6 +52,7 @@ __device__ __forceinline__ void copy_row(const Dims& D, Rows dst, int di, Rows s
   dst.tok[di] = src.tok[si];
   dst.term[di] = src.term[si];
   dst.nblk[di] = src.nblk[si];
+  dst.start[di] = src.start[si];
   dst.score[di] = src.score[si];
   for (int j = 0; j < src.nblk[si]; ++j) dst.table[(long long)di * D.MBR + j] = src.table[(long long)si * D.MBR + j];
 }
@@ -114,7 +115,8 @@ __global__ void __launch_bounds__(NT) k_admit(const AdmitEvent* __restrict__ ev,
       rows.slot[r] = slot;
       rows.b[r] = E.b;
       rows.ell[r] = 0;
-      rows.status[r] = RUNNING_ST;
+      rows.start[r] = E.start;
+      rows.status[r] = E.start > 1 ? ST_WAIT : RUNNING_ST;   // R44: waits for its interleaved prefill
       rows.done_step[r] = 0;
       rows.done_wstep[r] = 0;
       rows.nbnd[r] = 0;
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(NT) k_boundary(Dims D, Rows rows, Rows tmp, Re
     const int slot = rows.slot[r], b = rows.b[r];
     const long long sb = (long long)slot * SART_MAXN + b;
     float score;
-    if (rows.status[r] == RUNNING_ST || rows.status[r] == ST_STOP) {   // incomplete: running score (R43)
+    if (rows.status[r] == RUNNING_ST || rows.status[r] == ST_STOP || rows.status[r] == ST_WAIT) {   // incomplete (R43, R44)
       const int k = rows.nbnd[r];
       score = reqs.has_script[slot] ? reqs.sc_scores[sb * D.nbnd_max + min(k, reqs.nbnd[slot] - 1)] : prm[r];
       rows.nbnd[r] = k + 1;
@@ -198,7 +200,8 @@ __global__ void __launch_bounds__(NT) k_boundary(Dims D, Rows rows, Rows tmp, Re
     const int st = has ? rows.status[r] : 0;
     // stopped (es_every_step, R43): incomplete, not prunable, EarlyStopped by the finalize below
     const bool stopped = has && st == ST_STOP;
-    const bool running = has && (st == RUNNING_ST || stopped), done = has && (st == ST_EOS || st == ST_CAP);
+    const bool running = has && (st == RUNNING_ST || stopped || st == ST_WAIT),
+               done = has && (st == ST_EOS || st == ST_CAP);
     const float sc = has ? rows.score[r] : 0.f;
     int phase = reqs.phase[slot], maxp = reqs.maxp[slot], nc = reqs.nc[slot], np = reqs.np[slot];
     float thr = reqs.thr[slot];

@@ -131,9 +131,14 @@ int sample_chunks(int V) { return (V + SCHUNK - 1) / SCHUNK; }
 // Start of a decode step.  es_every_step (reading R43): a running row whose request already
 // has M completed branches -- counted at the end of the previous step -- stops here: it keeps
 // the steps it has (done_step = l) and is EarlyStopped at the boundary.
-__global__ void k_step_begin(Ctr* ctr, int es, Dims D, Rows rows, Reqs reqs, int n) {
+__global__ void k_step_begin(Ctr* ctr, int es, int wake, Dims D, Rows rows, Reqs reqs, int n) {
   pdl_wait();
   pdl_trigger();
+  if (wake) {   // R44: rows whose interleaved prefill has completed start decoding at this step
+    for (int r = threadIdx.x; r < n; r += blockDim.x)
+      if (rows.status[r] == ST_WAIT && rows.start[r] <= ctr->wstep + 1) rows.status[r] = RUNNING_ST;
+    __syncthreads();
+  }
   if (es) {
     int stopped = 0;
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
@@ -151,6 +156,6 @@ __global__ void k_step_begin(Ctr* ctr, int es, Dims D, Rows rows, Reqs reqs, int
   }
   if (threadIdx.x == 0 && ctr->live > 0) { ctr->wstep += 1; ctr->steps += 1; }
 }
-void launch_step_begin(Ctr* ctr, int es, Dims D, Rows rows, Reqs reqs, int n, cudaStream_t s) {
-  launch_pdl(k_step_begin, dim3(1), dim3(es ? 1024 : 1), 0, s, ctr, es, D, rows, reqs, n);
+void launch_step_begin(Ctr* ctr, int es, int wake, Dims D, Rows rows, Reqs reqs, int n, cudaStream_t s) {
+  launch_pdl(k_step_begin, dim3(1), dim3(es || wake ? 1024 : 1), 0, s, ctr, es, wake, D, rows, reqs, n);
 }

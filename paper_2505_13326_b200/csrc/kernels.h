@@ -150,13 +150,14 @@ void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg,
 void launch_sample(const float* logits, Dims D, Rows rows, Reqs reqs, Ctr* ctr, int n, int* dbg_tok, float* pkey,
                    int* pv, cudaStream_t s);
 int sample_chunks(int V);
-void launch_step_begin(Ctr* ctr, int es, Dims D, Rows rows, Reqs reqs, int n, cudaStream_t s);
+void launch_step_begin(Ctr* ctr, int es, int wake, Dims D, Rows rows, Reqs reqs, int n, cudaStream_t s);
 
 // ---- control (k_ctl.cu)
 // type 0 = prefill (pop the prefix blocks, init meta[i], Alg. 1 L16), 1 = new row (L5)
 struct AdmitEvent {
   int type, slot, b, pop_off, row, first_tok;
   int N, M, P, beta, prune, npre, has_script, has_answer, has_forced, nbnd;
+  int start;   // new row: window step of its first decode (R44; 1 = immediately)
   float alpha;
   long long id;
 };

@@ -106,6 +106,12 @@ struct sart_ctx {
   int4* d_pf_blocks = nullptr;
   cudaEvent_t pf_ev[2] = {nullptr, nullptr};
   bool pf_pending = false;
+  // R44 (row f1): chunked prefill interleaved with the window's decode steps
+  int pf_chunk = 0;            // tokens per interleaved chunk (0: inline prefill)
+  int pf_ntok = 0, pf_done = 0;   // this fill's prefill tokens, tokens already processed
+  std::vector<int> fill_ready;    // per slot: start step of the rows of a request prefilled in this fill
+  std::vector<cudaEvent_t> step_ev;   // profile mode: per-step completion events of a window
+  double first_step_ms_max = 0, step_ms_max = 0;
   AdmitEvent* d_events = nullptr;
   int ev_cap = 0;
   AttnPlan plan{};
@@ -255,7 +261,8 @@ cudaError_t dalloc(sart_ctx* ctx, P** p, size_t bytes, bool zero = true) {
 cudaError_t alloc_rows(sart_ctx* ctx, Rows& r) {
   const Dims& D = ctx->D;
   cudaError_t e;
-  int** ints[] = {&r.slot, &r.b, &r.ell, &r.status, &r.done_step, &r.done_wstep, &r.nbnd, &r.tok, &r.term, &r.nblk};
+  int** ints[] = {&r.slot, &r.b, &r.ell, &r.status, &r.done_step, &r.done_wstep, &r.nbnd, &r.tok, &r.term, &r.nblk,
+                  &r.start};
   for (auto p : ints)
     if ((e = dalloc(ctx, p, sizeof(int) * D.R)) != cudaSuccess) return e;
   if ((e = dalloc(ctx, &r.score, sizeof(float) * D.R)) != cudaSuccess) return e;
@@ -444,7 +451,7 @@ void decode_step(sart_ctx* ctx, int n) {
   const Dims& D = ctx->D;
   cudaStream_t s = ctx->st;
   const int ab = ctx->ablate;
-  launch_step_begin(ctx->ctr, ctx->cfg.es_every_step, D, ctx->rows, ctx->reqs, n, s);
+  launch_step_begin(ctx->ctr, ctx->cfg.es_every_step, ctx->pf_chunk > 0, D, ctx->rows, ctx->reqs, n, s);
   launch_embed<T>(ctx->rows.tok, ctx->W_<T>(t_embed()), ctx->h, n, D.d, s);
   ctx->launches += 2;
   if (ctx->cfg.profile) {
@@ -485,11 +492,11 @@ void decode_step(sart_ctx* ctx, int n) {
 // ctx is the decoder being prefilled (the policy, or the f2 PRM model into its own pool);
 // src holds the batch's token lists (always the policy ctx).
 template <typename T>
-void prefill_batch(sart_ctx* ctx, sart_ctx* src, int ntok) {
+void prefill_batch(sart_ctx* ctx, sart_ctx* src, int t_begin, int t_end) {
   const Dims& D = ctx->D;
   cudaStream_t s = ctx->st;
-  for (int t0 = 0; t0 < ntok; t0 += ctx->PC) {
-    const int c = std::min(ctx->PC, ntok - t0);
+  for (int t0 = t_begin; t0 < t_end; t0 += ctx->PC) {
+    const int c = std::min(ctx->PC, t_end - t0);
     const RopeArgs ra{src->d_pf_slot + t0, src->d_pf_pos + t0};
     // 64-position query blocks of each request segment of this chunk (tensor-core prefill)
     int nqb = 0;
@@ -701,12 +708,31 @@ int upload_request(sart_ctx* ctx, const HostReq& q, int slot) {
   return SART_OK;
 }
 
+// Prefill tokens [pf_done, upto) of this fill's batch (policy, then the f2 PRM model's cache).
+int run_prefill(sart_ctx* ctx, int upto) {
+  upto = std::min(upto, ctx->pf_ntok);
+  if (upto <= ctx->pf_done) return SART_OK;
+  if (ctx->bf16) prefill_batch<bf16>(ctx, ctx, ctx->pf_done, upto);
+  else prefill_batch<float>(ctx, ctx, ctx->pf_done, upto);
+  if (ctx->prm) {   // f2: the PRM model's own prefix KV (same block ids)
+    if (ctx->bf16) prefill_batch<bf16>(ctx->prm, ctx, ctx->pf_done, upto);
+    else prefill_batch<float>(ctx->prm, ctx, ctx->pf_done, upto);
+    ctx->launches += ctx->prm->launches;
+    ctx->prm->launches = 0;
+    if (ctx->prm->gemm_failed) return set_err(SART_EINVAL, "GEMM shape unsupported by the tcgen05 kernel (PRM model)");
+  }
+  ctx->pf_done = upto;
+  CK(cudaGetLastError());
+  return SART_OK;
+}
+
 int fill(sart_ctx* ctx) {
   const Dims& D = ctx->D;
   const int RC = cdiv(D.cap, D.bs);
   const int nfirst = cdiv(std::min(D.T, D.cap), D.bs);
   std::vector<AdmitEvent> ev;
   int pop_off = 0, new_rows = 0, commit_delta = 0;
+  std::fill(ctx->fill_ready.begin(), ctx->fill_ready.end(), 1);
   while (ctx->n_rows + new_rows < ctx->cfg.max_rows) {  // L3
     if (!ctx->branch_queue.empty()) {                   // L4-5
       auto [slot, b] = ctx->branch_queue.front();
@@ -721,6 +747,7 @@ int fill(sart_ctx* ctx) {
       e.pop_off = pop_off;
       e.row = ctx->n_rows + new_rows;
       e.first_tok = ctx->slots[slot].first_tok;   // prompt[P-1] (R22)
+      e.start = ctx->fill_ready[slot];            // R44: 1 unless its prefix is prefilled in this window
       ev.push_back(e);
       pop_off += nfirst;
       new_rows++;
@@ -761,6 +788,8 @@ int fill(sart_ctx* ctx) {
         ctx->pf_slot.push_back(slot);
         ctx->pf_pos.push_back(p);
       }
+      if (ctx->pf_chunk > 0 && P > 1)   // R44: its rows start at the step whose chunk completes the prefix
+        ctx->fill_ready[slot] = std::min(((int)ctx->pf_tok.size() - 1) / ctx->pf_chunk + 1, D.T);
       SlotInfo& si = ctx->slots[slot];
       si.id = q.id;
       si.N = q.N;
@@ -783,24 +812,20 @@ int fill(sart_ctx* ctx) {
     CK(xfer(ctx, ctx->d_prompt, ctx->pf_tok.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
     CK(xfer(ctx, ctx->d_pf_slot, ctx->pf_slot.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
     CK(xfer(ctx, ctx->d_pf_pos, ctx->pf_pos.data(), 4 * (size_t)ntok, cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaEventRecord(ctx->pf_ev[0], ctx->st));
     ctx->pf_slot_h.swap(ctx->pf_slot);
     ctx->pf_pos_h.swap(ctx->pf_pos);
-    if (ctx->bf16) prefill_batch<bf16>(ctx, ctx, ntok);
-    else prefill_batch<float>(ctx, ctx, ntok);
-    if (ctx->prm) {   // f2: the PRM model's own prefix KV (same block ids)
-      if (ctx->bf16) prefill_batch<bf16>(ctx->prm, ctx, ntok);
-      else prefill_batch<float>(ctx->prm, ctx, ntok);
-      ctx->launches += ctx->prm->launches;
-      ctx->prm->launches = 0;
-      if (ctx->prm->gemm_failed) return set_err(SART_EINVAL, "GEMM shape unsupported by the tcgen05 kernel (PRM model)");
-    }
-    CK(cudaEventRecord(ctx->pf_ev[1], ctx->st));
-    CK(cudaGetLastError());
-    ctx->pf_pending = true;
     ctx->pf_tok.clear();
     ctx->pf_slot.clear();
     ctx->pf_pos.clear();
+    ctx->pf_ntok = ntok;
+    ctx->pf_done = 0;
+    if (ctx->pf_chunk == 0) {   // Alg. 1 L7: the whole batch before the window's first decode step
+      CK(cudaEventRecord(ctx->pf_ev[0], ctx->st));
+      int rc = run_prefill(ctx, ntok);
+      if (rc) return rc;
+      CK(cudaEventRecord(ctx->pf_ev[1], ctx->st));
+      ctx->pf_pending = true;
+    }
   }
   return SART_OK;
 }
@@ -1045,6 +1070,10 @@ int run_window(sart_ctx* ctx) {
   }
   constexpr int POLL = 16;
   int polls = 0;
+  // profile mode: per-step completion times; step_ev[0] was recorded by sart_step before the
+  // fill, so an inline prefill counts toward the first step (R44 stall measurement)
+  const bool step_times = ctx->cfg.profile != 0 && (int)ctx->step_ev.size() > D.T;
+  int steps_launched = 0;
   for (int k = 1; k <= D.T; ++k) {
     if (k > 1 && (k % POLL) == 1) {
       if (polls >= 2) {   // bound the run-ahead: wait for the poll two periods back
@@ -1058,12 +1087,23 @@ int run_window(sart_ctx* ctx) {
           ctx->h_live[(polls - 2) & 1] == 0)
         break;
     }
+    if (ctx->pf_done < ctx->pf_ntok) {   // R44: chunk k-1 before step k (all the rest before step T)
+      const int upto = k < D.T ? k * ctx->pf_chunk : ctx->pf_ntok;
+      const int rc = run_prefill(ctx, upto);
+      if (rc) return rc;
+    }
     if (graph) {
       CK(cudaGraphLaunch(ctx->step_exec, ctx->st));
       ctx->launches += per_step;
     } else {
       decode_step<T>(ctx, n);
     }
+    if (step_times) CK(cudaEventRecord(ctx->step_ev[k], ctx->st));
+    steps_launched = k;
+  }
+  if (ctx->pf_done < ctx->pf_ntok) {   // a window that ended early (R31) still completes this fill's prefixes
+    const int rc = run_prefill(ctx, ctx->pf_ntok);
+    if (rc) return rc;
   }
   CK(cudaGetLastError());
   if (ctx->gemm_failed) return set_err(SART_EINVAL, "GEMM shape unsupported by the tcgen05 kernel");
@@ -1100,6 +1140,18 @@ int run_window(sart_ctx* ctx) {
               (long long)(hts[i][4] - hts[i][0]), (long long)(hts[i][5] - hts[i][0]), (long long)(hts[i][6] - hts[i][0]),
               (long long)(hts[i][7] - hts[i][0]), (long long)(hts[i][8] - hts[i][0]));
     }
+  }
+  if (step_times && steps_launched > 0) {   // window start -> first decode step done; longest step
+    float first = 0.f, mx = 0.f;
+    cudaEventElapsedTime(&first, ctx->step_ev[0], ctx->step_ev[1]);
+    mx = first;
+    for (int k = 2; k <= steps_launched; ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->step_ev[k - 1], ctx->step_ev[k]);
+      mx = std::max(mx, ms);
+    }
+    ctx->first_step_ms_max = std::max(ctx->first_step_ms_max, (double)first);
+    ctx->step_ms_max = std::max(ctx->step_ms_max, (double)mx);
   }
   if (ctx->cfg.profile) {
     for (int i = 0; i + 1 < ctx->ev_used; i += 2) {
@@ -1283,6 +1335,7 @@ int sart_destroy(sart_ctx* ctx) {
   for (auto e : ctx->prm_ev)
     if (e) cudaEventDestroy(e);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (auto e : ctx->step_ev) cudaEventDestroy(e);
   for (auto e : ctx->poll_ev)
     if (e) cudaEventDestroy(e);
   for (auto e : ctx->pf_ev)
@@ -1332,6 +1385,7 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   if (cfg.es_every_step != 0 && cfg.es_every_step != 1) return set_err(SART_EINVAL, "es_every_step must be 0 or 1");
   if (cfg.record_trace != 0 && cfg.record_trace != 1) return set_err(SART_EINVAL, "record_trace must be 0 or 1");
   if (cfg.kv_pool && cfg.kv_pool_bytes == 0) return set_err(SART_EINVAL, "kv_pool given with kv_pool_bytes == 0");
+  if (cfg.prefill_chunk < 0 || cfg.prefill_chunk > 2048) return set_err(SART_EINVAL, "prefill_chunk must be in [0, 2048]");
   if (cfg.tp_size == 0) cfg.tp_size = 1;
   if (cfg.tp_size < 1 || cfg.tp_size > SART_MAX_TP || cfg.tp_rank < 0 || cfg.tp_rank >= cfg.tp_size)
     return set_err(SART_EINVAL, "need 1 <= tp_size <= 8 and 0 <= tp_rank < tp_size");
@@ -1370,6 +1424,7 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   D.theta = cfg.rope_theta; D.eps = cfg.rms_eps; D.tau = cfg.temperature; D.seed = cfg.sampler_seed;
   D.select_mode = cfg.select_mode;
   ctx->PC = 2048;   // prefill chunk (tokens)
+  ctx->pf_chunk = cfg.prefill_chunk;
   ctx->W = std::max(D.R, ctx->PC);
   const size_t es = ctx->bf16 ? 2 : 4;
 
@@ -1561,6 +1616,7 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   }
   ctx->free_top = NB;
   ctx->slots.resize(D.S);
+  ctx->fill_ready.assign(D.S, 1);
   ctx->last_slot_id.assign(D.S, -1);
   for (int s = D.S - 1; s >= 0; --s) ctx->free_slots.push_back(s);
   if (cfg.profile) {
@@ -1645,6 +1701,14 @@ int sart_step(sart_ctx* ctx, int32_t max_windows, sart_stats* out) {
   if (ctx->tp > 1 && !ctx->tp_connected) return set_err(SART_ESTATE, "tensor-parallel ctx not connected (sart_tp_connect)");
   cudaSetDevice(ctx->cfg.device);
   for (int w = 0; w < max_windows; ++w) {
+    if (ctx->cfg.profile) {   // window start, before the fill (and an inline prefill)
+      while ((int)ctx->step_ev.size() < ctx->D.T + 1) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return set_err(SART_ECUDA, "event create");
+        ctx->step_ev.push_back(e);
+      }
+      if (cudaEventRecord(ctx->step_ev[0], ctx->st) != cudaSuccess) return set_err(SART_ECUDA, "event record");
+    }
     int rc = fill(ctx);
     if (rc) return rc;
     if (ctx->n_rows == 0) break;   // idle
@@ -2014,6 +2078,8 @@ int sart_get_profile(sart_ctx* ctx, sart_profile* o) {
   o->prm_passes = ctx->prm_passes;
   o->h2d_bytes = ctx->h2d_bytes;
   o->d2h_bytes = ctx->d2h_bytes;
+  o->first_step_ms_max = ctx->first_step_ms_max;
+  o->step_ms_max = ctx->step_ms_max;
   return SART_OK;
 }
 int sart_set_profile(sart_ctx* ctx, int32_t enable) {
@@ -2034,6 +2100,7 @@ int sart_reset_profile(sart_ctx* ctx) {
   ctx->prm_tokens = ctx->prm_passes = 0;
   ctx->attn_launches = ctx->launches = 0;
   ctx->h2d_bytes = ctx->d2h_bytes = 0;
+  ctx->first_step_ms_max = ctx->step_ms_max = 0;
   return SART_OK;
 }
 

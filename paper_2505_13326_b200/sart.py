@@ -46,6 +46,7 @@ class SartConfig(C.Structure):
         ("prm_weight_seed", C.c_uint64), ("prm_host_weights", C.c_void_p),
         ("kv_pool", C.c_void_p), ("kv_pool_bytes", C.c_size_t), ("es_every_step", C.c_int32),
         ("record_trace", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32),
+        ("prefill_chunk", C.c_int32),
     ]
 
 
@@ -104,7 +105,7 @@ class SartProfile(C.Structure):
     _fields_ = [("attn_ms", C.c_double), ("attn_launches", C.c_int64), ("attn_bytes", C.c_double),
                 ("kernel_launches", C.c_int64), ("prefill_ms", C.c_double), ("prm_ms", C.c_double),
                 ("prm_tokens", C.c_int64), ("prm_passes", C.c_int64), ("h2d_bytes", C.c_int64),
-                ("d2h_bytes", C.c_int64)]
+                ("d2h_bytes", C.c_int64), ("first_step_ms_max", C.c_double), ("step_ms_max", C.c_double)]
 
 
 _lib = None
@@ -228,7 +229,8 @@ class Engine:
                  attn_mode: int = SART_ATTN_CASCADE, device: int = 0, stream: int = 0,
                  enable_forced_tokens: bool = False, debug_capture: bool = False, profile: bool = False,
                  prm_shape=None, prm_host_weights: Optional[np.ndarray] = None, prm_weight_seed: int = 0,
-                 kv_pool=None, es_every_step: bool = False, record_trace: bool = False, tp=(1, 0)):
+                 kv_pool=None, es_every_step: bool = False, record_trace: bool = False, tp=(1, 0),
+                 prefill_chunk: int = 0):
         """prm_shape (a synth.ModelShape, vocab = the policy's): the separate PRM decoder of
         row f2; None -> the PRM head on the policy's hidden state.  kv_pool: (device address,
         bytes) of a caller-owned KV pool buffer (e.g. a torch tensor's data_ptr() and nbytes;
@@ -258,6 +260,7 @@ class Engine:
             cfg.kv_pool, cfg.kv_pool_bytes = int(kv_pool[0]), int(kv_pool[1])
         cfg.es_every_step, cfg.record_trace = int(es_every_step), int(record_trace)
         cfg.tp_size, cfg.tp_rank = int(tp[0]), int(tp[1])
+        cfg.prefill_chunk = int(prefill_chunk)
         self.tp = max(1, int(tp[0]))
         self._prm_weights = None
         if prm_shape is not None:

@@ -11,9 +11,9 @@ def gpu_engine(shape, dtype="bf16", weights=None, **kw):
     return Engine(shape, dtype, host_weights=blob, **kw)
 
 
-def oracle_engine(bs, nb, T, cap, B=1 << 30, eos=1, select=0, source=None, es=False):
+def oracle_engine(bs, nb, T, cap, B=1 << 30, eos=1, select=0, source=None, es=False, prefill_chunk=0):
     cfg = EngineConfig(block_size=bs, num_blocks=nb, max_rows=B, T=T, cap=cap, eos_id=eos, select_mode=select,
-                       es_every_step=es)
+                       es_every_step=es, prefill_chunk=prefill_chunk)
     return OEngine(cfg, source if source is not None else ScriptedSource(eos))
 
 

@@ -17,10 +17,11 @@ from synth import SHAPES, gen_requests, gen_weights
 pytestmark = pytest.mark.gpu
 
 
-def run_pair(shape, reqs, bs, nb, T, cap, B, select=0, windows=100000, check_every=1, es=False):
+def run_pair(shape, reqs, bs, nb, T, cap, B, select=0, windows=100000, check_every=1, es=False, prefill_chunk=0):
     g = gpu_engine(shape, "bf16", None, block_size=bs, num_blocks=nb, max_rows=B, max_requests=64, max_prompt=2048,
-                   T=T, cap=cap, eos_id=1, select_mode=select, weight_seed=3, es_every_step=es)
-    o = oracle_engine(bs, nb, T, cap, B=B, select=select, es=es)
+                   T=T, cap=cap, eos_id=1, select_mode=select, weight_seed=3, es_every_step=es,
+                   prefill_chunk=prefill_chunk)
+    o = oracle_engine(bs, nb, T, cap, B=B, select=select, es=es, prefill_chunk=prefill_chunk)
     for r in reqs:
         g.admit(r)
         o.admit(r)
@@ -170,3 +171,20 @@ def test_es_every_step_random_workloads(seed):
     reqs = _mixed_requests(rng, shape, 40, cap, T, 0, 70 + seed)
     need = max(-(-(len(r.prompt) - 1) // bs) for r in reqs) + -(-cap // bs)
     run_pair(shape, reqs, bs, int(need * 5), T, cap, B=int(rng.integers(8, 96)), es=True)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_interleaved_prefill_random_workloads(seed):
+    """Reading R44 (row f1): prefill chunks interleaved with decode steps -- rows of a request
+    prefilled in the window start at the step its last chunk precedes.  Chunks of 8-48 tokens
+    over prompts of up to 150 tokens spread a fill's prefill over many steps; mixed N / M /
+    alpha / beta, tight pools, es_every_step on half the seeds: bit-exact every window."""
+    rng = np.random.default_rng(900 + seed)
+    shape = SHAPES["tiny"]
+    bs = int(rng.choice([16, 64]))
+    T = int(rng.choice([4, 16, 40]))
+    cap = int(rng.integers(16, 100))
+    reqs = _mixed_requests(rng, shape, 30, cap, T, 0, 90 + seed)
+    need = max(-(-(len(r.prompt) - 1) // bs) for r in reqs) + -(-cap // bs)
+    run_pair(shape, reqs, bs, int(need * 5), T, cap, B=int(rng.integers(8, 96)), es=bool(seed % 2),
+             prefill_chunk=int(rng.choice([8, 16, 48])))

@@ -311,3 +311,51 @@ def test_sampler_full_vocab_1p5b(tau):
     g.close()
     print(f"PP3 full vocab tau={tau}: {n_cmp} row-steps, {n_tie} near-ties, {n_eos} scripted EOS")
     assert n_cmp >= 500 and n_tie <= 2 and n_eos >= 4
+
+
+def test_interleaved_prefill_teacher_forced():
+    """Reading R44 (row f1): with 16-token prefill chunks interleaved with the decode steps, the
+    rows of later prompts start mid-window; every row's logits at the end of each window still
+    match the fp64 oracle at that row's own step count (PP1)."""
+    shape = SHAPES["small"]
+    weights = gen_weights(shape, "bf16", std=0.02, root_seed=7)
+    model = Model(shape, weights)
+    prompts = [gen_prompt(31, shape.vocab, EOS, 20, 20), gen_prompt(32, shape.vocab, EOS, 45, 45),
+               gen_prompt(33, shape.vocab, EOS, 70, 70)]
+    T, cap, N = 8, 24, 2
+    rng = np.random.default_rng(7)
+    forced = {rid: rng.integers(2, shape.vocab, size=(N, cap)).astype(np.int32) for rid in range(3)}
+    g = gpu_engine(shape, "bf16", weights, block_size=16, num_blocks=1024, max_rows=64, max_requests=8,
+                   max_prompt=80, T=T, cap=cap, eos_id=EOS, enable_forced_tokens=True, prefill_chunk=16)
+    for rid, p in enumerate(prompts):
+        g.admit(Request(rid, p, N, N, -1.0, 0, None), forced_tokens=forced[rid])
+    ref = {}
+    for rid, p in enumerate(prompts):
+        pre = model.prefill(p)
+        for b in range(N):
+            suf = [{"k": [], "v": []} for _ in range(shape.n_layers)]
+            for s in range(1, cap + 1):
+                tok = p[-1] if s == 1 else forced[rid][b, s - 2]
+                _, lg = model.decode(np.array([tok]), np.array([len(p) - 2 + s]), [pre], [suf])
+                ref[(rid, b, s)] = lg[0]
+    starts = set()
+    worst = 0.0
+    for w in range(6):
+        st = g.step(1)
+        ids = g.debug_fetch(DBG_ROWIDS)
+        if len(ids) == 0:
+            break
+        lg = g.debug_fetch(DBG_LOGITS)
+        ell = {(r[0], r[1]): r[2] for r in g.state()["rows"]}
+        for i, key in enumerate(ids):
+            rid, b = int(key) >> 8, int(key) & 0xFF
+            s = ell.get((rid, b), cap)          # finished rows have left the batch at the cap
+            if w == 0:
+                starts.add(s)
+            e = rel_err_rows(lg[i], ref[(rid, b, s)])[0]
+            worst = max(worst, e)
+            assert e <= 2e-2, (rid, b, s, e)
+    g.close()
+    # prefixes 19 / 44 / 69 tokens -> batch ends 19, 63, 132 -> chunks 1, 3, 8 -> starts 2, 4, 8
+    assert starts == {T - 1, T - 3, T - 7}, starts
+    print("interleaved prefill worst logits", worst)

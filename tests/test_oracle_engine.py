@@ -339,3 +339,57 @@ def test_prm_model_source_scores_the_read_prefix():
         seq = [int(t) for t in prompt] + [int(t) for t in forced[b, : L - 1]]
         assert r["branch_score"][b] == np.float32(pm.prm_model_score(seq))
     assert e.stats()["free_blocks"] == 64
+
+
+# ------------------------------------------------------------------ R44: interleaved prefill
+def _engine_pc(T, cap, pc, bs=16, nb=4096, B=1 << 30):
+    return Engine(EngineConfig(block_size=bs, num_blocks=nb, max_rows=B, T=T, cap=cap, eos_id=1,
+                               prefill_chunk=pc), ScriptedSource(1))
+
+
+def test_interleaved_prefill_start_steps():
+    """Three requests prefilled in one fill with 10, 25 and 5 prefix tokens and 16-token chunks:
+    the batch is [0, 10) [10, 35) [35, 40), chunks [0,16) [16,32) [32,48) run before steps 1,
+    2, 3, so the requests' rows start at steps 1, 3 and 3 and have 8, 6, 6 tokens after an
+    8-step window (lengths longer than the window, pruning off)."""
+    e = _engine_pc(T=8, cap=64, pc=16)
+    for rid, P in enumerate((11, 26, 6)):
+        e.admit(mk_req(rid, [50, 50], np.zeros((2, 8)), M=2, alpha=-1.0, beta=0, P=P))
+    e.step(1)
+    ells = {(r[0], r[1]): r[2] for r in e.snapshot()["rows"]}
+    assert ells == {(0, 0): 8, (0, 1): 8, (1, 0): 6, (1, 1): 6, (2, 0): 6, (2, 1): 6}
+    e.step(1)                                   # the next window starts every row at step 1
+    assert {(r[0], r[1]): r[2] for r in e.snapshot()["rows"]} == {k: v + 8 for k, v in ells.items()}
+
+
+def test_interleaved_prefill_one_chunk_equals_inline():
+    """A chunk that holds every fill's whole batch is inline prefill: identical snapshots and
+    records on random scripted workloads."""
+    rng = np.random.default_rng(44)
+    for seed in range(4):
+        reqs = gen_requests(8, SHAPES["tiny"], 4, 2, 0.5, 2, 48, 8, eos_id=1, p_range=(2, 60), length="uniform",
+                            len_range=(1, 48), root_seed=seed)
+        a, b = _engine_pc(8, 48, 0, nb=120, B=12), _engine_pc(8, 48, 10 ** 6, nb=120, B=12)
+        for r in reqs:
+            a.admit(r)
+            b.admit(r)
+        for _ in range(200):
+            a.step(1)
+            b.step(1)
+            assert a.snapshot() == b.snapshot()
+        assert a.collect() == b.collect()
+
+
+def test_interleaved_prefill_keeps_branch_lengths():
+    """With M = N and pruning off every branch completes at its scripted length, whatever step
+    it starts at: interleaving changes when rows decode, never what they decode."""
+    for pc in (4, 16, 64):
+        e = _engine_pc(T=6, cap=40, pc=pc, nb=400, B=10)
+        reqs = gen_requests(6, SHAPES["tiny"], 3, 3, -1.0, 0, 40, 6, eos_id=1, p_range=(10, 90), length="uniform",
+                            len_range=(1, 40), root_seed=pc)
+        for r in reqs:
+            e.admit(r)
+        e.step(1000)
+        res = {x["request_id"]: x for x in e.collect()}
+        for r in reqs:
+            assert res[r.request_id]["branch_len"] == [int(x) for x in r.script.forced_len]
