@@ -622,6 +622,241 @@ __global__ void __launch_bounds__(Epi<MODE>::NTHREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ CTA-pair variant
+// cta_group::2 (two SMs of a TPC cooperate on one MMA): a pair tile is 256 rows x NP columns.
+// CTA r of the pair loads its own 128 A rows and half of the pair's B rows (for each 256-column
+// MMA chunk c: B rows [c 256 + r 128, +128)), so per SM the operand bytes per flop drop by a
+// quarter (NP = 256) to a third (NP = 512) against the one-SM 256 x 256 tile -- the decode GEMMs
+// are bound by per-SM operand delivery (profiles/r2_gemm_phase_ts.txt).  Only the leader (even
+// CTA) issues tcgen05.mma.cta_group::2; both CTAs' TMA loads complete on the leader's stage
+// barrier; the leader's commits multicast to both CTAs' stage-empty / accumulator-full barriers;
+// both CTAs' epilogue warps release the accumulator on the leader's barrier.  Each CTA's TMEM
+// holds its own 128 rows x NP columns, so the epilogue is the one-SM epilogue on 128 rows.
+// Modes: GEMM_STORE (split-K partial or bias store) and GEMM_SWIGLU (NP / 256 interleaved
+// [gate 128 | up 128] tiles).  Every output element accumulates the same K-blocks in the same
+// order as the one-SM kernel.
+template <int NP>
+struct Smem2 {
+  static constexpr int BH = NP / 2;                                      // B rows per CTA
+  static constexpr int STAGES = (192 * 1024) / ((BM + BH) * BK * 2);
+  alignas(1024) bf16 a[STAGES][BM * BK];
+  alignas(1024) bf16 b[STAGES][BH * BK];
+  uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  uint32_t tmem_base;
+  alignas(16) float slab[4][32 * 32];
+};
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// TMA load whose bytes complete on the PAIR LEADER's barrier (CUTLASS SM100_TMA_2SM_LOAD_2D:
+// clearing bit 24 of the shared::cluster barrier address selects the even CTA of the pair)
+__device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_2sm(uint64_t* bar) {   // arrive on bar in BOTH CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int NP, int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Epi<MODE>::NTHREADS, 1)
+    k_gemm_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* C,
+               const float* __restrict__ bias, bf16* act, int M, int N, int K, int S) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Smem2<NP>& sm = *reinterpret_cast<Smem2<NP>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int STAGES = Smem2<NP>::STAGES, BH = Smem2<NP>::BH;
+  constexpr int NEPI = Epi<MODE>::NEPI, CSTEP = Epi<MODE>::CSTEP;
+  constexpr int NBUF = 2 * NP <= 512 ? 2 : 1, TCOLS = NBUF * NP;
+  constexpr uint32_t PAIR_TX = 2u * (BM + BH) * BK * 2;   // bytes of one stage over both CTAs
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int mt = (M + 2 * BM - 1) / (2 * BM), nt = (N + NP - 1) / NP, ntiles = mt * nt * S;
+  const int kb_all = (K + BK - 1) / BK;
+  auto unit_of = [&](int t, int& m0, int& n0, int& kb0, int& kb1, int& sp) {
+    m0 = (t % mt) * (2 * BM) + (int)rank * BM;   // this CTA's 128 rows of the pair's 256
+    const int rest = t / mt;
+    sp = rest % S;
+    n0 = (rest / S) * NP;
+    kb0 = sp * kb_all / S;
+    kb1 = (sp + 1) * kb_all / S;
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&sm.full[i], 1); mbar_init(&sm.empty[i], 1); }
+    for (int i = 0; i < NBUF; ++i) { mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 2 * NEPI); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();   // both CTAs' barriers initialised and TMEM allocated before any cross-CTA signal
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = sm.tmem_base;
+  if (threadIdx.x == 0) pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+      auto load_b = [&](int st, int kbi, int n0_) {
+#pragma unroll
+        for (int c = 0; c < NP / 256; ++c)
+          tma_load_2sm(sm.b[st] + c * 128 * BK, &tmB, &sm.full[st], kbi * BK, n0_ + c * 256 + (int)rank * 128);
+      };
+      int stage = 0;
+      uint32_t phase = 0;
+      bool first = true;
+      for (int t = pair; t < ntiles; t += npairs) {
+        int m0, n0, kb0, kb1, sp;
+        unit_of(t, m0, n0, kb0, kb1, sp);
+        int kb = kb0;
+        if (first) {   // PDL: weight stages before waiting for the previous kernel
+          first = false;
+          const int pre = min(STAGES, kb1 - kb0);
+          for (int i = 0; i < pre; ++i) {
+            if (leader) mbar_expect_tx(&sm.full[i], PAIR_TX);
+            load_b(i, kb0 + i, n0);
+          }
+          pdl_wait();
+          for (int i = 0; i < pre; ++i) tma_load_2sm(sm.a[i], &tmA, &sm.full[i], (kb0 + i) * BK, m0);
+          kb += pre;
+          stage = pre % STAGES;
+          phase = pre == STAGES ? 1 : 0;
+        }
+        for (; kb < kb1; ++kb) {
+          mbar_wait(&sm.empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&sm.full[stage], PAIR_TX);
+          tma_load_2sm(sm.a[stage], &tmA, &sm.full[stage], kb * BK, m0);
+          load_b(stage, kb, n0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+      if (first) pdl_wait();
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // D f32, A/B bf16, K-major, N = 256 per instruction, M = 256 (the pair)
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair; t < ntiles; t += npairs, ++it) {
+        const int as = it % NBUF;
+        const uint32_t aph = (it / NBUF) & 1;
+        int m0, n0, kb0, kb1, sp;
+        unit_of(t, m0, n0, kb0, kb1, sp);
+        mbar_wait(&sm.tempty[as], aph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem + as * NP;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&sm.full[stage], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(sm.a[stage]), b0 = smem_u32(sm.b[stage]);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+#pragma unroll
+              for (int c = 0; c < NP / 256; ++c)
+                umma_bf16_2sm(d + c * 256, umma_desc(a0 + k * 32), umma_desc(b0 + c * 128 * BK * 2 + k * 32), idesc,
+                              (kb > kb0 || k) ? 1u : 0u);
+            umma_commit_2sm(&sm.empty[stage]);
+            if (kb == kb1 - 1) umma_commit_2sm(&sm.tfull[as]);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    pdl_wait();
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&sm.tempty[0]), 0);
+    int it = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++it) {
+      const int as = it % NBUF;
+      const uint32_t aph = (it / NBUF) & 1;
+      int m0, n0, kb0, kb1, sp;
+      unit_of(t, m0, n0, kb0, kb1, sp);
+      mbar_wait(&sm.tfull[as], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int gm = m0 + row;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + as * NP;
+      if constexpr (MODE == GEMM_SWIGLU) {
+        const int F = N / 2;
+#pragma unroll 1
+        for (int g2 = 0; g2 < NP / 256; ++g2) {
+          const int f0 = n0 / 2 + g2 * 128;
+#pragma unroll 1
+          for (int c = half * 32; c < 128; c += CSTEP) {
+            float g[32], u[32];
+            tmem_ld32(tbase + g2 * 256 + c, g);
+            tmem_ld32(tbase + g2 * 256 + 128 + c, u);
+            if (gm < M) {
+              bf16* dst = act + (size_t)gm * F + f0 + c;
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                if (f0 + c + j + 8 <= F) {
+                  __align__(16) bf16 o[8];
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    float x = g[j + e];
+                    o[e] = __float2bfloat16_rn(__fdividef(x, 1.0f + __expf(-x)) * u[j + e]);
+                  }
+                  *reinterpret_cast<uint4*>(dst + j) = *reinterpret_cast<uint4*>(o);
+                }
+              }
+            }
+          }
+        }
+      } else {
+        float* Cs = C + (size_t)sp * M * N;
+        store_tile_f32<NP, GEMM_STORE>(tbase, Cs, m0 + q * 32, n0, M, N, bias, smem_u32(sm.slab[(warp - 2) & 3]), lane,
+                                       half * 32, CSTEP);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0)   // release the accumulator on the LEADER's barrier (both CTAs' epilogues count)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader0 + as * 8)
+                     : "memory");
+    }
+  }
+  __syncwarp();
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();   // the leader's MMAs into this CTA's TMEM / smem are done before either CTA exits
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+}
+
 }  // namespace
 void gemm_ts_reset() { int z = 0; cudaMemcpyToSymbol(g_gemm_ts_idx, &z, 4); }
 void gemm_ts_fetch(unsigned long long* h) { cudaMemcpyFromSymbol(h, g_gemm_ts, sizeof(g_gemm_ts)); }
@@ -693,13 +928,56 @@ bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* 
              t);
   return true;
 }
+template <int NP, int MODE>
+bool launch_2sm(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K, int S,
+                cudaStream_t s) {
+  const CUtensorMap* ma = g_maps.get(A, M, K, BM);
+  const CUtensorMap* mb = g_maps.get(B, N, K, 128);
+  if (!ma || !mb) return false;
+  const size_t smem = sizeof(Smem2<NP>) + 1024;
+  ensure_dyn_smem(k_gemm_2sm<NP, MODE>, (int)smem);
+  const int npairs_max = device_sms() / 2;
+  const int ntiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + NP - 1) / NP) * S;
+  const int pairs = ntiles < npairs_max ? ntiles : npairs_max;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(Epi<MODE>::NTHREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_gemm_2sm<NP, MODE>, *ma, *mb, C, bias, act, M, N, K, S) == cudaSuccess;
+}
 }  // namespace
+// CTA-pair routing (bit mask; SART_GEMM_2SM overrides): 1 = fused gate/up SwiGLU, 2 = split-K
+// long-K projections (down), 4 = LM head
+int gemm_2sm_mask() {
+  static const int v = getenv("SART_GEMM_2SM") ? atoi(getenv("SART_GEMM_2SM")) : 0;
+  return v;
+}
+
+bool launch_gemm_2sm(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
+                     int mode, int S, int NP, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return true;
+  if (K % 8 || N % 256) return false;
+  if (mode == GEMM_SWIGLU && S == 1 && NP == 512) return launch_2sm<512, GEMM_SWIGLU>(A, B, bias, C, act, M, N, K, 1, s);
+  if (mode == GEMM_SWIGLU && S == 1 && NP == 256) return launch_2sm<256, GEMM_SWIGLU>(A, B, bias, C, act, M, N, K, 1, s);
+  if (mode == GEMM_STORE && NP == 256) return launch_2sm<256, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s);
+  if (mode == GEMM_STORE && NP == 512) return launch_2sm<512, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s);
+  return false;
+}
 
 bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
                     int mode, cudaStream_t s, const bf16* Bt) {
   // 256-row tiles (two MMA tiles per weight stage) once they still fill ~3/4 of the SMs:
   // measured 7% faster on the C2 gate/up projection (profiles/r1_gemm_bm256_sweep.txt)
   const int g_num_sms = device_sms();
+  if (!Bt && M > BM && N % 512 == 0 && (gemm_2sm_mask() & (mode == GEMM_SWIGLU ? 1 : 4)) &&
+      (mode == GEMM_SWIGLU || mode == GEMM_STORE))
+    return launch_gemm_2sm(A, B, bias, C, act, M, N, K, mode, 1, mode == GEMM_SWIGLU ? 512 : 256, s);
   const int ms = (mode == GEMM_SWIGLU && M > BM && ((M + 2 * BM - 1) / (2 * BM)) * ((N + 255) / 256) >= g_num_sms * 3 / 4)
                      ? 2 : 1;
   return launch_gemm_tc_split(A, B, bias, C, act, M, N, K, mode, 1, 256, ms, s, Bt);

@@ -95,6 +95,11 @@ void launch_interleave_gate_up(bf16* w, bf16* tmp, int F, int d, cudaStream_t s)
 bool launch_gemm_tc_split(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
                           int mode, int S, int BN, int MSUB, cudaStream_t s, const bf16* Bt = nullptr,
                           const TpOut* tp = nullptr);
+// CTA-pair (cta_group::2) variant: pair tiles 256 x NP (NP 256 / 512), GEMM_STORE (split-K S) or
+// GEMM_SWIGLU (S = 1); returns false for unsupported shapes.  gemm_2sm_mask(): which call sites use it.
+bool launch_gemm_2sm(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
+                     int mode, int S, int NP, cudaStream_t s);
+int gemm_2sm_mask();
 // pre-tiled weight layout for the tcgen05 GEMM (k_gemm_tc.cu)
 size_t tiled_b_elems(int N, int K, int BN);
 void launch_tile_b(const bf16* W, bf16* Wt, int N, int K, int BN, cudaStream_t s);

@@ -316,7 +316,12 @@ int proj(sart_ctx* ctx, const T* A, const T* B, int M, int N, int K) {
   if constexpr (std::is_same<T, bf16>::value) {
     int BN = 256, MS = 1;
     choose_split(M, N, K, S, BN, MS);
-    if (!launch_gemm_tc_split(A, B, nullptr, ctx->parts, nullptr, M, N, K, GEMM_STORE, S, BN, MS, ctx->st))
+    if ((gemm_2sm_mask() & 2) && K >= 4096 && M > 128 && N % 256 == 0) {   // CTA pairs: 256 x 256 pair tiles
+      const int pt = ((M + 255) / 256) * (N / 256);
+      S = std::max(1, std::min(8, std::min((K / 64) / 2, device_sms() / 2 / std::max(1, pt))));
+      if (!launch_gemm_2sm(A, B, nullptr, ctx->parts, nullptr, M, N, K, GEMM_STORE, S, 256, ctx->st))
+        ctx->gemm_failed = true;
+    } else if (!launch_gemm_tc_split(A, B, nullptr, ctx->parts, nullptr, M, N, K, GEMM_STORE, S, BN, MS, ctx->st))
       ctx->gemm_failed = true;
   } else {
     launch_gemm_simt<T>(A, B, nullptr, ctx->parts, M, N, K, GEMM_STORE, ctx->st);
@@ -1857,7 +1862,7 @@ int sart_debug_fetch(sart_ctx* ctx, int32_t what, int32_t layer, void* host_out,
 int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const uint16_t* B, const float* bias,
                     float* C, int32_t mode, int32_t splits, int32_t bn, int32_t bm) {
   if (M < 1 || N < 1 || K < 1 || !A || !B || !C || mode < 0 || mode > 2 || splits < 1 || splits > 8 ||
-      (bn != 64 && bn != 128 && bn != 256) || (bm != 128 && bm != 256))
+      (bn != 64 && bn != 128 && bn != 256 && !(bn == 512 && getenv("SART_DEBUG_2SM"))) || (bm != 128 && bm != 256))
     return set_err(SART_EINVAL, "bad args");
   bf16 *dA = nullptr, *dB = nullptr, *dact = nullptr, *dBt = nullptr;
   float *dC = nullptr, *dbias = nullptr;
@@ -1881,7 +1886,9 @@ int sart_debug_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const ui
       if (e == cudaSuccess) launch_tile_b(dB, dBt, N, K, bn, 0);
     }
     chk(cudaDeviceSynchronize());   // the kernel prefetches B before its PDL wait: B must be resident
-    if (!launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, bm / 128, 0, dBt))
+    if (getenv("SART_DEBUG_2SM")) {   // the CTA-pair kernel on the same problem (pair tile 256 x bn)
+      if (!launch_gemm_2sm(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, 0)) e = cudaErrorInvalidValue;
+    } else if (!launch_gemm_tc_split(dA, dB, dbias, dC, dact, M, N, K, mode, splits, bn, bm / 128, 0, dBt))
       e = cudaErrorInvalidValue;
     chk(cudaGetLastError());
     chk(cudaDeviceSynchronize());

@@ -77,3 +77,26 @@ def test_gemm_split_k(M, N, K, S, BN, BM, tiled, monkeypatch):
     C = parts.astype(np.float64).reshape(-1, M, N).sum(axis=0)   # S = 1 returns [M][N]
     ref = bits_to_f32(A).astype(np.float64) @ bits_to_f32(B).astype(np.float64).T
     assert np.max(np.abs(C - ref)) / np.max(np.abs(ref)) < 1e-4
+
+
+@pytest.mark.parametrize("M,N,K,mode,splits,bn", [
+    (470, 1536, 8960, 0, 6, 256),      # C2 down projection, split-K partials
+    (512, 1536, 8960, 0, 1, 256),
+    (129, 4096, 1536, 0, 1, 256),      # LM-head-like, ragged M (second pair tile = 1 row)
+    (300, 2048, 1536, 0, 1, 512),
+    (470, 17920, 1536, 2, 1, 512),     # C2 fused gate/up SwiGLU (interleaved 256-row tiles)
+    (200, 2048, 640, 2, 1, 256),
+])
+def test_gemm_cta_pair_matches_one_sm(M, N, K, mode, splits, bn, monkeypatch):
+    """The cta_group::2 kernel (pair tile 256 x bn) against the one-SM kernel on the same bf16
+    operands: every output element accumulates the same K-blocks in the same order, so the
+    results are bit-identical (and the one-SM kernel is itself checked against fp64 above)."""
+    rng = np.random.default_rng(M + N + K)
+    A, B = rnd(rng, (M, K)), rnd(rng, (N, K), 0.05)
+    from paper_2505_13326_b200.sart import debug_gemm
+    ref = debug_gemm(A, B, mode=mode, splits=splits, bn=256 if mode == 2 else (128 if bn == 512 else bn))
+    monkeypatch.setenv("SART_DEBUG_2SM", "1")
+    got = debug_gemm(A, B, mode=mode, splits=splits, bn=bn)
+    if splits > 1:
+        got, ref = got.sum(0), ref.sum(0)
+    assert np.array_equal(got, ref), float(np.max(np.abs(got - ref)))
