@@ -295,6 +295,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
         l0 = l0 * c0 + p[0][0] + p[0][1] + p[1][0] + p[1][1];
         l1 = l1 * c1 + p[0][2] + p[0][3] + p[1][2] + p[1][3];
+        // (skipping this rescale when c0 = c1 = 1 is bit-exact but measured neutral:
+        // profiles/r2_attn_lazy_rescale_ab.txt -- the kernel waits on data, not on issue)
 #pragma unroll
         for (int nt = 0; nt < HD / 8; ++nt) { o[nt][0] *= c0; o[nt][1] *= c0; o[nt][2] *= c1; o[nt][3] *= c1; }
         uint32_t pa[4];

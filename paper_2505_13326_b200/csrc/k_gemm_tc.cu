@@ -955,7 +955,9 @@ bool launch_2sm(const bf16* A, const bf16* B, const float* bias, float* C, bf16*
 // CTA-pair routing (bit mask; SART_GEMM_2SM overrides): 1 = fused gate/up SwiGLU, 2 = split-K
 // long-K projections (down), 4 = LM head
 int gemm_2sm_mask() {
-  static const int v = getenv("SART_GEMM_2SM") ? atoi(getenv("SART_GEMM_2SM")) : 0;
+  // default 2: measured on C2 in-graph -- down -0.8%, SwiGLU and LM head neutral (the SwiGLU
+  // mainloop already runs at ~77% of the per-SM MMA rate; profiles/r2_gemm_2sm_ab.txt)
+  static const int v = getenv("SART_GEMM_2SM") ? atoi(getenv("SART_GEMM_2SM")) : 2;
   return v;
 }
 

@@ -316,9 +316,9 @@ int proj(sart_ctx* ctx, const T* A, const T* B, int M, int N, int K) {
   if constexpr (std::is_same<T, bf16>::value) {
     int BN = 256, MS = 1;
     choose_split(M, N, K, S, BN, MS);
-    if ((gemm_2sm_mask() & 2) && K >= 4096 && M > 128 && N % 256 == 0) {   // CTA pairs: 256 x 256 pair tiles
-      const int pt = ((M + 255) / 256) * (N / 256);
-      S = std::max(1, std::min(8, std::min((K / 64) / 2, device_sms() / 2 / std::max(1, pt))));
+    if ((gemm_2sm_mask() & 2) && K >= 4096 && M > 128 && N % 256 == 0 && BN == 256) {
+      // CTA pairs (256 x 256 pair tiles) with the SAME split count, so every split covers the same
+      // K-blocks and the partials are bit-identical to the one-SM kernel's
       if (!launch_gemm_2sm(A, B, nullptr, ctx->parts, nullptr, M, N, K, GEMM_STORE, S, 256, ctx->st))
         ctx->gemm_failed = true;
     } else if (!launch_gemm_tc_split(A, B, nullptr, ctx->parts, nullptr, M, N, K, GEMM_STORE, S, BN, MS, ctx->st))
