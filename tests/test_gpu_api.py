@@ -183,3 +183,31 @@ def test_dist_serve_with_cuda_engine_world1():
         assert sorted(recs[:, 0].tolist()) == sorted(ref)
     finally:
         dist.destroy_process_group()
+
+
+def test_kv_pool_caller_owned():
+    """SURVEY §8(b) kv_pool: a torch-allocated device buffer as the KV pool (filled with NaN to
+    prove the engine zeroes it) gives exactly the results of the engine-owned pool."""
+    import torch
+    shape = SHAPES["tiny"]
+    reqs = gen_requests(6, shape, 4, 2, 0.5, 2, 32, 8, eos_id=EOS, p_range=(2, 40), length="uniform",
+                        len_range=(1, 32), root_seed=23)
+    weights = gen_weights(shape, "bf16", std=0.08)
+    ref = gpu_engine(shape, "bf16", weights, block_size=16, num_blocks=200, max_rows=64, max_requests=16,
+                     max_prompt=64, T=8, cap=32, eos_id=EOS, sampler_seed=3)
+    for r in reqs:
+        ref.admit(r)
+    ref.step(100)
+    want = ref.collect()
+    ref.close()
+    blk = shape.n_layers * 2 * shape.n_kv_heads * 16 * shape.head_dim * 2      # bf16 bytes per block
+    pool = torch.full((200 * blk // 2,), float("nan"), dtype=torch.bfloat16, device="cuda")
+    g = gpu_engine(shape, "bf16", weights, block_size=16, num_blocks=0, max_rows=64, max_requests=16, max_prompt=64,
+                   T=8, cap=32, eos_id=EOS, sampler_seed=3, kv_pool=(pool.data_ptr(), pool.numel() * 2))
+    for r in reqs:
+        g.admit(r)
+    g.step(100)
+    got = g.collect()
+    g.close()
+    keys = ("request_id", "answer_vote", "branch_len", "branch_state", "branch_score", "tokens")
+    assert [{k: x[k] for k in keys} for x in got] == [{k: x[k] for k in keys} for x in want]
