@@ -5,7 +5,7 @@
 c1: tiny decoder, 1 request, N=4, M=2, cap 64, T=16, alpha 0.5, beta 2 (BJ configs[0])
 c3: 7B shape, 32 requests/GPU (the per-GPU share of 256 on 8 GPUs), N=16, M=4, cap 8192,
     T=400, alpha 0.5, beta 8, scripted rewards (BJ configs[2]); admission is commitment-limited
-c70: the paper's 70B model shape on ONE B200 (TP = 1; row f4's TP path is not built),
+c70: the paper's 70B model shape on ONE B200 (TP = 1; row f4's TP split: tools/run_tp.py),
     16 requests (commitment admits ~66 rows at a time, the rest queue), N=8, M=4, cap 2048, alpha 0.5, beta 4
 c5: 14B shape, 8192-token shared prompt, N=32, M=16, alpha 0.5, beta 16, cap 16384, T=400,
     1 request per GPU (BJ configs[4])
