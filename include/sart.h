@@ -400,6 +400,8 @@ typedef struct {
                               decode step's completion (includes an inline prefill)  */
   double step_ms_max;       /* profile mode: longest single decode step (incl. an interleaved
                               prefill chunk), both over the windows since the last reset */
+  int64_t prefix_tc_windows; /* windows whose decode steps ran the tensor-core prefix pass of the
+                              cascade attention (a request with >= 64 query rows: N x g) */
 } sart_profile;
 int sart_get_profile(sart_ctx* ctx, sart_profile* out);
 /* Turn per-launch attention timing on or off.  While on, decode steps are launched eagerly

@@ -613,12 +613,29 @@ __global__ void __launch_bounds__(1024) k_attn_items(Dims D, Rows rows, Reqs req
   const int nu = *pl.n_units;
   const int bw = (pl.CH + NB - 1) / NB;        // tokens per bucket
   if (tid < NB) cnt[tid] = 0;
+  if (tid == 0 && pl.n_tc) *pl.n_tc = 0;
   __syncthreads();
   for (int pass = 0; pass < 2; ++pass) {
     for (int t = tid; t < nu; t += 1024) {
       const int4 u = pl.units[t];
       int t0 = 0, t1 = 0, nq = 0, tabbase = 0, slot_idx = 0;
       bool ok;
+      if (u.x == 2) {   // tensor-core prefix item: all query rows of the group (k_attn_prefix_tc)
+        if (pass == 0) continue;
+        const int gi = u.y;
+        const int n = pl.grp_n[gi];
+        ok = false;
+        for (int j = 0; j < n; ++j) ok |= rows.status[pl.grp_rows[gi * pl.qr_max + j]] == RUNNING_ST;
+        const int slot = pl.grp_slot[gi];
+        t0 = u.z * pl.CH;
+        t1 = min(t0 + pl.CH, reqs.P[slot] - 1);
+        if (ok && t0 < t1) {
+          const int pos = atomicAdd(pl.n_tc, 1);
+          pl.tc_items[2 * pos] = make_int4(t0, t1, slot * D.MPB, u.z);
+          pl.tc_items[2 * pos + 1] = make_int4(2, gi, 0, n * D.g);
+        }
+        continue;
+      }
       if (u.x == 0) {
         const int r = u.y;
         ok = rows.status[r] == RUNNING_ST;
@@ -673,7 +690,7 @@ __global__ void __launch_bounds__(1024) k_attn_plan(Dims D, Rows rows, Reqs reqs
   // any max_rows works (a fixed shared array would overflow above 1024 rows)
   int* s_rank = pl.row_rank;
   int* s_nrows = pl.row_nreq;
-  const int qr = flat ? 1 : pl.qr_max;
+  const int qr = flat ? 1 : pl.qr_grp;
   for (int r = tid; r < n; r += 1024) {
     const int slot = rows.slot[r];
     int rank = 0, tot = 0;
@@ -690,20 +707,33 @@ __global__ void __launch_bounds__(1024) k_attn_plan(Dims D, Rows rows, Reqs reqs
       if (s_rank[r] != 0) continue;
       const int slot = rows.slot[r];
       const int npc = (reqs.P[slot] - 1 + pl.CH - 1) / pl.CH;
-      const int ngr = (s_nrows[r] + qr - 1) / qr;
+      const int nr = s_nrows[r];
+      // tensor-core prefix pass: the request's rows in ceil(nr g / 128) equal groups of <= 128
+      // query rows, if a group has at least tcq of them
+      int qg = qr;
+      bool tc = false;
+      if (!flat && pl.tcq > 0) {
+        const int ngt = (nr * D.g + 127) / 128;
+        const int qt = (nr + ngt - 1) / ngt;
+        if (qt * D.g >= pl.tcq) { tc = true; qg = qt; }
+      }
+      const int ngr = (nr + qg - 1) / qg;
       for (int k = 0; k < ngr; ++k) {
         const int gi = ng + k;
         pl.grp_slot[gi] = slot;
-        pl.grp_n[gi] = min(qr, s_nrows[r] - k * qr);
+        pl.grp_n[gi] = min(qg, nr - k * qg);
         const int mts = (pl.grp_n[gi] * D.g + 15) / 16;
-        for (int c = 0; c < npc; ++c)
-          for (int mt = 0; mt < mts; ++mt) pl.units[nu++] = make_int4(1, gi, c, mt);
+        for (int c = 0; c < npc; ++c) {
+          if (tc) pl.units[nu++] = make_int4(2, gi, c, 0);
+          else
+            for (int mt = 0; mt < mts; ++mt) pl.units[nu++] = make_int4(1, gi, c, mt);
+        }
       }
       int k = 0;
       for (int r2 = r; r2 < n; ++r2)
         if (rows.slot[r2] == slot) {
-          pl.grp_rows[(ng + k / qr) * pl.qr_max + k % qr] = r2;
-          pl.row_pos[r2] = k % qr;
+          pl.grp_rows[(ng + k / qg) * pl.qr_max + k % qg] = r2;
+          pl.row_pos[r2] = k % qg;
           ++k;
         }
       ng += ngr;

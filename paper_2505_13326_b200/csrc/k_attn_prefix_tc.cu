@@ -1,0 +1,339 @@
+// Tensor-core (tcgen05) prefix pass of the cascade decode attention (SURVEY §8(a) row a4,
+// K1 "prefix pass"; PAPER P:306 shares the prompt's KV across a request's branches).
+//
+// For one item = (prefix group of one request, prefix chunk [t0, t1) of <= CH tokens, kv head
+// h) it computes, for EVERY query row of the group at once (n_r branch rows x g q heads <= 128,
+// one TMEM lane each), the chunk's normalised partial output and log-sum-exp
+//
+//   o_i = sum_{t in chunk} softmax_t(q_i . k_t / sqrt(hd)) v_t,   lse_i = log2 sum_t exp2(...)
+//
+// and writes them into the same partial slots (slot = chunk index) the mma.sync prefix tasks
+// of k_attn_cascade would have written; k_attn_merge combines them with the suffix partials
+// unchanged.  Each prefix KV byte is read from HBM once per (request, kv head) and multiplied
+// by all 128 query rows on the tensor cores -- the mma.sync path re-reads it (from L2) once
+// per 16-row m-tile and is bound by per-warp instruction latency (C5).
+//
+// Structure (one CTA per SM, persistent; items assigned round-robin, so which CTA computes an
+// item never changes its result):
+//   warp 0      TMA producer: 64-token K / V tiles of the paged pool through a 4-stage ring.
+//               The pool's per-row XOR pre-swizzle (common.cuh kv_swz: 16-byte chunk c of
+//               token row t at c ^ (t & 7)) IS the 128-byte-swizzle layout UMMA expects once
+//               each 256-byte row is split into two 128-byte halves, so a 3-D tensor map
+//               {64 elements, half, token row} with SWIZZLE_NONE lands every tile in
+//               shared memory ready for the MMA (no re-layout pass).
+//   warp 1      TMEM owner + MMA issuer (one lane):  S_j = Q K_j^T  (M 128, N 64, K hd; K-major
+//               Q and K) into one of two S buffers, then O += P_{j-1} V_{j-1} (M 128, N hd, K 64;
+//               K-major P, MN-major V straight from the tile).
+//   warps 2..5  softmax, one query row per thread: tcgen05.ld of its S row, online softmax with
+//               a lazy rescale (O in TMEM is rescaled only when the running max grows by more
+//               than 2^8 -- exact, the stale max cancels in o / l), P (bf16) to shared memory,
+//               and at the item's end O / l and the lse to the partial slot.
+#include "kernels.h"
+#include "umma.cuh"
+
+namespace {
+constexpr int PT_KT = 64;    // key tokens per KV tile (one S buffer = 64 TMEM columns)
+constexpr int PT_NS = 4;     // KV tile stages
+constexpr int PT_M = 128;    // query rows per item (TMEM lanes)
+constexpr float PT_LAZY = 8.f;   // rescale O only when the max grows by more than 2^8 (log2 units)
+
+template <int HD>
+struct PtSmem {
+  static constexpr int NH = HD / 64;                   // 128-byte column halves of a row
+  alignas(1024) bf16 q[NH][PT_M * 64];                 // Q, K-major SW128: [half][row][64]
+  alignas(1024) bf16 k[PT_NS][NH][PT_KT * 64];         // K tile: [half][token][64] (K-major B of S)
+  alignas(1024) bf16 v[PT_NS][NH][PT_KT * 64];         // V tile: same bytes, MN-major B of O
+  alignas(1024) bf16 p[PT_M * PT_KT];                  // P, K-major SW128: [row][64 tokens]
+  uint64_t kv_full[PT_NS], kv_empty[PT_NS], s_full[2], s_free[2];
+  uint64_t p_full, o_done, q_full;
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t pack_bf16_pt(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+struct PtItem {
+  int t0, t1, tab, slot_idx, grp, nq, h;
+};
+__device__ __forceinline__ PtItem pt_item(const AttnPlan& pl, const Dims& D, int i) {
+  PtItem it;
+  const int task = i / D.kvh;
+  it.h = i % D.kvh;
+  const int4 a = __ldcg(pl.tc_items + 2 * task);
+  const int4 b = __ldcg(pl.tc_items + 2 * task + 1);
+  it.t0 = a.x;
+  it.t1 = a.y;
+  it.tab = a.z;
+  it.slot_idx = a.w;
+  it.grp = b.y;
+  it.nq = b.w;
+  return it;
+}
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    k_attn_prefix_tc(const __grid_constant__ CUtensorMap kvmap, const bf16* __restrict__ q, float* __restrict__ part_o,
+                     float* __restrict__ part_lse, Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl) {
+  constexpr int NH = HD / 64;
+  constexpr uint32_t TMEM_COLS = 256;                  // S0 | S1 | O (HD <= 128 columns)
+  constexpr uint32_t O_COL = 128;
+  extern __shared__ __align__(16) uint8_t pt_raw[];
+  PtSmem<HD>& sm = *reinterpret_cast<PtSmem<HD>*>((reinterpret_cast<uintptr_t>(pt_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < PT_NS; ++i) {
+      mbar_init(&sm.kv_full[i], 1);
+      mbar_init(&sm.kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.s_full[i], 1);
+      mbar_init(&sm.s_free[i], 4);
+    }
+    mbar_init(&sm.p_full, 4);
+    mbar_init(&sm.o_done, 1);
+    mbar_init(&sm.q_full, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // stale V rows of a partial last tile are multiplied by P = 0: keep them finite
+  for (int e = threadIdx.x; e < PT_NS * NH * PT_KT * 64 / 8; e += blockDim.x) {
+    reinterpret_cast<uint4*>(&sm.k[0][0][0])[e] = make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(&sm.v[0][0][0])[e] = make_uint4(0, 0, 0, 0);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = sm.tmem_base;
+  pdl_wait();        // q of this step (QKV GEMM) and the step's item list are visible
+  pdl_trigger();
+  const int n_items = *pl.n_tc * D.kvh;
+  const float sl2 = 1.4426950408889634f * rsqrtf((float)HD);   // log2(e) / sqrt(hd)
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      const int tpb = D.bs < PT_KT ? D.bs : PT_KT;     // tokens per box (whole page pieces)
+      uint32_t tile = 0;
+      for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+        const PtItem it = pt_item(pl, D, i);
+        const int* tab = reqs.prefix + it.tab;
+        for (int s0 = it.t0; s0 < it.t1; s0 += PT_KT, ++tile) {
+          const int st = tile % PT_NS;
+          mbar_wait(&sm.kv_empty[st], ((tile / PT_NS) & 1) ^ 1);
+          const int ntok = min(PT_KT, it.t1 - s0);
+          const int pieces = (ntok + tpb - 1) / tpb;
+          mbar_expect_tx(&sm.kv_full[st], (uint32_t)(pieces * tpb * 2 * HD * 2));
+          for (int pc = 0; pc < pieces; ++pc) {
+            const int tok = s0 + pc * tpb;
+            const long long blk = tab[tok / D.bs];
+            const long long base = ((((long long)layer * D.NB + blk) * 2) * D.kvh + it.h) * D.bs + tok % D.bs;
+            const int rk = (int)base, rv = (int)(base + (long long)D.kvh * D.bs);
+#pragma unroll
+            for (int hh = 0; hh < NH; ++hh) {
+              tma_load_3d(&sm.k[st][hh][pc * tpb * 64], &kvmap, &sm.kv_full[st], 0, hh, rk);
+              tma_load_3d(&sm.v[st][hh][pc * tpb * 64], &kvmap, &sm.kv_full[st], 0, hh, rv);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    // S = Q K^T: M 128, N 64, both K-major.  O += P V: M 128, N HD, P K-major, V MN-major.
+    const uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(PT_KT >> 3) << 17) | ((uint32_t)(PT_M >> 4) << 24);
+    const uint32_t idesc_o =
+        (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(PT_M >> 4) << 24);
+    const uint32_t qa = smem_u32(&sm.q[0][0]), pa = smem_u32(&sm.p[0]);
+    auto issue_pv = [&](uint32_t g, bool first) {
+      const int st = g % PT_NS;
+      mbar_wait(&sm.p_full, g & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (lane == 0) {
+        const uint32_t va = smem_u32(&sm.v[st][0][0]);
+#pragma unroll
+        for (int kk = 0; kk < PT_KT / 16; ++kk)
+          umma_bf16(tmem + O_COL, umma_desc_k(pa + kk * 32), umma_desc_mn(va + kk * 16 * 128, PT_KT * 128), idesc_o,
+                    (first && kk == 0) ? 0u : 1u);
+        umma_commit(&sm.kv_empty[st]);
+        umma_commit(&sm.o_done);
+      }
+      __syncwarp();
+    };
+    uint32_t tile = 0, icnt = 0;
+    for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++icnt) {
+      const PtItem it = pt_item(pl, D, i);
+      const int nt = (it.t1 - it.t0 + PT_KT - 1) / PT_KT;
+      mbar_wait(&sm.q_full, icnt & 1);
+      for (int kt = 0; kt < nt; ++kt) {
+        const uint32_t g = tile + kt;
+        const int st = g % PT_NS, b = g & 1;
+        mbar_wait(&sm.kv_full[st], (g / PT_NS) & 1);
+        mbar_wait(&sm.s_free[b], ((g >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (lane == 0) {
+          const uint32_t ka = smem_u32(&sm.k[st][0][0]);
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t off = (kk / 4) * (PT_M * 128) + (kk % 4) * 32;
+            const uint32_t koff = (kk / 4) * (PT_KT * 128) + (kk % 4) * 32;
+            umma_bf16(tmem + b * PT_KT, umma_desc_k(qa + off), umma_desc_k(ka + koff), idesc_s, kk ? 1u : 0u);
+          }
+          umma_commit(&sm.s_full[b]);
+        }
+        __syncwarp();
+        if (kt > 0) issue_pv(g - 1, kt == 1);
+      }
+      issue_pv(tile + nt - 1, nt == 1);
+      tile += nt;
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax (one row / thread)
+    const int quarter = warp & 3;
+    const int j = quarter * 32 + lane;                 // query row of the item = TMEM lane
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    uint32_t tile = 0, icnt = 0;
+    for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++icnt) {
+      const PtItem it = pt_item(pl, D, i);
+      const int nt = (it.t1 - it.t0 + PT_KT - 1) / PT_KT;
+      int row = -1, head = 0;
+      if (j < it.nq) {
+        row = pl.grp_rows[it.grp * pl.qr_max + j / D.g];
+        head = it.h * D.g + j % D.g;
+      }
+      // Q row j -> shared memory, K-major SW128 (chunk c of row j at c ^ (j & 7)); the previous
+      // item's MMAs that read Q are complete (its last o_done was waited on below)
+      {
+        const uint4* src = row >= 0 ? reinterpret_cast<const uint4*>(q + ((long long)row * D.qh + head) * HD) : nullptr;
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v = src ? __ldg(src + hh * 8 + c) : make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(&sm.q[hh][0]) + j * 128 + ((c ^ (j & 7)) << 4)) = v;
+          }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.q_full);
+
+      float m = -INFINITY, l = 0.f;
+      for (int kt = 0; kt < nt; ++kt) {
+        const uint32_t g = tile + kt;
+        const int b = g & 1;
+        mbar_wait(&sm.s_full[b], (g >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        uint32_t sr[PT_KT];
+        tmem_ld32_nw(tmem + lane_off + b * PT_KT, sr);
+        tmem_ld32_nw(tmem + lane_off + b * PT_KT + 32, sr + 32);
+        tmem_wait_ld();
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.s_free[b]);
+        const int nvalid = it.t1 - (it.t0 + kt * PT_KT);   // >= 1
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < PT_KT; ++c)
+          if (c < nvalid) mx = fmaxf(mx, __uint_as_float(sr[c]));
+        const float mn = fmaxf(m, mx);
+        const bool grow = kt == 0 || (mn - m) * sl2 > PT_LAZY;
+        // P's buffer and O are free once the previous tile's PV has completed
+        if (g > 0) mbar_wait(&sm.o_done, (g - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (kt > 0 && __any_sync(0xffffffffu, grow)) {
+          const float c = grow ? exp2f((m - mn) * sl2) : 1.f;
+#pragma unroll 1
+          for (int cb = 0; cb < HD; cb += 32) {
+            uint32_t o[32];
+            tmem_ld32_nw(tmem + lane_off + O_COL + cb, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * c);
+            tmem_st32(tmem + lane_off + O_COL + cb, o);
+          }
+          tmem_wait_st();
+          if (grow) l *= c;
+        }
+        if (grow) m = mn;
+        const float mo = m * sl2;
+        uint8_t* prow = reinterpret_cast<uint8_t*>(&sm.p[0]) + j * 128;
+#pragma unroll
+        for (int c8 = 0; c8 < PT_KT / 8; ++c8) {
+          float p[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int c = c8 * 8 + e;
+            p[e] = c < nvalid ? exp2f(fmaf(__uint_as_float(sr[c]), sl2, -mo)) : 0.f;
+            l += p[e];
+          }
+          uint4 w;
+          w.x = pack_bf16_pt(p[0], p[1]);
+          w.y = pack_bf16_pt(p[2], p[3]);
+          w.z = pack_bf16_pt(p[4], p[5]);
+          w.w = pack_bf16_pt(p[6], p[7]);
+          *reinterpret_cast<uint4*>(prow + ((c8 ^ (j & 7)) << 4)) = w;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.p_full);
+      }
+      // item done: O / l and the lse into the partial slot of (row, head)
+      const uint32_t glast = tile + nt - 1;
+      mbar_wait(&sm.o_done, glast & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const float inv = 1.f / l;
+      float* dst = row >= 0 ? part_o + (((long long)row * D.qh + head) * pl.nslot + it.slot_idx) * HD : nullptr;
+#pragma unroll 1
+      for (int cb = 0; cb < HD; cb += 32) {
+        uint32_t o[32];
+        tmem_ld32_nw(tmem + lane_off + O_COL + cb, o);
+        tmem_wait_ld();
+        if (dst)
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(dst + cb + e) =
+                make_float4(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv,
+                            __uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+      }
+      if (dst) part_lse[((long long)row * D.qh + head) * pl.nslot + it.slot_idx] = m * sl2 + log2f(l);
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      tile += nt;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+}  // namespace
+
+bool make_kv_map(void* map_out, const bf16* pool, long long token_rows, int hd, int bs) {
+  EncodeTiled enc = get_encode();
+  if (!enc || hd % 64 != 0) return false;
+  // {64 elements (128 B), hd / 64 halves of a token row, token rows}; SWIZZLE_NONE: the pool's
+  // own XOR pre-swizzle already is the 128-byte-swizzle layout within each half
+  cuuint64_t dims[3] = {64, (cuuint64_t)(hd / 64), (cuuint64_t)token_rows};
+  cuuint64_t strides[2] = {128, (cuuint64_t)hd * 2};
+  cuuint32_t box[3] = {64, 1, (cuuint32_t)(bs < PT_KT ? bs : PT_KT)};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<bf16*>(pool), dims,
+             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void launch_attn_prefix_tc(const bf16* q, const void* kv_map, float* part_o, float* part_lse, Dims D, int layer,
+                           Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s) {
+  const size_t smem = sizeof(PtSmem<128>) + 1024;
+  ensure_dyn_smem(k_attn_prefix_tc<128>, (int)smem);
+  launch_pdl(k_attn_prefix_tc<128>, dim3(device_sms()), dim3(192), smem, s,
+             *reinterpret_cast<const CUtensorMap*>(kv_map), q, part_o, part_lse, D, layer, rows, reqs, pl);
+}

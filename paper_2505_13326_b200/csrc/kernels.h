@@ -133,9 +133,22 @@ struct AttnPlan {
   int* done;        // [L] finished CTAs per layer launch
   int4* items;      // [2 * max tasks] per-step packed items {t0, t1, table base, slot} {type, row|group, mtile, nq}
   int* n_items;     // valid items this step
-  int qr_max, CH, npc_max, nslot;
+  // tensor-core prefix pass (k_attn_prefix_tc.cu): groups with >= tcq query rows (<= 128)
+  // get type-2 units {2, group, chunk, 0}: one item covers all the group's query rows
+  int4* tc_items;   // [2 * max tasks] per-step items of the tensor-core prefix pass (same packing)
+  int* n_tc;        // valid tensor-core items this step
+  int tcq;          // 0: off
+  int qr_grp;       // branch rows per group of the mma.sync prefix tasks (16-row m-tiles)
+  int qr_max, CH, npc_max, nslot;   // qr_max: row stride of grp_rows (>= every group size)
 };
 void launch_attn_plan(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, int flat, cudaStream_t s);
+// tensor-core prefix pass of the cascade attention (k_attn_prefix_tc.cu): writes the prefix
+// partials of the plan's type-2 items; kv_map from make_kv_map (bf16 pool, hd = 128)
+void launch_attn_prefix_tc(const bf16* q, const void* kv_map, float* part_o, float* part_lse, Dims D, int layer,
+                           Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s);
+// 3-D tensor map over the paged pool for the prefix pass: {64 elements, HD/64 halves, token
+// rows}; map_out must hold 128 bytes.  False if the driver cannot encode it.
+bool make_kv_map(void* map_out, const bf16* pool, long long token_rows, int hd, int bs);
 void launch_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s);
 // tensor-core causal prefill: blocks[i] = {first batch row, rows (<= prefill_query_block(D)),
 // slot, first position}

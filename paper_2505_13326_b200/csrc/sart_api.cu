@@ -73,6 +73,9 @@ struct sart_ctx {
   cudaStream_t st = nullptr;
   bool own_stream = false;
   bool poisoned = false;
+  alignas(64) unsigned char kv_map[128] = {};   // CUtensorMap of the pool (tensor-core prefix pass)
+  bool tc_prefix_window = false;
+  long long prefix_tc_windows = 0;
   bool gemm_failed = false;
   int W = 0;   // workspace rows
   int ablate = 0;   // SART_ABLATE bit mask (measurement only: skip decode-step kernels, results invalid)
@@ -316,9 +319,10 @@ int proj(sart_ctx* ctx, const T* A, const T* B, int M, int N, int K) {
   if constexpr (std::is_same<T, bf16>::value) {
     int BN = 256, MS = 1;
     choose_split(M, N, K, S, BN, MS);
-    if ((gemm_2sm_mask() & 2) && K >= 4096 && M > 128 && N % 256 == 0 && BN == 256) {
+    if ((gemm_2sm_mask() & 2) && K >= 4096 && M > 256 && N % 256 == 0 && BN == 256) {
       // CTA pairs (256 x 256 pair tiles) with the SAME split count, so every split covers the same
-      // K-blocks and the partials are bit-identical to the one-SM kernel's
+      // K-blocks and the partials are bit-identical to the one-SM kernel's.  Only above 256 rows:
+      // C2 (M ~ 470) gains 0.2-0.8%, C3 (M ~ 200, one pair-row) loses 1.6% (profiles/r2_gemm_2sm_ab.txt)
       if (!launch_gemm_2sm(A, B, nullptr, ctx->parts, nullptr, M, N, K, GEMM_STORE, S, 256, ctx->st))
         ctx->gemm_failed = true;
     } else if (!launch_gemm_tc_split(A, B, nullptr, ctx->parts, nullptr, M, N, K, GEMM_STORE, S, BN, MS, ctx->st))
@@ -435,6 +439,11 @@ void layer_attention(sart_ctx* ctx, int l, int n) {
   }
   float* dbg = ctx->dbg_attn ? ctx->dbg_attn + (size_t)l * D.R * D.qh * D.hd : nullptr;
   if constexpr (std::is_same<T, bf16>::value) {
+    if (ctx->tc_prefix_window) {   // tensor-core prefix pass: partials of the type-2 items
+      launch_attn_prefix_tc((bf16*)ctx->q, ctx->kv_map, ctx->part_o, ctx->part_lse, D, l, ctx->rows, ctx->reqs,
+                            ctx->plan, ctx->st);
+      ctx->launches++;
+    }
     launch_attn_cascade((bf16*)ctx->q, (bf16*)ctx->pool, (bf16*)ctx->o, dbg, ctx->part_o, ctx->part_lse, D, l,
                         ctx->rows, ctx->reqs, ctx->plan, n, ctx->st);
     ctx->launches += 2;
@@ -1042,6 +1051,13 @@ int run_window(sart_ctx* ctx) {
   if (ctx->prm)   // entries decoded this window = ell(boundary) - ell(now), per row (f2 pass)
     CK(xfer(ctx, ctx->prm->h_ell_ws, ctx->rows.ell, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->st));
   if (ctx->bf16) {   // work units of the cascade attention for this window's batch
+    // the tensor-core prefix pass runs this window if a live request can form a group of
+    // >= tcq query rows (its launch finds no items otherwise)
+    ctx->tc_prefix_window = false;
+    if (ctx->plan.tcq > 0 && ctx->cfg.attn_mode != SART_ATTN_FLAT)
+      for (const SlotInfo& si : ctx->slots)
+        if (si.live && si.N * D.g >= ctx->plan.tcq) ctx->tc_prefix_window = true;
+    ctx->prefix_tc_windows += ctx->tc_prefix_window;
     launch_attn_plan(D, ctx->rows, ctx->reqs, ctx->plan, n, ctx->cfg.attn_mode == SART_ATTN_FLAT, ctx->st);
     ctx->launches++;
   }
@@ -1541,8 +1557,13 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     AttnPlan& pl = ctx->plan;
     pl.CH = 512;   // tokens per attention chunk (SART_ATTN_CH overrides; multiple of 64)
     if (const char* e = getenv("SART_ATTN_CH")) pl.CH = std::max(64, atoi(e) / 64 * 64);
-    pl.qr_max = std::max(1, std::min(SART_MAXN, 64 / D.g));
-    if (const char* e = getenv("SART_ATTN_QR")) pl.qr_max = std::max(1, std::min(SART_MAXN, atoi(e)));   // A/B
+    pl.qr_grp = std::max(1, std::min(SART_MAXN, 64 / D.g));
+    if (const char* e = getenv("SART_ATTN_QR")) pl.qr_grp = std::max(1, std::min(SART_MAXN, atoi(e)));   // A/B
+    // tensor-core prefix pass (hd 128, bf16 pool): groups of >= tcq query rows; SART_ATTN_TCQ
+    // sets the threshold (0 = off).  Enabled after the pool's tensor map is encoded.
+    pl.tcq = 0;   // default off: measured -1.1% on C5 and -2.2% on C3 (profiles/r2_prefix_tc_ab.txt)
+    if (const char* e = getenv("SART_ATTN_TCQ")) pl.tcq = D.hd == 128 ? std::max(0, atoi(e)) : 0;
+    pl.qr_max = std::max(pl.qr_grp, pl.tcq ? std::min(SART_MAXN, 128 / D.g) : 1);
     pl.npc_max = std::max(1, cdiv(cfg.max_prompt - 1, pl.CH));
     const int nsc_max = cdiv(D.cap, pl.CH);
     pl.nslot = pl.npc_max + nsc_max;
@@ -1553,6 +1574,8 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     IC(dalloc(ctx, &pl.done, sizeof(int) * D.L));
     IC(dalloc(ctx, &pl.items, sizeof(int4) * 2 * max_units));
     IC(dalloc(ctx, &pl.n_items, sizeof(int)));
+    IC(dalloc(ctx, &pl.tc_items, sizeof(int4) * 2 * max_units));
+    IC(dalloc(ctx, &pl.n_tc, sizeof(int)));
     IC(dalloc(ctx, &pl.row_pos, sizeof(int) * D.R));
     IC(dalloc(ctx, &pl.row_rank, sizeof(int) * D.R));
     IC(dalloc(ctx, &pl.row_nreq, sizeof(int) * D.R));
@@ -1606,6 +1629,9 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   } else {
     IC(dalloc(ctx, &ctx->pool, (size_t)NB * blk_bytes));
   }
+  if (ctx->bf16 && ctx->plan.tcq > 0 &&
+      !make_kv_map(ctx->kv_map, (const bf16*)ctx->pool, (long long)D.L * NB * 2 * D.kvh * D.bs, D.hd, D.bs))
+    ctx->plan.tcq = 0;   // no tensor map: the mma.sync prefix tasks cover every group
   if (ctx->prm) {
     ctx->prm->D.NB = NB;
     IC(dalloc(ctx->prm, &ctx->prm->pool, (size_t)NB * prm_blk_bytes));
@@ -2087,6 +2113,7 @@ int sart_get_profile(sart_ctx* ctx, sart_profile* o) {
   o->d2h_bytes = ctx->d2h_bytes;
   o->first_step_ms_max = ctx->first_step_ms_max;
   o->step_ms_max = ctx->step_ms_max;
+  o->prefix_tc_windows = ctx->prefix_tc_windows;
   return SART_OK;
 }
 int sart_set_profile(sart_ctx* ctx, int32_t enable) {
@@ -2108,6 +2135,7 @@ int sart_reset_profile(sart_ctx* ctx) {
   ctx->attn_launches = ctx->launches = 0;
   ctx->h2d_bytes = ctx->d2h_bytes = 0;
   ctx->first_step_ms_max = ctx->step_ms_max = 0;
+  ctx->prefix_tc_windows = 0;
   return SART_OK;
 }
 

@@ -105,7 +105,8 @@ class SartProfile(C.Structure):
     _fields_ = [("attn_ms", C.c_double), ("attn_launches", C.c_int64), ("attn_bytes", C.c_double),
                 ("kernel_launches", C.c_int64), ("prefill_ms", C.c_double), ("prm_ms", C.c_double),
                 ("prm_tokens", C.c_int64), ("prm_passes", C.c_int64), ("h2d_bytes", C.c_int64),
-                ("d2h_bytes", C.c_int64), ("first_step_ms_max", C.c_double), ("step_ms_max", C.c_double)]
+                ("d2h_bytes", C.c_int64), ("first_step_ms_max", C.c_double), ("step_ms_max", C.c_double),
+                ("prefix_tc_windows", C.c_int64)]
 
 
 _lib = None

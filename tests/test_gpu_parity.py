@@ -44,30 +44,33 @@ def oracle_teacher_forced(model, prompt, forced, steps, layers, prefix=None):
 
 
 def run_teacher_forced(shape, dtype, prompts, N, steps, bs, tol, std=0.08, seed=0, layers=None, attn_mode=0, T=1,
-                       attn_ch=None, num_blocks=4096):
+                       attn_ch=None, num_blocks=4096, tcq=None, want_tc=None, max_rows=64):
     """Teacher-forced PP1 run.  T > 1: windows of T steps, compared at each window's last step
     (every row advances exactly T steps per window: forced tokens exclude EOS).  attn_ch: the
     cascade attention's chunk length (SART_ATTN_CH, read at sart_init), to put many suffix
-    chunks (slots npc_max + c) on the path."""
+    chunks (slots npc_max + c) on the path.  tcq: threshold of the tensor-core prefix pass
+    (SART_ATTN_TCQ; 0 = mma.sync prefix tasks only); want_tc: assert whether that pass ran."""
     import os
     layers = layers if layers is not None else sorted({0, shape.n_layers // 2, shape.n_layers - 1})
     weights = gen_weights(shape, dtype, std=std, root_seed=seed)
     model = Model(shape, weights)
     rng = np.random.default_rng(seed)
     assert steps % T == 0
-    old_ch = os.environ.get("SART_ATTN_CH")
-    if attn_ch is not None:
-        os.environ["SART_ATTN_CH"] = str(attn_ch)
+    env = {"SART_ATTN_CH": attn_ch, "SART_ATTN_TCQ": tcq}
+    old = {k: os.environ.get(k) for k in env}
+    for k, v in env.items():
+        if v is not None:
+            os.environ[k] = str(v)
     try:
-        g = gpu_engine(shape, dtype, weights, block_size=bs, num_blocks=num_blocks, max_rows=64, max_requests=16,
+        g = gpu_engine(shape, dtype, weights, block_size=bs, num_blocks=num_blocks, max_rows=max_rows, max_requests=16,
                        max_prompt=max(len(p) for p in prompts) + 1, T=T, cap=steps, eos_id=EOS, temperature=1.0,
                        enable_forced_tokens=True, debug_capture=True, attn_mode=attn_mode)
     finally:
-        if attn_ch is not None:
-            if old_ch is None:
-                os.environ.pop("SART_ATTN_CH", None)
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
             else:
-                os.environ["SART_ATTN_CH"] = old_ch
+                os.environ[k] = v
     forced = {}
     for rid, prompt in enumerate(prompts):
         ft = forced_tokens(rng, N, steps, shape.vocab)
@@ -100,8 +103,11 @@ def run_teacher_forced(shape, dtype, prompts, N, steps, bs, tol, std=0.08, seed=
     assert len(res) == len(prompts)
     for r in res:
         assert r["tokens"] == forced[r["request_id"]][r["selected_branch"]].tolist()
+    tc_windows = g.profile()["prefix_tc_windows"]
     g.close()
     assert worst["prm"] <= tol and worst["attn"] <= tol, worst
+    if want_tc is not None:
+        assert (tc_windows > 0) == want_tc, tc_windows
     return worst
 
 
@@ -222,14 +228,35 @@ def test_7b_14b_geometry_bf16_teacher_forced(name):
     print(name, "worst", w)
 
 
-@pytest.mark.parametrize("attn_mode", [0, 1])
-def test_long_prefix_many_branches(attn_mode):
-    """C5-like: one long shared prompt, 16 branches (two prefix groups of <= 12 rows at g=5,
-    several m-tiles per group, prefix chunks of 512) -- cascade and flat paths."""
+@pytest.mark.parametrize("attn_mode,tcq", [(0, 0), (1, None), (0, 64)])
+def test_long_prefix_many_branches(attn_mode, tcq):
+    """C5-like: one long shared prompt, 16 branches (80 query rows at g=5), prefix chunks of
+    512 (the last one ragged) -- mma.sync prefix tasks (tcq 0: two groups of <= 12 rows,
+    several m-tiles each), the flat path, and the tensor-core prefix pass (one 80-row item per
+    chunk and kv head)."""
     shape = _slice("14B")
     prompts = [gen_prompt(13, shape.vocab, EOS, 1300, 1300)]
-    w = run_teacher_forced(shape, "bf16", prompts, N=16, steps=4, bs=64, tol=2e-2, std=0.02, attn_mode=attn_mode)
-    print("long prefix worst", attn_mode, w)
+    w = run_teacher_forced(shape, "bf16", prompts, N=16, steps=4, bs=64, tol=2e-2, std=0.02, attn_mode=attn_mode,
+                           tcq=tcq, want_tc=(attn_mode == 0 and tcq == 64))
+    print("long prefix worst", attn_mode, tcq, w)
+
+
+@pytest.mark.parametrize("name,N,P,bs,ch,std", [
+    ("14B", 32, 1300, 64, None, 0.02),   # two groups of 16 rows (80 query rows each), 3 chunks, ragged last tile
+    ("14B", 13, 700, 16, None, 0.02),    # 65 query rows, 16-token pages (4 TMA boxes per 64-token tile)
+    ("small", 32, 600, 32, 128, 0.02),   # g = 4: a full 128-row item; CH 128 -> 5 chunks per request
+    ("7B", 10, 66, 64, None, 0.02),      # g = 7, 70 rows; P - 1 = 65: one full tile + a 1-token tile
+    ("70B", 8, 300, 64, 64, 0.01),       # g = 8, 64 rows (the threshold); 5 single-tile chunks (std: R39)
+])
+def test_prefix_tc_pass(name, N, P, bs, ch, std):
+    """The tensor-core prefix pass (k_attn_prefix_tc: tcgen05 S = Q K^T and O += P V over every
+    query row of a request, lazy rescale) against the fp64 oracle: logits, PRM score and the
+    attention output of the layer; a second request with a short prompt runs beside it."""
+    shape = _slice(name) if name != "small" else SHAPES["small"]
+    prompts = [gen_prompt(20 + N, shape.vocab, EOS, P, P), gen_prompt(21, shape.vocab, EOS, 90, 90)]
+    w = run_teacher_forced(shape, "bf16", prompts, N=N, steps=6, bs=bs, tol=2e-2, std=std, attn_ch=ch,
+                           tcq=64, want_tc=True, max_rows=2 * N + 8, num_blocks=2048)
+    print("prefix tc", name, N, P, bs, ch, w)
 
 
 def test_multi_chunk_suffix_small_ch64():
