@@ -402,6 +402,8 @@ typedef struct {
                               prefill chunk), both over the windows since the last reset */
   int64_t prefix_tc_windows; /* windows whose decode steps ran the tensor-core prefix pass of the
                               cascade attention (a request with >= 64 query rows: N x g) */
+  double attn_stream_ms;    /* profile mode: the part of attn_ms spent in the streaming kernel(s)
+                              (k_attn_cascade, + k_attn_prefix_tc when on), merge excluded */
 } sart_profile;
 int sart_get_profile(sart_ctx* ctx, sart_profile* out);
 /* Turn per-launch attention timing on or off.  While on, decode steps are launched eagerly

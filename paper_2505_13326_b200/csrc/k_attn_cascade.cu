@@ -160,7 +160,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncwarp();
-  pdl_wait();                      // predecessor's q / KV writes are visible from here on
+  // predecessor's q / KV writes are visible from here on.  With a concurrent prefix pass
+  // (pl.tc_grid > 0) the predecessor is that pass, whose CTAs release this grid only after
+  // their own PDL wait on the QKV GEMM: q and the appended KV are complete before any CTA of
+  // this grid starts, so it does not wait (q is read through L2, __ldcg)
+  if (pl.tc_grid == 0) pdl_wait();
   pdl_trigger();
   const int n_items = *pl.n_items * D.kvh;
 
@@ -228,10 +232,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
       const bf16* q1 = q_of(pl, D, it, r1, row, head) ? q + ((long long)row * D.qh + head) * HD : nullptr;
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
-        qa[kk][0] = q0 ? *reinterpret_cast<const uint32_t*>(q0 + 16 * kk + cc) : 0u;
-        qa[kk][1] = q1 ? *reinterpret_cast<const uint32_t*>(q1 + 16 * kk + cc) : 0u;
-        qa[kk][2] = q0 ? *reinterpret_cast<const uint32_t*>(q0 + 16 * kk + 8 + cc) : 0u;
-        qa[kk][3] = q1 ? *reinterpret_cast<const uint32_t*>(q1 + 16 * kk + 8 + cc) : 0u;
+        qa[kk][0] = q0 ? __ldcg(reinterpret_cast<const unsigned int*>(q0 + 16 * kk + cc)) : 0u;
+        qa[kk][1] = q1 ? __ldcg(reinterpret_cast<const unsigned int*>(q1 + 16 * kk + cc)) : 0u;
+        qa[kk][2] = q0 ? __ldcg(reinterpret_cast<const unsigned int*>(q0 + 16 * kk + 8 + cc)) : 0u;
+        qa[kk][3] = q1 ? __ldcg(reinterpret_cast<const unsigned int*>(q1 + 16 * kk + 8 + cc)) : 0u;
       }
     }
     float o[HD / 8][4];
@@ -356,6 +360,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(pl.done + layer, 1) == (int)gridDim.x - 1) {
+      if (pl.tc_grid > 0) {   // this grid completes only after the concurrent prefix pass
+        volatile int* td = pl.tc_done + layer;
+        while (*td < pl.tc_grid) __nanosleep(256);
+        __threadfence();
+        pl.tc_done[layer] = 0;
+      }
       pl.work[layer] = 0;
       pl.done[layer] = 0;
     }
@@ -856,6 +866,7 @@ static int attn_cfg() {
   return c;
 }
 thread_local bool g_attn_skip_merge = false;   // per host thread (ctx of a TP group each drive one)
+thread_local cudaEvent_t g_attn_mid_event = nullptr;
 template <int HD>
 static void launch_hd(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse, Dims D,
                       int layer, Rows rows, Reqs reqs, AttnPlan pl, int n, cudaStream_t s) {
@@ -865,6 +876,7 @@ static void launch_hd(const bf16* q, const bf16* pool, bf16* out, float* dbg, fl
     case 3: launch_cfg<HD, 7, 3, 16>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
     default: launch_cfg<HD, 8, 3, 16>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
   }
+  if (g_attn_mid_event) cudaEventRecord(g_attn_mid_event, s);
   if (g_attn_skip_merge) return;
   launch_pdl(k_attn_merge<HD>, dim3((n * D.qh * 32 + 255) / 256), dim3(256), 0, s, part_o, part_lse, out, dbg, D,
              rows, reqs, pl, n);

@@ -28,6 +28,13 @@
 //               a lazy rescale (O in TMEM is rescaled only when the running max grows by more
 //               than 2^8 -- exact, the stale max cancels in o / l), P (bf16) to shared memory,
 //               and at the item's end O / l and the lse to the partial slot.
+//
+// CAUSAL = true is the tensor-core causal prefill of row f1 (Alg. 1 L15): an item is
+// (a block of <= 128 prompt positions of one request, one q head); its rows see keys
+// [0, position] of the request's prefix pages (written by this layer's QKV epilogue), and O / l
+// is written in bf16 as the prefill's attention output.
+#include <algorithm>
+
 #include "kernels.h"
 #include "umma.cuh"
 
@@ -56,26 +63,45 @@ __device__ __forceinline__ uint32_t pack_bf16_pt(float lo, float hi) {
 
 struct PtItem {
   int t0, t1, tab, slot_idx, grp, nq, h;
+  int head, r0, nr, p0;   // CAUSAL (prefill): q head, first batch row, rows, first position
 };
-__device__ __forceinline__ PtItem pt_item(const AttnPlan& pl, const Dims& D, int i) {
+// item i: prefix pass = (tc task i / kvh, kv head i % kvh); causal prefill = (query block
+// i / qh of <= 128 positions, q head i % qh), keys [0, p0 + nr) of the request's prefix table
+template <bool CAUSAL>
+__device__ __forceinline__ PtItem pt_item(const AttnPlan& pl, const Dims& D, const int4* __restrict__ blocks, int i) {
   PtItem it;
-  const int task = i / D.kvh;
-  it.h = i % D.kvh;
-  const int4 a = __ldcg(pl.tc_items + 2 * task);
-  const int4 b = __ldcg(pl.tc_items + 2 * task + 1);
-  it.t0 = a.x;
-  it.t1 = a.y;
-  it.tab = a.z;
-  it.slot_idx = a.w;
-  it.grp = b.y;
-  it.nq = b.w;
+  if constexpr (CAUSAL) {
+    const int4 b = __ldg(blocks + i / D.qh);             // {first batch row, rows, slot, first position}
+    it.head = i % D.qh;
+    it.h = it.head / D.g;
+    it.r0 = b.x;
+    it.nr = b.y;
+    it.p0 = b.w;
+    it.t0 = 0;
+    it.t1 = b.w + b.y;
+    it.tab = b.z * D.MPB;
+    it.slot_idx = it.grp = it.nq = 0;
+  } else {
+    const int task = i / D.kvh;
+    it.h = i % D.kvh;
+    const int4 a = __ldcg(pl.tc_items + 2 * task);
+    const int4 b = __ldcg(pl.tc_items + 2 * task + 1);
+    it.t0 = a.x;
+    it.t1 = a.y;
+    it.tab = a.z;
+    it.slot_idx = a.w;
+    it.grp = b.y;
+    it.nq = b.w;
+    it.head = it.r0 = it.nr = it.p0 = 0;
+  }
   return it;
 }
 
-template <int HD>
+template <int HD, bool CAUSAL>
 __global__ void __launch_bounds__(192, 1)
     k_attn_prefix_tc(const __grid_constant__ CUtensorMap kvmap, const bf16* __restrict__ q, float* __restrict__ part_o,
-                     float* __restrict__ part_lse, Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl) {
+                     float* __restrict__ part_lse, bf16* __restrict__ out, const int4* __restrict__ blocks, int nblocks,
+                     Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl) {
   constexpr int NH = HD / 64;
   constexpr uint32_t TMEM_COLS = 256;                  // S0 | S1 | O (HD <= 128 columns)
   constexpr uint32_t O_COL = 128;
@@ -114,7 +140,7 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem = sm.tmem_base;
   pdl_wait();        // q of this step (QKV GEMM) and the step's item list are visible
   pdl_trigger();
-  const int n_items = *pl.n_tc * D.kvh;
+  const int n_items = CAUSAL ? nblocks * D.qh : *pl.n_tc * D.kvh;
   const float sl2 = 1.4426950408889634f * rsqrtf((float)HD);   // log2(e) / sqrt(hd)
 
   if (warp == 0) {
@@ -123,7 +149,7 @@ __global__ void __launch_bounds__(192, 1)
       const int tpb = D.bs < PT_KT ? D.bs : PT_KT;     // tokens per box (whole page pieces)
       uint32_t tile = 0;
       for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
-        const PtItem it = pt_item(pl, D, i);
+        const PtItem it = pt_item<CAUSAL>(pl, D, blocks, i);
         const int* tab = reqs.prefix + it.tab;
         for (int s0 = it.t0; s0 < it.t1; s0 += PT_KT, ++tile) {
           const int st = tile % PT_NS;
@@ -169,7 +195,7 @@ __global__ void __launch_bounds__(192, 1)
     };
     uint32_t tile = 0, icnt = 0;
     for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++icnt) {
-      const PtItem it = pt_item(pl, D, i);
+      const PtItem it = pt_item<CAUSAL>(pl, D, blocks, i);
       const int nt = (it.t1 - it.t0 + PT_KT - 1) / PT_KT;
       mbar_wait(&sm.q_full, icnt & 1);
       for (int kt = 0; kt < nt; ++kt) {
@@ -201,10 +227,12 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t tile = 0, icnt = 0;
     for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++icnt) {
-      const PtItem it = pt_item(pl, D, i);
+      const PtItem it = pt_item<CAUSAL>(pl, D, blocks, i);
       const int nt = (it.t1 - it.t0 + PT_KT - 1) / PT_KT;
       int row = -1, head = 0;
-      if (j < it.nq) {
+      if constexpr (CAUSAL) {
+        if (j < it.nr) { row = it.r0 + j; head = it.head; }
+      } else if (j < it.nq) {
         row = pl.grp_rows[it.grp * pl.qr_max + j / D.g];
         head = it.h * D.g + j % D.g;
       }
@@ -237,7 +265,10 @@ __global__ void __launch_bounds__(192, 1)
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.s_free[b]);
-        const int nvalid = it.t1 - (it.t0 + kt * PT_KT);   // >= 1
+        // keys of this tile the row may see: >= 1 in its first tile (key 0 precedes every
+        // position); causal: key index <= the row's position p0 + j
+        int nvalid = it.t1 - (it.t0 + kt * PT_KT);
+        if constexpr (CAUSAL) nvalid = min(nvalid, it.p0 + j - kt * PT_KT + 1);
         float mx = -INFINITY;
 #pragma unroll
         for (int c = 0; c < PT_KT; ++c)
@@ -290,20 +321,40 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&sm.o_done, glast & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const float inv = 1.f / l;
-      float* dst = row >= 0 ? part_o + (((long long)row * D.qh + head) * pl.nslot + it.slot_idx) * HD : nullptr;
+      if constexpr (CAUSAL) {   // the prefill's attention output, bf16 [row][qh][hd]
+        bf16* dst = row >= 0 ? out + ((long long)row * D.qh + head) * HD : nullptr;
 #pragma unroll 1
-      for (int cb = 0; cb < HD; cb += 32) {
-        uint32_t o[32];
-        tmem_ld32_nw(tmem + lane_off + O_COL + cb, o);
-        tmem_wait_ld();
-        if (dst)
+        for (int cb = 0; cb < HD; cb += 32) {
+          uint32_t o[32];
+          tmem_ld32_nw(tmem + lane_off + O_COL + cb, o);
+          tmem_wait_ld();
+          if (dst)
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(dst + cb + e) =
-                make_float4(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv,
-                            __uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+            for (int e = 0; e < 32; e += 8) {
+              uint4 w;
+              w.x = pack_bf16_pt(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
+              w.y = pack_bf16_pt(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+              w.z = pack_bf16_pt(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+              w.w = pack_bf16_pt(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+              *reinterpret_cast<uint4*>(dst + cb + e) = w;
+            }
+        }
+      } else {
+        float* dst = row >= 0 ? part_o + (((long long)row * D.qh + head) * pl.nslot + it.slot_idx) * HD : nullptr;
+#pragma unroll 1
+        for (int cb = 0; cb < HD; cb += 32) {
+          uint32_t o[32];
+          tmem_ld32_nw(tmem + lane_off + O_COL + cb, o);
+          tmem_wait_ld();
+          if (dst)
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(dst + cb + e) =
+                  make_float4(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv,
+                              __uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+        }
+        if (dst) part_lse[((long long)row * D.qh + head) * pl.nslot + it.slot_idx] = m * sl2 + log2f(l);
       }
-      if (dst) part_lse[((long long)row * D.qh + head) * pl.nslot + it.slot_idx] = m * sl2 + log2f(l);
       asm volatile("tcgen05.fence::before_thread_sync;");
       tile += nt;
     }
@@ -312,6 +363,12 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+  if constexpr (!CAUSAL) {   // the concurrent k_attn_cascade's last CTA waits for every CTA of the pass
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(pl.tc_done + layer, 1);
+    }
   }
 }
 }  // namespace
@@ -333,7 +390,19 @@ bool make_kv_map(void* map_out, const bf16* pool, long long token_rows, int hd, 
 void launch_attn_prefix_tc(const bf16* q, const void* kv_map, float* part_o, float* part_lse, Dims D, int layer,
                            Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s) {
   const size_t smem = sizeof(PtSmem<128>) + 1024;
-  ensure_dyn_smem(k_attn_prefix_tc<128>, (int)smem);
-  launch_pdl(k_attn_prefix_tc<128>, dim3(device_sms()), dim3(192), smem, s,
-             *reinterpret_cast<const CUtensorMap*>(kv_map), q, part_o, part_lse, D, layer, rows, reqs, pl);
+  ensure_dyn_smem(k_attn_prefix_tc<128, false>, (int)smem);
+  launch_pdl(k_attn_prefix_tc<128, false>, dim3(pl.tc_grid), dim3(192), smem, s,
+             *reinterpret_cast<const CUtensorMap*>(kv_map), q, part_o, part_lse, (bf16*)nullptr, (const int4*)nullptr, 0,
+             D, layer, rows, reqs, pl);
+}
+
+void launch_attn_prefill_umma(const bf16* q, const void* kv_map, bf16* out, Dims D, int layer, Reqs reqs,
+                              const int4* blocks, int nblocks, cudaStream_t s) {
+  if (nblocks <= 0) return;
+  const size_t smem = sizeof(PtSmem<128>) + 1024;
+  ensure_dyn_smem(k_attn_prefix_tc<128, true>, (int)smem);
+  const int items = nblocks * D.qh;
+  launch_pdl(k_attn_prefix_tc<128, true>, dim3(std::min(items, device_sms())), dim3(192), smem, s,
+             *reinterpret_cast<const CUtensorMap*>(kv_map), q, (float*)nullptr, (float*)nullptr, out, blocks, nblocks,
+             D, layer, Rows{}, reqs, AttnPlan{});
 }

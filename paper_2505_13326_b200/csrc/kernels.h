@@ -138,6 +138,10 @@ struct AttnPlan {
   int4* tc_items;   // [2 * max tasks] per-step items of the tensor-core prefix pass (same packing)
   int* n_tc;        // valid tensor-core items this step
   int tcq;          // 0: off
+  int* tc_done;     // [L] finished CTAs of the prefix pass per layer launch
+  int tc_grid;      // CTAs of this window's prefix pass (0: no pass): the pass runs on tc_grid SMs
+                    // CONCURRENTLY with k_attn_cascade (which skips its PDL wait and, in its last
+                    // CTA, waits for tc_done == tc_grid, so the merge sees both kernels' partials)
   int qr_grp;       // branch rows per group of the mma.sync prefix tasks (16-row m-tiles)
   int qr_max, CH, npc_max, nslot;   // qr_max: row stride of grp_rows (>= every group size)
 };
@@ -149,6 +153,10 @@ void launch_attn_prefix_tc(const bf16* q, const void* kv_map, float* part_o, flo
 // 3-D tensor map over the paged pool for the prefix pass: {64 elements, HD/64 halves, token
 // rows}; map_out must hold 128 bytes.  False if the driver cannot encode it.
 bool make_kv_map(void* map_out, const bf16* pool, long long token_rows, int hd, int bs);
+// tensor-core (tcgen05) causal prefill, hd = 128 (k_attn_prefix_tc.cu, CAUSAL): blocks[i] =
+// {first batch row, rows (<= 128), request slot, first position}; out[row][qh][hd] bf16
+void launch_attn_prefill_umma(const bf16* q, const void* kv_map, bf16* out, Dims D, int layer, Reqs reqs,
+                              const int4* blocks, int nblocks, cudaStream_t s);
 void launch_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s);
 // tensor-core causal prefill: blocks[i] = {first batch row, rows (<= prefill_query_block(D)),
 // slot, first position}
@@ -159,6 +167,7 @@ int prefill_query_block(const Dims& D);   // query positions per prefill CTA (16
 // entries over [prefix ; suffix entries 0..entry] (causal)
 void launch_attn_suffix_tc(const bf16* q, const bf16* pool, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
                            const int4* qblocks, int nqb, cudaStream_t s);
+extern thread_local cudaEvent_t g_attn_mid_event;   // profile mode: recorded between the streaming kernel and the merge
 extern thread_local bool g_attn_skip_merge;   // measurement only (SART_ABLATE): launch the cascade kernel without its merge
 void launch_attn_account(Dims D, Rows rows, Reqs reqs, AttnPlan pl, int n, double* acc, cudaStream_t s);
 void launch_attn_cascade(const bf16* q, const bf16* pool, bf16* out, float* dbg, float* part_o, float* part_lse,

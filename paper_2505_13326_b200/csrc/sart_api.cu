@@ -75,6 +75,8 @@ struct sart_ctx {
   bool poisoned = false;
   alignas(64) unsigned char kv_map[128] = {};   // CUtensorMap of the pool (tensor-core prefix pass)
   bool tc_prefix_window = false;
+  bool kv_map_ok = false;   // kv_map describes this ctx's pool (bf16, hd 128)
+  bool pf_umma = false;     // causal prefill on tcgen05 (k_attn_prefix_tc<CAUSAL>); SART_PF_UMMA=0: mma.sync
   long long prefix_tc_windows = 0;
   bool gemm_failed = false;
   int W = 0;   // workspace rows
@@ -145,6 +147,7 @@ struct sart_ctx {
   std::vector<cudaEvent_t> ev_pool;
   int ev_used = 0;
   double attn_ms = 0, attn_bytes = 0, attn_bytes_base = 0, prefill_ms = 0;
+  double attn_stream_ms = 0;   // profile mode: the streaming kernel(s) alone (merge excluded)
   long long attn_launches = 0, launches = 0;
   long long h2d_bytes = 0, d2h_bytes = 0;   // host<->device bytes of the serving path (sart_profile)
   // record_trace (PP2): per-window streams and per-boundary state hashes for oracle replay
@@ -432,8 +435,11 @@ template <typename T>
 void layer_attention(sart_ctx* ctx, int l, int n) {
   const Dims& D = ctx->D;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (ctx->cfg.profile && ctx->ev_used + 2 <= (int)ctx->ev_pool.size()) {
+  // profile mode: events before the attention, between the streaming kernel and the merge
+  // (g_attn_mid_event, recorded by launch_attn_cascade) and after the merge
+  if (ctx->cfg.profile && ctx->ev_used + 3 <= (int)ctx->ev_pool.size()) {
     e0 = ctx->ev_pool[ctx->ev_used++];
+    g_attn_mid_event = ctx->ev_pool[ctx->ev_used++];
     e1 = ctx->ev_pool[ctx->ev_used++];
     cudaEventRecord(e0, ctx->st);
   }
@@ -453,6 +459,7 @@ void layer_attention(sart_ctx* ctx, int l, int n) {
   }
   ctx->attn_launches++;
   if (e1) cudaEventRecord(e1, ctx->st);
+  g_attn_mid_event = nullptr;
 }
 
 // SART_ABLATE bits (measurement only, tools/ablate_c2.py): the in-graph marginal cost of a
@@ -512,11 +519,13 @@ void prefill_batch(sart_ctx* ctx, sart_ctx* src, int t_begin, int t_end) {
   for (int t0 = t_begin; t0 < t_end; t0 += ctx->PC) {
     const int c = std::min(ctx->PC, t_end - t0);
     const RopeArgs ra{src->d_pf_slot + t0, src->d_pf_pos + t0};
-    // 64-position query blocks of each request segment of this chunk (tensor-core prefill)
+    // query blocks of each request segment of this chunk (tensor-core prefill): 128 positions
+    // (tcgen05, one TMEM lane each; largest key range first for the static CTA assignment) or
+    // 16-64 (mma.sync)
     int nqb = 0;
     if constexpr (std::is_same<T, bf16>::value) {
       std::vector<int4> qb;
-      const int QP = prefill_query_block(D);
+      const int QP = ctx->pf_umma ? 128 : prefill_query_block(D);
       for (int i = 0; i < c;) {
         const int slot = src->pf_slot_h[t0 + i];
         int j = i;
@@ -524,6 +533,8 @@ void prefill_batch(sart_ctx* ctx, sart_ctx* src, int t_begin, int t_end) {
         qb.push_back(make_int4(i, j - i, slot, src->pf_pos_h[t0 + i]));
         i = j;
       }
+      if (ctx->pf_umma)
+        std::stable_sort(qb.begin(), qb.end(), [](const int4& a, const int4& b) { return a.w + a.y > b.w + b.y; });
       nqb = (int)qb.size();
       xfer(src, src->d_pf_blocks, qb.data(), sizeof(int4) * qb.size(), cudaMemcpyHostToDevice, s);
     }
@@ -534,9 +545,13 @@ void prefill_batch(sart_ctx* ctx, sart_ctx* src, int t_begin, int t_end) {
       norm<T>(ctx, res, ctx->W_<T>(t_layer(l, 0)), (T*)ctx->a, nullptr, nullptr, c);
       qkv_rope<T>(ctx, l, c, ra);
       if (l == D.L - 1) break;
-      if constexpr (std::is_same<T, bf16>::value)
-        launch_attn_prefill_tc((bf16*)ctx->q, (bf16*)ctx->pool, (bf16*)ctx->o, D, l, ctx->reqs, src->d_pf_blocks, nqb,
-                               s);
+      if constexpr (std::is_same<T, bf16>::value) {
+        if (ctx->pf_umma)
+          launch_attn_prefill_umma((bf16*)ctx->q, ctx->kv_map, (bf16*)ctx->o, D, l, ctx->reqs, src->d_pf_blocks, nqb, s);
+        else
+          launch_attn_prefill_tc((bf16*)ctx->q, (bf16*)ctx->pool, (bf16*)ctx->o, D, l, ctx->reqs, src->d_pf_blocks,
+                                 nqb, s);
+      }
       else
         launch_attn_prefill<T>((T*)ctx->q, (T*)ctx->pool, (T*)ctx->o, D, l, ctx->reqs, ra.pf_slot, ra.pf_pos, c, s);
       const ResParts ro = proj_res<T>(ctx, (T*)ctx->o, ctx->W_<T>(t_layer(l, 3)), c, D.d, D.qh * D.hd, 2 * l);
@@ -1058,6 +1073,9 @@ int run_window(sart_ctx* ctx) {
       for (const SlotInfo& si : ctx->slots)
         if (si.live && si.N * D.g >= ctx->plan.tcq) ctx->tc_prefix_window = true;
     ctx->prefix_tc_windows += ctx->tc_prefix_window;
+    // the pass's SMs (SART_TC_SMS); the cascade kernel streams the suffixes on the others
+    static const int tc_sms = getenv("SART_TC_SMS") ? atoi(getenv("SART_TC_SMS")) : 64;
+    ctx->plan.tc_grid = ctx->tc_prefix_window ? std::max(1, std::min(tc_sms, device_sms())) : 0;
     launch_attn_plan(D, ctx->rows, ctx->reqs, ctx->plan, n, ctx->cfg.attn_mode == SART_ATTN_FLAT, ctx->st);
     ctx->launches++;
   }
@@ -1175,10 +1193,12 @@ int run_window(sart_ctx* ctx) {
     ctx->step_ms_max = std::max(ctx->step_ms_max, (double)mx);
   }
   if (ctx->cfg.profile) {
-    for (int i = 0; i + 1 < ctx->ev_used; i += 2) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ctx->ev_pool[i], ctx->ev_pool[i + 1]);
+    for (int i = 0; i + 2 < ctx->ev_used; i += 3) {
+      float ms = 0.f, ms_s = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev_pool[i], ctx->ev_pool[i + 2]);
+      cudaEventElapsedTime(&ms_s, ctx->ev_pool[i], ctx->ev_pool[i + 1]);
       ctx->attn_ms += ms;
+      ctx->attn_stream_ms += ms_s;
     }
   }
   return SART_OK;
@@ -1572,6 +1592,8 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     IC(dalloc(ctx, &pl.n_units, sizeof(int)));
     IC(dalloc(ctx, &pl.work, sizeof(int) * D.L));
     IC(dalloc(ctx, &pl.done, sizeof(int) * D.L));
+    IC(dalloc(ctx, &pl.tc_done, sizeof(int) * D.L));
+    pl.tc_grid = 0;
     IC(dalloc(ctx, &pl.items, sizeof(int4) * 2 * max_units));
     IC(dalloc(ctx, &pl.n_items, sizeof(int)));
     IC(dalloc(ctx, &pl.tc_items, sizeof(int4) * 2 * max_units));
@@ -1629,12 +1651,20 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   } else {
     IC(dalloc(ctx, &ctx->pool, (size_t)NB * blk_bytes));
   }
-  if (ctx->bf16 && ctx->plan.tcq > 0 &&
-      !make_kv_map(ctx->kv_map, (const bf16*)ctx->pool, (long long)D.L * NB * 2 * D.kvh * D.bs, D.hd, D.bs))
-    ctx->plan.tcq = 0;   // no tensor map: the mma.sync prefix tasks cover every group
+  // TMA map of the pool for the tensor-core attention kernels (prefix pass, causal prefill)
+  static const bool pf_umma_env = !(getenv("SART_PF_UMMA") && atoi(getenv("SART_PF_UMMA")) == 0);
+  ctx->kv_map_ok = ctx->bf16 && D.hd == 128 &&
+                   make_kv_map(ctx->kv_map, (const bf16*)ctx->pool, (long long)D.L * NB * 2 * D.kvh * D.bs, D.hd, D.bs);
+  if (!ctx->kv_map_ok) ctx->plan.tcq = 0;   // no tensor map: the mma.sync prefix tasks cover every group
+  ctx->pf_umma = ctx->kv_map_ok && pf_umma_env;
   if (ctx->prm) {
     ctx->prm->D.NB = NB;
     IC(dalloc(ctx->prm, &ctx->prm->pool, (size_t)NB * prm_blk_bytes));
+    const Dims& PD = ctx->prm->D;
+    ctx->prm->kv_map_ok = ctx->prm->bf16 && PD.hd == 128 &&
+                          make_kv_map(ctx->prm->kv_map, (const bf16*)ctx->prm->pool,
+                                      (long long)PD.L * NB * 2 * PD.kvh * PD.bs, PD.hd, PD.bs);
+    ctx->prm->pf_umma = ctx->prm->kv_map_ok && pf_umma_env;
   }
   IC(dalloc(ctx, &ctx->free_stack, sizeof(int) * (size_t)NB, false));
   {
@@ -1651,7 +1681,7 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   ctx->last_slot_id.assign(D.S, -1);
   for (int s = D.S - 1; s >= 0; --s) ctx->free_slots.push_back(s);
   if (cfg.profile) {
-    ctx->ev_pool.resize(2 * D.L * D.T + 2);
+    ctx->ev_pool.resize(3 * D.L * D.T + 3);
     for (auto& ev : ctx->ev_pool) IC(cudaEventCreate(&ev));
   }
   IC(cudaStreamSynchronize(ctx->st));
@@ -2114,12 +2144,13 @@ int sart_get_profile(sart_ctx* ctx, sart_profile* o) {
   o->first_step_ms_max = ctx->first_step_ms_max;
   o->step_ms_max = ctx->step_ms_max;
   o->prefix_tc_windows = ctx->prefix_tc_windows;
+  o->attn_stream_ms = ctx->attn_stream_ms;
   return SART_OK;
 }
 int sart_set_profile(sart_ctx* ctx, int32_t enable) {
   if (!ctx) return set_err(SART_EINVAL, "null argument");
   if (enable && ctx->ev_pool.empty()) {
-    ctx->ev_pool.resize(2 * ctx->D.L * ctx->D.T + 2);
+    ctx->ev_pool.resize(3 * ctx->D.L * ctx->D.T + 3);
     for (auto& ev : ctx->ev_pool)
       if (cudaEventCreate(&ev) != cudaSuccess) return set_err(SART_ECUDA, "event create");
   }
@@ -2130,7 +2161,7 @@ int sart_set_profile(sart_ctx* ctx, int32_t enable) {
 int sart_reset_profile(sart_ctx* ctx) {
   if (!ctx) return set_err(SART_EINVAL, "null argument");
   ctx->attn_bytes_base += ctx->attn_bytes;
-  ctx->attn_ms = ctx->attn_bytes = ctx->prefill_ms = ctx->prm_ms = 0;
+  ctx->attn_ms = ctx->attn_bytes = ctx->prefill_ms = ctx->prm_ms = ctx->attn_stream_ms = 0;
   ctx->prm_tokens = ctx->prm_passes = 0;
   ctx->attn_launches = ctx->launches = 0;
   ctx->h2d_bytes = ctx->d2h_bytes = 0;

@@ -106,7 +106,7 @@ class SartProfile(C.Structure):
                 ("kernel_launches", C.c_int64), ("prefill_ms", C.c_double), ("prm_ms", C.c_double),
                 ("prm_tokens", C.c_int64), ("prm_passes", C.c_int64), ("h2d_bytes", C.c_int64),
                 ("d2h_bytes", C.c_int64), ("first_step_ms_max", C.c_double), ("step_ms_max", C.c_double),
-                ("prefix_tc_windows", C.c_int64)]
+                ("prefix_tc_windows", C.c_int64), ("attn_stream_ms", C.c_double)]
 
 
 _lib = None

@@ -99,6 +99,8 @@ def main():
            "attn_GBps": att_b / (att_ms / 1e3) / 1e9 if att_ms else None,
            "attn_frac_of_6455": att_b / (att_ms / 1e3) / 1e9 / 6455.3 if att_ms else None,
            "attn_ms_per_launch": att_ms / max(1, q1["attn_launches"] - q0["attn_launches"]),
+           "attn_stream_frac_of_6455": att_b / ((q1["attn_stream_ms"] - q0["attn_stream_ms"]) / 1e3) / 1e9 / 6455.3
+           if q1["attn_stream_ms"] > q0["attn_stream_ms"] else None,
            "init_s": init_s, "warmup_s": warm_s}
     if prm is not None:
         d, F, L = prm.d_model, prm.d_ff, prm.n_layers
