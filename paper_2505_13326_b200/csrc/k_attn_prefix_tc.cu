@@ -29,10 +29,12 @@
 //               than 2^8 -- exact, the stale max cancels in o / l), P (bf16) to shared memory,
 //               and at the item's end O / l and the lse to the partial slot.
 //
-// CAUSAL = true is the tensor-core causal prefill of row f1 (Alg. 1 L15): an item is
+// MODE = PT_PREFILL is the tensor-core causal prefill of row f1 (Alg. 1 L15): an item is
 // (a block of <= 128 prompt positions of one request, one q head); its rows see keys
 // [0, position] of the request's prefix pages (written by this layer's QKV epilogue), and O / l
-// is written in bf16 as the prefill's attention output.
+// is written in bf16 as the prefill's attention output.  MODE = PT_SUF is the same for the f2
+// PRM pass: the rows are one batch row's new suffix entries, the keys its prefix pages
+// (padding slots masked) followed by its suffix entries.
 #include <algorithm>
 
 #include "kernels.h"
@@ -63,24 +65,41 @@ __device__ __forceinline__ uint32_t pack_bf16_pt(float lo, float hi) {
 
 struct PtItem {
   int t0, t1, tab, slot_idx, grp, nq, h;
-  int head, r0, nr, p0;   // CAUSAL (prefill): q head, first batch row, rows, first position
+  int head, r0, nr, p0;   // causal modes: q head, first batch row, rows, first key index of the block
+  int rtab, npre, pbase;  // PT_SUF: row table offset; masked padding keys [npre, pbase) of the prefix pages
 };
-// item i: prefix pass = (tc task i / kvh, kv head i % kvh); causal prefill = (query block
-// i / qh of <= 128 positions, q head i % qh), keys [0, p0 + nr) of the request's prefix table
-template <bool CAUSAL>
-__device__ __forceinline__ PtItem pt_item(const AttnPlan& pl, const Dims& D, const int4* __restrict__ blocks, int i) {
+// modes: PT_PREFIX = the cascade's prefix pass (partials); PT_PREFILL = causal prefill of
+// prompt positions; PT_SUF = the f2 PRM pass (a row's new suffix entries over the virtual key
+// space [prefix pages (pbase slots, slots >= P - 1 masked) ; suffix entries])
+enum { PT_PREFIX = 0, PT_PREFILL = 1, PT_SUF = 2 };
+// item i: prefix pass = (tc task i / kvh, kv head i % kvh); causal modes = (query block i / qh
+// of <= 128 rows, q head i % qh), keys [0, p0 + nr)
+template <int MODE>
+__device__ __forceinline__ PtItem pt_item(const AttnPlan& pl, const Dims& D, const Rows& rows, const Reqs& reqs,
+                                          const int4* __restrict__ blocks, int i) {
   PtItem it;
-  if constexpr (CAUSAL) {
-    const int4 b = __ldg(blocks + i / D.qh);             // {first batch row, rows, slot, first position}
+  it.rtab = 0;
+  it.npre = it.pbase = 0x7fffffff;
+  if constexpr (MODE != PT_PREFIX) {
+    const int4 b = __ldg(blocks + i / D.qh);
     it.head = i % D.qh;
     it.h = it.head / D.g;
     it.r0 = b.x;
     it.nr = b.y;
-    it.p0 = b.w;
     it.t0 = 0;
-    it.t1 = b.w + b.y;
-    it.tab = b.z * D.MPB;
     it.slot_idx = it.grp = it.nq = 0;
+    if constexpr (MODE == PT_PREFILL) {                  // {first batch row, rows, slot, first position}
+      it.p0 = b.w;
+      it.tab = b.z * D.MPB;
+    } else {                                             // {first token, entries, row, first entry}
+      const int slot = rows.slot[b.z];
+      it.npre = reqs.P[slot] - 1;
+      it.pbase = (it.npre + D.bs - 1) / D.bs * D.bs;
+      it.p0 = it.pbase + b.w;
+      it.tab = slot * D.MPB;
+      it.rtab = b.z * D.MBR;
+    }
+    it.t1 = it.p0 + it.nr;
   } else {
     const int task = i / D.kvh;
     it.h = i % D.kvh;
@@ -97,7 +116,7 @@ __device__ __forceinline__ PtItem pt_item(const AttnPlan& pl, const Dims& D, con
   return it;
 }
 
-template <int HD, bool CAUSAL>
+template <int HD, int MODE>
 __global__ void __launch_bounds__(192, 1)
     k_attn_prefix_tc(const __grid_constant__ CUtensorMap kvmap, const bf16* __restrict__ q, float* __restrict__ part_o,
                      float* __restrict__ part_lse, bf16* __restrict__ out, const int4* __restrict__ blocks, int nblocks,
@@ -140,6 +159,7 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem = sm.tmem_base;
   pdl_wait();        // q of this step (QKV GEMM) and the step's item list are visible
   pdl_trigger();
+  constexpr bool CAUSAL = MODE != PT_PREFIX;
   const int n_items = CAUSAL ? nblocks * D.qh : *pl.n_tc * D.kvh;
   const float sl2 = 1.4426950408889634f * rsqrtf((float)HD);   // log2(e) / sqrt(hd)
 
@@ -149,8 +169,9 @@ __global__ void __launch_bounds__(192, 1)
       const int tpb = D.bs < PT_KT ? D.bs : PT_KT;     // tokens per box (whole page pieces)
       uint32_t tile = 0;
       for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
-        const PtItem it = pt_item<CAUSAL>(pl, D, blocks, i);
+        const PtItem it = pt_item<MODE>(pl, D, rows, reqs, blocks, i);
         const int* tab = reqs.prefix + it.tab;
+        const int* rtab = rows.table + it.rtab;            // PT_SUF: keys >= pbase are suffix entries
         for (int s0 = it.t0; s0 < it.t1; s0 += PT_KT, ++tile) {
           const int st = tile % PT_NS;
           mbar_wait(&sm.kv_empty[st], ((tile / PT_NS) & 1) ^ 1);
@@ -159,7 +180,7 @@ __global__ void __launch_bounds__(192, 1)
           mbar_expect_tx(&sm.kv_full[st], (uint32_t)(pieces * tpb * 2 * HD * 2));
           for (int pc = 0; pc < pieces; ++pc) {
             const int tok = s0 + pc * tpb;
-            const long long blk = tab[tok / D.bs];
+            const long long blk = tok < it.pbase ? tab[tok / D.bs] : rtab[(tok - it.pbase) / D.bs];
             const long long base = ((((long long)layer * D.NB + blk) * 2) * D.kvh + it.h) * D.bs + tok % D.bs;
             const int rk = (int)base, rv = (int)(base + (long long)D.kvh * D.bs);
 #pragma unroll
@@ -195,7 +216,7 @@ __global__ void __launch_bounds__(192, 1)
     };
     uint32_t tile = 0, icnt = 0;
     for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++icnt) {
-      const PtItem it = pt_item<CAUSAL>(pl, D, blocks, i);
+      const PtItem it = pt_item<MODE>(pl, D, rows, reqs, blocks, i);
       const int nt = (it.t1 - it.t0 + PT_KT - 1) / PT_KT;
       mbar_wait(&sm.q_full, icnt & 1);
       for (int kt = 0; kt < nt; ++kt) {
@@ -227,7 +248,7 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t tile = 0, icnt = 0;
     for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++icnt) {
-      const PtItem it = pt_item<CAUSAL>(pl, D, blocks, i);
+      const PtItem it = pt_item<MODE>(pl, D, rows, reqs, blocks, i);
       const int nt = (it.t1 - it.t0 + PT_KT - 1) / PT_KT;
       int row = -1, head = 0;
       if constexpr (CAUSAL) {
@@ -269,10 +290,12 @@ __global__ void __launch_bounds__(192, 1)
         // position); causal: key index <= the row's position p0 + j
         int nvalid = it.t1 - (it.t0 + kt * PT_KT);
         if constexpr (CAUSAL) nvalid = min(nvalid, it.p0 + j - kt * PT_KT + 1);
+        // PT_SUF: the prefix pages' padding slots [npre, pbase) of this tile are masked
+        const int h0 = it.npre - (it.t0 + kt * PT_KT), h1 = it.pbase - (it.t0 + kt * PT_KT);
         float mx = -INFINITY;
 #pragma unroll
         for (int c = 0; c < PT_KT; ++c)
-          if (c < nvalid) mx = fmaxf(mx, __uint_as_float(sr[c]));
+          if (c < nvalid && (MODE != PT_SUF || c < h0 || c >= h1)) mx = fmaxf(mx, __uint_as_float(sr[c]));
         const float mn = fmaxf(m, mx);
         const bool grow = kt == 0 || (mn - m) * sl2 > PT_LAZY;
         // P's buffer and O are free once the previous tile's PV has completed
@@ -301,7 +324,8 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int c = c8 * 8 + e;
-            p[e] = c < nvalid ? exp2f(fmaf(__uint_as_float(sr[c]), sl2, -mo)) : 0.f;
+            p[e] = c < nvalid && (MODE != PT_SUF || c < h0 || c >= h1) ? exp2f(fmaf(__uint_as_float(sr[c]), sl2, -mo))
+                                                                      : 0.f;
             l += p[e];
           }
           uint4 w;
@@ -390,19 +414,28 @@ bool make_kv_map(void* map_out, const bf16* pool, long long token_rows, int hd, 
 void launch_attn_prefix_tc(const bf16* q, const void* kv_map, float* part_o, float* part_lse, Dims D, int layer,
                            Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s) {
   const size_t smem = sizeof(PtSmem<128>) + 1024;
-  ensure_dyn_smem(k_attn_prefix_tc<128, false>, (int)smem);
-  launch_pdl(k_attn_prefix_tc<128, false>, dim3(pl.tc_grid), dim3(192), smem, s,
+  ensure_dyn_smem(k_attn_prefix_tc<128, PT_PREFIX>, (int)smem);
+  launch_pdl(k_attn_prefix_tc<128, PT_PREFIX>, dim3(pl.tc_grid), dim3(192), smem, s,
              *reinterpret_cast<const CUtensorMap*>(kv_map), q, part_o, part_lse, (bf16*)nullptr, (const int4*)nullptr, 0,
              D, layer, rows, reqs, pl);
 }
 
-void launch_attn_prefill_umma(const bf16* q, const void* kv_map, bf16* out, Dims D, int layer, Reqs reqs,
-                              const int4* blocks, int nblocks, cudaStream_t s) {
+template <int MODE>
+static void launch_causal(const bf16* q, const void* kv_map, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
+                          const int4* blocks, int nblocks, cudaStream_t s) {
   if (nblocks <= 0) return;
   const size_t smem = sizeof(PtSmem<128>) + 1024;
-  ensure_dyn_smem(k_attn_prefix_tc<128, true>, (int)smem);
+  ensure_dyn_smem(k_attn_prefix_tc<128, MODE>, (int)smem);
   const int items = nblocks * D.qh;
-  launch_pdl(k_attn_prefix_tc<128, true>, dim3(std::min(items, device_sms())), dim3(192), smem, s,
+  launch_pdl(k_attn_prefix_tc<128, MODE>, dim3(std::min(items, device_sms())), dim3(192), smem, s,
              *reinterpret_cast<const CUtensorMap*>(kv_map), q, (float*)nullptr, (float*)nullptr, out, blocks, nblocks,
-             D, layer, Rows{}, reqs, AttnPlan{});
+             D, layer, rows, reqs, AttnPlan{});
+}
+void launch_attn_prefill_umma(const bf16* q, const void* kv_map, bf16* out, Dims D, int layer, Reqs reqs,
+                              const int4* blocks, int nblocks, cudaStream_t s) {
+  launch_causal<PT_PREFILL>(q, kv_map, out, D, layer, Rows{}, reqs, blocks, nblocks, s);
+}
+void launch_attn_suffix_umma(const bf16* q, const void* kv_map, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
+                             const int4* qblocks, int nqb, cudaStream_t s) {
+  launch_causal<PT_SUF>(q, kv_map, out, D, layer, rows, reqs, qblocks, nqb, s);
 }

@@ -157,6 +157,9 @@ bool make_kv_map(void* map_out, const bf16* pool, long long token_rows, int hd, 
 // {first batch row, rows (<= 128), request slot, first position}; out[row][qh][hd] bf16
 void launch_attn_prefill_umma(const bf16* q, const void* kv_map, bf16* out, Dims D, int layer, Reqs reqs,
                               const int4* blocks, int nblocks, cudaStream_t s);
+// the same for one f2 PRM chunk: qblocks[i] = {first token, entries (<= 128), row, first entry}
+void launch_attn_suffix_umma(const bf16* q, const void* kv_map, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
+                             const int4* qblocks, int nqb, cudaStream_t s);
 void launch_attn_items(Dims D, Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s);
 // tensor-core causal prefill: blocks[i] = {first batch row, rows (<= prefill_query_block(D)),
 // slot, first position}

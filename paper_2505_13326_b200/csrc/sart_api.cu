@@ -631,7 +631,7 @@ void prm_model_scores(sart_ctx* ctx, int n) {
   CK_VOID(cudaStreamSynchronize(s));
   if (ncu_range) cudaProfilerStart();
   CK_VOID(cudaEventRecord(m->prm_ev[0], s));
-  const PrmPlan pl = plan_prm_pass(m->h_ell_ws, m->h_ell, n, m->prm_chunk, prefill_query_block(D));
+  const PrmPlan pl = plan_prm_pass(m->h_ell_ws, m->h_ell, n, m->prm_chunk, m->pf_umma ? 128 : prefill_query_block(D));
   const std::vector<int4>&seg = pl.seg, &qb = pl.qb, &gat = pl.gat;
   const std::vector<PrmPlan::Chunk>& chunks = pl.chunks;
   const long long entries = pl.entries;
@@ -660,8 +660,13 @@ void prm_model_scores(sart_ctx* ctx, int n) {
       launch_rmsnorm<T>(m->h, m->parts, np_res, m->W_<T>(t_layer(l, 0)), (T*)m->a, nullptr, nullptr, nt, D.d, D.eps,
                         s);
       qkv_rope<T>(m, l, nt, ra);
-      if constexpr (std::is_same<T, bf16>::value)
-        launch_attn_suffix_tc((bf16*)m->q, (bf16*)m->pool, (bf16*)m->o, D, l, m->rows, m->reqs, dqb + c.qb, c.nqb, s);
+      if constexpr (std::is_same<T, bf16>::value) {
+        if (m->pf_umma)
+          launch_attn_suffix_umma((bf16*)m->q, m->kv_map, (bf16*)m->o, D, l, m->rows, m->reqs, dqb + c.qb, c.nqb, s);
+        else
+          launch_attn_suffix_tc((bf16*)m->q, (bf16*)m->pool, (bf16*)m->o, D, l, m->rows, m->reqs, dqb + c.qb, c.nqb,
+                                s);
+      }
       else
         launch_attn_suffix<T>((T*)m->q, (T*)m->pool, (T*)m->o, D, l, m->rows, m->reqs, m->prm_row, m->prm_ent, nt, s);
       int np = proj<T>(m, (T*)m->o, m->W_<T>(t_layer(l, 3)), nt, D.d, D.qh * D.hd);
