@@ -402,13 +402,15 @@ typedef struct {
                               prefill chunk), both over the windows since the last reset */
   int64_t prefix_tc_windows; /* windows whose decode steps ran the tensor-core prefix pass of the
                               cascade attention (a request with >= 64 query rows: N x g) */
-  double attn_stream_ms;    /* profile mode: the part of attn_ms spent in the streaming kernel(s)
+  double attn_stream_ms;    /* profile mode 2: the part of attn_ms spent in the streaming kernel(s)
                               (k_attn_cascade, + k_attn_prefix_tc when on), merge excluded */
 } sart_profile;
 int sart_get_profile(sart_ctx* ctx, sart_profile* out);
 /* Turn per-launch attention timing on or off.  While on, decode steps are launched eagerly
- * with CUDA events around each attention launch; while off, each window's decode step is
- * captured once as a CUDA graph and replayed (the default serving mode). */
+ * with CUDA events around each attention launch (enable = 1: around the whole operator, the
+ * streaming kernel + merge -> attn_ms; enable = 2: also an event between the streaming kernel
+ * and the merge -> attn_stream_ms, which delays the merge's launch); while off, each window's
+ * decode step is captured once as a CUDA graph and replayed (the default serving mode). */
 int sart_set_profile(sart_ctx* ctx, int32_t enable);
 int sart_reset_profile(sart_ctx* ctx);
 

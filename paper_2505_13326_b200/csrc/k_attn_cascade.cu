@@ -125,7 +125,13 @@ __device__ __forceinline__ bool q_of(const AttnPlan& pl, const Dims& D, const It
 __device__ __forceinline__ int items_for_row(const AttnPlan& pl, const Dims& D, const Rows& rows, const Reqs& reqs,
                                              int r, int& npc, int& nsc) {
   npc = (reqs.P[rows.slot[r]] - 1 + pl.CH - 1) / pl.CH;
-  nsc = (rows.ell[r] + 1 + pl.CH - 1) / pl.CH;
+  const int len = rows.ell[r] + 1;
+  if (pl.PC) {   // whole chunks, then the pieces of the partial last chunk
+    const int nfull = len / pl.CH;
+    nsc = nfull + (len - nfull * pl.CH + pl.PC - 1) / pl.PC;
+  } else {
+    nsc = (len + pl.CH - 1) / pl.CH;
+  }
   const int j = pl.row_pos[r];
   const int tiles = (j * D.g + D.g - 1) / 16 - (j * D.g) / 16 + 1;   // prefix m-tiles holding this row
   return nsc + npc * tiles;
@@ -649,11 +655,25 @@ __global__ void __launch_bounds__(1024) k_attn_items(Dims D, Rows rows, Reqs req
       if (u.x == 0) {
         const int r = u.y;
         ok = rows.status[r] == RUNNING_ST;
-        t0 = u.z * pl.CH;
-        t1 = min(t0 + pl.CH, rows.ell[r] + 1);
+        const int len = rows.ell[r] + 1;
+        if (pl.PC) {   // unit u.z = piece u.z: a whole chunk is emitted by its first piece
+          const int q = pl.CH / pl.PC, nfull = len / pl.CH;
+          t0 = u.z * pl.PC;
+          if (u.z / q < nfull) {
+            ok = ok && (u.z % q) == 0;
+            t1 = t0 + pl.CH;
+            slot_idx = pl.npc_max + u.z / q;
+          } else {
+            t1 = min(t0 + pl.PC, len);
+            slot_idx = pl.npc_max + nfull + (u.z - nfull * q);
+          }
+        } else {
+          t0 = u.z * pl.CH;
+          t1 = min(t0 + pl.CH, len);
+          slot_idx = pl.npc_max + u.z;
+        }
         nq = D.g;
         tabbase = r * D.MBR;
-        slot_idx = pl.npc_max + u.z;
       } else {
         const int gi = u.y;
         const int n = pl.grp_n[gi];
@@ -750,7 +770,7 @@ __global__ void __launch_bounds__(1024) k_attn_plan(Dims D, Rows rows, Reqs reqs
     }
     for (int r = 0; r < n; ++r) {
       const int maxlen = min(rows.ell[r] + D.T, D.cap);   // suffix length at the window's last step
-      const int nsc = (maxlen + pl.CH - 1) / pl.CH;
+      const int nsc = (maxlen + (pl.PC ? pl.PC : pl.CH) - 1) / (pl.PC ? pl.PC : pl.CH);
       for (int c = 0; c < nsc; ++c) pl.units[nu++] = make_int4(0, r, c, 0);
     }
     *pl.n_units = nu;

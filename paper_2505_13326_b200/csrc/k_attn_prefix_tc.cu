@@ -52,9 +52,9 @@ struct PtSmem {
   alignas(1024) bf16 q[NH][PT_M * 64];                 // Q, K-major SW128: [half][row][64]
   alignas(1024) bf16 k[PT_NS][NH][PT_KT * 64];         // K tile: [half][token][64] (K-major B of S)
   alignas(1024) bf16 v[PT_NS][NH][PT_KT * 64];         // V tile: same bytes, MN-major B of O
-  alignas(1024) bf16 p[PT_M * PT_KT];                  // P, K-major SW128: [row][64 tokens]
+  alignas(1024) bf16 p[2][PT_M * PT_KT];               // P, K-major SW128: [row][64 tokens], double-buffered
   uint64_t kv_full[PT_NS], kv_empty[PT_NS], s_full[2], s_free[2];
-  uint64_t p_full, o_done, q_full;
+  uint64_t p_full[2], o_done[2], q_full;   // [tile & 1]
   uint32_t tmem_base;
 };
 
@@ -137,8 +137,10 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&sm.s_full[i], 1);
       mbar_init(&sm.s_free[i], 4);
     }
-    mbar_init(&sm.p_full, 4);
-    mbar_init(&sm.o_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.p_full[i], 4);
+      mbar_init(&sm.o_done[i], 1);
+    }
     mbar_init(&sm.q_full, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -198,10 +200,12 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(PT_KT >> 3) << 17) | ((uint32_t)(PT_M >> 4) << 24);
     const uint32_t idesc_o =
         (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(PT_M >> 4) << 24);
-    const uint32_t qa = smem_u32(&sm.q[0][0]), pa = smem_u32(&sm.p[0]);
+    const uint32_t qa = smem_u32(&sm.q[0][0]);
+    // PV of tile g reads P buffer g & 1 and completes on o_done[g & 1] (phase g >> 1)
     auto issue_pv = [&](uint32_t g, bool first) {
       const int st = g % PT_NS;
-      mbar_wait(&sm.p_full, g & 1);
+      const uint32_t pa = smem_u32(&sm.p[g & 1][0]);
+      mbar_wait(&sm.p_full[g & 1], (g >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (lane == 0) {
         const uint32_t va = smem_u32(&sm.v[st][0][0]);
@@ -210,7 +214,7 @@ __global__ void __launch_bounds__(192, 1)
           umma_bf16(tmem + O_COL, umma_desc_k(pa + kk * 32), umma_desc_mn(va + kk * 16 * 128, PT_KT * 128), idesc_o,
                     (first && kk == 0) ? 0u : 1u);
         umma_commit(&sm.kv_empty[st]);
-        umma_commit(&sm.o_done);
+        umma_commit(&sm.o_done[g & 1]);
       }
       __syncwarp();
     };
@@ -298,10 +302,15 @@ __global__ void __launch_bounds__(192, 1)
           if (c < nvalid && (MODE != PT_SUF || c < h0 || c >= h1)) mx = fmaxf(mx, __uint_as_float(sr[c]));
         const float mn = fmaxf(m, mx);
         const bool grow = kt == 0 || (mn - m) * sl2 > PT_LAZY;
-        // P's buffer and O are free once the previous tile's PV has completed
-        if (g > 0) mbar_wait(&sm.o_done, (g - 1) & 1);
+        // P buffer g & 1 is free once PV(g - 2) has completed; O may be rescaled only after
+        // PV(g - 1).  (Neither barrier can be two phases ahead of a wait: PV(t + 2) needs
+        // P(t + 2), which is written only after PV(t) was waited for.)
+        auto wait_pv = [&](uint32_t t) { mbar_wait(&sm.o_done[t & 1], (t >> 1) & 1); };
+        if (g >= 2) wait_pv(g - 2);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (kt > 0 && __any_sync(0xffffffffu, grow)) {
+          wait_pv(g - 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
           const float c = grow ? exp2f((m - mn) * sl2) : 1.f;
 #pragma unroll 1
           for (int cb = 0; cb < HD; cb += 32) {
@@ -317,7 +326,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         if (grow) m = mn;
         const float mo = m * sl2;
-        uint8_t* prow = reinterpret_cast<uint8_t*>(&sm.p[0]) + j * 128;
+        uint8_t* prow = reinterpret_cast<uint8_t*>(&sm.p[g & 1][0]) + j * 128;
 #pragma unroll
         for (int c8 = 0; c8 < PT_KT / 8; ++c8) {
           float p[8];
@@ -338,11 +347,11 @@ __global__ void __launch_bounds__(192, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.p_full);
+        if (lane == 0) mbar_arrive(&sm.p_full[g & 1]);
       }
       // item done: O / l and the lse into the partial slot of (row, head)
       const uint32_t glast = tile + nt - 1;
-      mbar_wait(&sm.o_done, glast & 1);
+      mbar_wait(&sm.o_done[glast & 1], (glast >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const float inv = 1.f / l;
       if constexpr (CAUSAL) {   // the prefill's attention output, bf16 [row][qh][hd]

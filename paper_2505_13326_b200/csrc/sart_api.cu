@@ -439,7 +439,8 @@ void layer_attention(sart_ctx* ctx, int l, int n) {
   // (g_attn_mid_event, recorded by launch_attn_cascade) and after the merge
   if (ctx->cfg.profile && ctx->ev_used + 3 <= (int)ctx->ev_pool.size()) {
     e0 = ctx->ev_pool[ctx->ev_used++];
-    g_attn_mid_event = ctx->ev_pool[ctx->ev_used++];
+    cudaEvent_t em = ctx->ev_pool[ctx->ev_used++];
+    if (ctx->cfg.profile == 2) g_attn_mid_event = em;   // (the mid event delays the merge's launch)
     e1 = ctx->ev_pool[ctx->ev_used++];
     cudaEventRecord(e0, ctx->st);
   }
@@ -1201,9 +1202,9 @@ int run_window(sart_ctx* ctx) {
     for (int i = 0; i + 2 < ctx->ev_used; i += 3) {
       float ms = 0.f, ms_s = 0.f;
       cudaEventElapsedTime(&ms, ctx->ev_pool[i], ctx->ev_pool[i + 2]);
-      cudaEventElapsedTime(&ms_s, ctx->ev_pool[i], ctx->ev_pool[i + 1]);
       ctx->attn_ms += ms;
-      ctx->attn_stream_ms += ms_s;
+      if (ctx->cfg.profile == 2 && cudaEventElapsedTime(&ms_s, ctx->ev_pool[i], ctx->ev_pool[i + 1]) == cudaSuccess)
+        ctx->attn_stream_ms += ms_s;
     }
   }
   return SART_OK;
@@ -1589,10 +1590,17 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     pl.tcq = 0;   // default off: measured -1.1% on C5 and -2.2% on C3 (profiles/r2_prefix_tc_ab.txt)
     if (const char* e = getenv("SART_ATTN_TCQ")) pl.tcq = D.hd == 128 ? std::max(0, atoi(e)) : 0;
     pl.qr_max = std::max(pl.qr_grp, pl.tcq ? std::min(SART_MAXN, 128 / D.g) : 1);
+    // SART_ATTN_PIECE: suffix piece length (0 = off; a divisor of CH, multiple of 16)
+    pl.PC = 0;
+    if (const char* e = getenv("SART_ATTN_PIECE")) {
+      const int pc = atoi(e) / 16 * 16;
+      if (pc >= 16 && pc < pl.CH && pl.CH % pc == 0) pl.PC = pc;
+    }
     pl.npc_max = std::max(1, cdiv(cfg.max_prompt - 1, pl.CH));
-    const int nsc_max = cdiv(D.cap, pl.CH);
+    const int nsc_max = cdiv(D.cap, pl.CH) + (pl.PC ? pl.CH / pl.PC : 0);   // chunks (+ pieces of the last)
     pl.nslot = pl.npc_max + nsc_max;
-    const size_t max_units = (size_t)D.R * (4 * pl.npc_max + nsc_max);
+    const int nsu_max = pl.PC ? cdiv(D.cap, pl.PC) : nsc_max;             // suffix units per row
+    const size_t max_units = (size_t)D.R * (4 * pl.npc_max + nsu_max);
     IC(dalloc(ctx, &pl.units, sizeof(int4) * max_units));
     IC(dalloc(ctx, &pl.n_units, sizeof(int)));
     IC(dalloc(ctx, &pl.work, sizeof(int) * D.L));
@@ -2159,7 +2167,7 @@ int sart_set_profile(sart_ctx* ctx, int32_t enable) {
     for (auto& ev : ctx->ev_pool)
       if (cudaEventCreate(&ev) != cudaSuccess) return set_err(SART_ECUDA, "event create");
   }
-  ctx->cfg.profile = enable ? 1 : 0;
+  ctx->cfg.profile = enable == 2 ? 2 : (enable ? 1 : 0);
   return SART_OK;
 }
 

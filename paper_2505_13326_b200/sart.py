@@ -468,5 +468,7 @@ class Engine:
     def reset_profile(self) -> None:
         _check(self.lib.sart_reset_profile(self.ctx))
 
-    def set_profile(self, enable: bool) -> None:
+    def set_profile(self, enable) -> None:
+        """False / True (1): events around each attention operator; 2: also between the
+        streaming kernel and the merge (attn_stream_ms)."""
         _check(self.lib.sart_set_profile(self.ctx, int(enable)))

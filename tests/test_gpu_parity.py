@@ -44,11 +44,12 @@ def oracle_teacher_forced(model, prompt, forced, steps, layers, prefix=None):
 
 
 def run_teacher_forced(shape, dtype, prompts, N, steps, bs, tol, std=0.08, seed=0, layers=None, attn_mode=0, T=1,
-                       attn_ch=None, num_blocks=4096, tcq=None, want_tc=None, max_rows=64):
+                       attn_ch=None, num_blocks=4096, tcq=None, want_tc=None, max_rows=64, piece=None):
     """Teacher-forced PP1 run.  T > 1: windows of T steps, compared at each window's last step
     (every row advances exactly T steps per window: forced tokens exclude EOS).  attn_ch: the
     cascade attention's chunk length (SART_ATTN_CH, read at sart_init), to put many suffix
-    chunks (slots npc_max + c) on the path.  tcq: threshold of the tensor-core prefix pass
+    chunks (slots npc_max + c) on the path.  piece: SART_ATTN_PIECE (the partial last suffix
+    chunk cut into pieces of that length).  tcq: threshold of the tensor-core prefix pass
     (SART_ATTN_TCQ; 0 = mma.sync prefix tasks only); want_tc: assert whether that pass ran."""
     import os
     layers = layers if layers is not None else sorted({0, shape.n_layers // 2, shape.n_layers - 1})
@@ -56,7 +57,7 @@ def run_teacher_forced(shape, dtype, prompts, N, steps, bs, tol, std=0.08, seed=
     model = Model(shape, weights)
     rng = np.random.default_rng(seed)
     assert steps % T == 0
-    env = {"SART_ATTN_CH": attn_ch, "SART_ATTN_TCQ": tcq}
+    env = {"SART_ATTN_CH": attn_ch, "SART_ATTN_TCQ": tcq, "SART_ATTN_PIECE": piece}
     old = {k: os.environ.get(k) for k in env}
     for k, v in env.items():
         if v is not None:
@@ -277,6 +278,21 @@ def test_multi_chunk_suffix_1p5b_geometry_ch64():
     prompts = [gen_prompt(23, shape.vocab, EOS, 300, 300)]
     w = run_teacher_forced(shape, "bf16", prompts, N=3, steps=208, bs=64, tol=2e-2, std=0.02, T=16, attn_ch=64)
     print("1.5B-L2 CH=64 208 steps worst", w)
+
+
+@pytest.mark.parametrize("name,piece", [("small", 16), ("1.5B", 32)])
+def test_multi_chunk_suffix_pieces(name, piece):
+    """SART_ATTN_PIECE: whole CH = 64 chunks stay items, the partial last chunk of every row is
+    cut into pieces of 16 / 32 tokens (slots npc_max + nfull + p, up to 4 / 2 pieces) -- the
+    slot mapping changes every step as l crosses chunk and piece boundaries."""
+    if name == "small":
+        shape, P, N, steps, bs, T = SHAPES["small"], 100, 4, 200, 16, 8
+    else:
+        shape, P, N, steps, bs, T = SHAPES["1.5B"].with_layers(2), 300, 3, 160, 64, 16
+    prompts = [gen_prompt(25, shape.vocab, EOS, P, P), gen_prompt(26, shape.vocab, EOS, 33, 33)]
+    w = run_teacher_forced(shape, "bf16", prompts, N=N, steps=steps, bs=bs, tol=2e-2, std=0.02, T=T, attn_ch=64,
+                           piece=piece)
+    print(f"{name} CH=64 pieces of {piece}, {steps} steps worst", w)
 
 
 def test_multi_chunk_suffix_production_ch():
