@@ -1,5 +1,6 @@
 // Shared device-side definitions of the SART engine (sm_100a).
 #pragma once
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -179,7 +180,9 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  // SART_NO_PDL=1: plain stream order (diagnostics)
+  static const int pdl = getenv("SART_NO_PDL") && atoi(getenv("SART_NO_PDL")) ? 0 : 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);

@@ -28,3 +28,14 @@ timeout 1800 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest
   -k "interleaved_prefill_random_workloads[0] or es_every_step_trace_B or model_mode_bf16_replay[True] or cta_pair_matches_one_sm[200 or kv_pool" \
   > gpurun_out/sanitize_r2.log 2>&1; echo r2_rc=$?; tail -3 gpurun_out/sanitize_r2.log
 fi
+# round 2, session 2: the tcgen05 attention kernel in its three modes (causal prefill of the
+# hd-128 `small` shape, the concurrent prefix pass, the f2 PRM pass over prm-small) and the
+# suffix pieces (SART_ATTN_PIECE)
+if [ -n "$SANITIZE_S2" ]; then
+timeout 1800 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_parity.py tests/test_gpu_prm_model.py -x -q \
+  -k "prefix_tc_pass[small or pieces[small or small-prm-small-bf16" > gpurun_out/sanitize_s2.log 2>&1; echo s2_rc=$?; tail -3 gpurun_out/sanitize_s2.log
+for tool in racecheck synccheck; do
+  timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests/test_gpu_prm_model.py -x -q \
+    -k "small-prm-small-bf16-16-40-None" > gpurun_out/sanitize_s2_$tool.log 2>&1; echo s2_${tool}_rc=$?; tail -2 gpurun_out/sanitize_s2_$tool.log
+done
+fi

@@ -42,6 +42,7 @@ def worker(rank, port):
     prompt = gen_prompt(45, shape.vocab, 1, 30, 30)
     e.admit(Request(0, prompt, 2, 2, -1.0, 0, None), forced_tokens=ft)
     ref = ref_logits(shape, weights, prompt, ft, 16)
+    errs = []
     for w in range(2):
         e.step(1)
         lg = e.debug_fetch(DBG_LOGITS)
@@ -49,8 +50,8 @@ def worker(rank, port):
         for i, k in enumerate(ids):
             b = int(k) & 0xFF
             r = ref[(b, 8 * (w + 1))]
-            print(f"rank {rank} window {w} row b{b} rel err {np.max(np.abs(lg[i] - r)) / np.max(np.abs(r)):.4e}",
-                  flush=True)
+            errs.append(f"w{w}b{b} {np.max(np.abs(lg[i] - r)) / np.max(np.abs(r)):.3e}")
+    print(f"rank {rank} rel err " + " ".join(errs), flush=True)
     e.close()
     dist.barrier()
     dist.destroy_process_group()
