@@ -253,13 +253,30 @@ cudaError_t xfer(sart_ctx* ctx, void* dst, const void* src, size_t bytes, cudaMe
   return cudaMemcpyAsync(dst, src, bytes, k, s);
 }
 
+// Host <-> device operations on the legacy default stream (initialisation uploads) complete
+// before anything on the ctx's non-blocking stream may touch the same memory.
+inline cudaError_t dsync(cudaError_t e) { return e == cudaSuccess ? cudaDeviceSynchronize() : e; }
+
 template <typename P>
 cudaError_t dalloc(sart_ctx* ctx, P** p, size_t bytes, bool zero = true) {
   void* v = nullptr;
   cudaError_t e = cudaMalloc(&v, bytes ? bytes : 16);
   if (e != cudaSuccess) return e;
   ctx->allocs.push_back(v);
-  if (zero) e = cudaMemset(v, 0, bytes ? bytes : 16);
+  // zeroed on the ctx's own stream and completed before returning: a plain cudaMemset runs on
+  // the legacy default stream, which a non-blocking ctx stream does not wait for -- executed
+  // late (seen with two processes time-sharing one GPU) it wiped state the ctx's kernels had
+  // already written (work counters, TP arrival counters / receive buffers): tests/test_gpu_tp.py
+  // two-process IPC, profiles/r2_tp_ipc_flake.txt
+  if (zero) {
+    if (ctx->st) {
+      e = cudaMemsetAsync(v, 0, bytes ? bytes : 16, ctx->st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
+    } else {
+      e = cudaMemset(v, 0, bytes ? bytes : 16);
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+  }
   *p = (P*)v;
   return e;
 }
@@ -1080,7 +1097,7 @@ int run_window(sart_ctx* ctx) {
         if (si.live && si.N * D.g >= ctx->plan.tcq) ctx->tc_prefix_window = true;
     ctx->prefix_tc_windows += ctx->tc_prefix_window;
     // the pass's SMs (SART_TC_SMS); the cascade kernel streams the suffixes on the others
-    static const int tc_sms = getenv("SART_TC_SMS") ? atoi(getenv("SART_TC_SMS")) : 64;
+    static const int tc_sms = getenv("SART_TC_SMS") ? atoi(getenv("SART_TC_SMS")) : 96;
     ctx->plan.tc_grid = ctx->tc_prefix_window ? std::max(1, std::min(tc_sms, device_sms())) : 0;
     launch_attn_plan(D, ctx->rows, ctx->reqs, ctx->plan, n, ctx->cfg.attn_mode == SART_ATTN_FLAT, ctx->st);
     ctx->launches++;
@@ -1271,10 +1288,10 @@ int init_model(sart_ctx* ctx, const void* host_w, uint64_t seed, float wstd) {
           const char* src = (const char*)host_w + foff[i] * es;
           const long long rows = g.n / g.cl;
           if (rows == 1)
-            MC(cudaMemcpy(dst, src + (g.goff + g.c0) * es, g.n * es, cudaMemcpyHostToDevice));
+            MC(dsync(cudaMemcpy(dst, src + (g.goff + g.c0) * es, g.n * es, cudaMemcpyHostToDevice)));
           else
-            MC(cudaMemcpy2D(dst, g.cl * es, src + (g.goff + g.c0) * es, g.cf * es, g.cl * es, rows,
-                            cudaMemcpyHostToDevice));
+            MC(dsync(cudaMemcpy2D(dst, g.cl * es, src + (g.goff + g.c0) * es, g.cf * es, g.cl * es, rows,
+                            cudaMemcpyHostToDevice)));
         } else if (ctx->bf16) {
           launch_init_slice<bf16>((bf16*)dst, g.n, (int)i, nrm, wstd, seed, g.cl, g.cf, g.c0, g.goff, ctx->st);
         } else {
@@ -1284,7 +1301,7 @@ int init_model(sart_ctx* ctx, const void* host_w, uint64_t seed, float wstd) {
     }
     MC(cudaGetLastError());
   } else if (host_w) {
-    MC(cudaMemcpy(ctx->wblob, host_w, total * es, cudaMemcpyHostToDevice));
+    MC(dsync(cudaMemcpy(ctx->wblob, host_w, total * es, cudaMemcpyHostToDevice)));
   } else {
     for (size_t i = 0; i < sizes.size(); ++i) {
       bool norm = is_norm_tensor(D, (int)i);
@@ -1335,7 +1352,7 @@ int init_model(sart_ctx* ctx, const void* host_w, uint64_t seed, float wstd) {
         cs[(size_t)p * D.hd + half + i] = (float)std::sin(ang);
       }
     MC(dalloc(ctx, &ctx->rope_cs, cs.size() * sizeof(float), false));
-    MC(cudaMemcpy(ctx->rope_cs, cs.data(), cs.size() * sizeof(float), cudaMemcpyHostToDevice));
+    MC(dsync(cudaMemcpy(ctx->rope_cs, cs.data(), cs.size() * sizeof(float), cudaMemcpyHostToDevice)));
   }
   MC(dalloc(ctx, &ctx->h, W * D.d * 4));
   MC(dalloc(ctx, &ctx->parts, W * std::max(D.qkv, D.d) * 8 * 4, false));   // split-K partials (S <= 8)
@@ -1556,7 +1573,7 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   IC(dalloc(ctx, &ctx->ctr, sizeof(Ctr) + sizeof(int) * D.S));
   IC(dalloc(ctx, &ctx->res, sizeof(DevResult) * D.S));
   IC(dalloc(ctx, &ctx->slot_row, sizeof(int) * (size_t)D.S * SART_MAXN));
-  IC(cudaMemset(ctx->slot_row, 0xff, sizeof(int) * (size_t)D.S * SART_MAXN));
+  IC(dsync(cudaMemset(ctx->slot_row, 0xff, sizeof(int) * (size_t)D.S * SART_MAXN)));
   // ---- workspaces
   IC(dalloc(ctx, &ctx->logits, (size_t)D.R * D.V * 4));
   IC(dalloc(ctx, &ctx->dbg_tok, (size_t)D.R * 4));
@@ -1587,7 +1604,11 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     if (const char* e = getenv("SART_ATTN_QR")) pl.qr_grp = std::max(1, std::min(SART_MAXN, atoi(e)));   // A/B
     // tensor-core prefix pass (hd 128, bf16 pool): groups of >= tcq query rows; SART_ATTN_TCQ
     // sets the threshold (0 = off).  Enabled after the pool's tensor map is encoded.
-    pl.tcq = 0;   // default off: measured -1.1% on C5 and -2.2% on C3 (profiles/r2_prefix_tc_ab.txt)
+    // default 64 query rows (C3: N 16 x g 7, C5: 32 x 5; not C2: 8 x 6), running concurrently with
+    // the cascade kernel on SART_TC_SMS = 96 SMs: C5 step -2.0%, C3 -1.0%
+    // (profiles/r2_prefix_tc_concurrent_ab.txt; serialised before the cascade it was a loss,
+    // profiles/r2_prefix_tc_ab.txt)
+    pl.tcq = D.hd == 128 ? 64 : 0;
     if (const char* e = getenv("SART_ATTN_TCQ")) pl.tcq = D.hd == 128 ? std::max(0, atoi(e)) : 0;
     pl.qr_max = std::max(pl.qr_grp, pl.tcq ? std::min(SART_MAXN, 128 / D.g) : 1);
     // SART_ATTN_PIECE: suffix piece length (0 = off; a divisor of CH, multiple of 16)
@@ -1683,10 +1704,10 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   {
     std::vector<int> fs(NB);
     for (long long i = 0; i < NB; ++i) fs[i] = (int)(NB - 1 - i);   // bottom -> top: NB-1 ... 0
-    IC(cudaMemcpy(ctx->free_stack, fs.data(), sizeof(int) * NB, cudaMemcpyHostToDevice));
+    IC(dsync(cudaMemcpy(ctx->free_stack, fs.data(), sizeof(int) * NB, cudaMemcpyHostToDevice)));
     Ctr c0{};
     c0.free_top = NB;
-    IC(cudaMemcpy(ctx->ctr, &c0, sizeof(Ctr), cudaMemcpyHostToDevice));
+    IC(dsync(cudaMemcpy(ctx->ctr, &c0, sizeof(Ctr), cudaMemcpyHostToDevice)));
   }
   ctx->free_top = NB;
   ctx->slots.resize(D.S);
