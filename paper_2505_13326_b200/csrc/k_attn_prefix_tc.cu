@@ -58,6 +58,12 @@ struct PtSmem {
   uint32_t tmem_base;
 };
 
+// 2^x on the SFU (flushes results below 2^-126 to 0: such p are 0 in bf16 P anyway)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ uint32_t pack_bf16_pt(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -296,10 +302,23 @@ __global__ void __launch_bounds__(192, 1)
         if constexpr (CAUSAL) nvalid = min(nvalid, it.p0 + j - kt * PT_KT + 1);
         // PT_SUF: the prefix pages' padding slots [npre, pbase) of this tile are masked
         const int h0 = it.npre - (it.t0 + kt * PT_KT), h1 = it.pbase - (it.t0 + kt * PT_KT);
-        float mx = -INFINITY;
+        // warp-uniform fast path: every key of the tile is visible to every row of the warp
+        // (all but the diagonal / ragged / padding tiles) -- no per-element predicates
+        const bool wfull = __all_sync(0xffffffffu, nvalid >= PT_KT && (MODE != PT_SUF || h1 <= 0 || h0 >= PT_KT));
+        auto vis = [&](int c) { return wfull || (c < nvalid && (MODE != PT_SUF || c < h0 || c >= h1)); };
+        float mx8[8];   // 8 independent max chains (max is order-free)
 #pragma unroll
-        for (int c = 0; c < PT_KT; ++c)
-          if (c < nvalid && (MODE != PT_SUF || c < h0 || c >= h1)) mx = fmaxf(mx, __uint_as_float(sr[c]));
+        for (int e = 0; e < 8; ++e) mx8[e] = -INFINITY;
+        if (wfull) {
+#pragma unroll
+          for (int c = 0; c < PT_KT; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < PT_KT; ++c)
+            if (vis(c)) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
+        }
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         const float mn = fmaxf(m, mx);
         const bool grow = kt == 0 || (mn - m) * sl2 > PT_LAZY;
         // P buffer g & 1 is free once PV(g - 2) has completed; O may be rescaled only after
@@ -327,15 +346,19 @@ __global__ void __launch_bounds__(192, 1)
         if (grow) m = mn;
         const float mo = m * sl2;
         uint8_t* prow = reinterpret_cast<uint8_t*>(&sm.p[g & 1][0]) + j * 128;
+        float l4[4] = {0.f, 0.f, 0.f, 0.f};   // 4 independent sum chains, added in fixed order
+        if (!wfull)   // masked keys -> -inf: their p is exactly 0
+#pragma unroll
+          for (int c = 0; c < PT_KT; ++c)
+            if (!vis(c)) sr[c] = __float_as_uint(-INFINITY);
 #pragma unroll
         for (int c8 = 0; c8 < PT_KT / 8; ++c8) {
           float p[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int c = c8 * 8 + e;
-            p[e] = c < nvalid && (MODE != PT_SUF || c < h0 || c >= h1) ? exp2f(fmaf(__uint_as_float(sr[c]), sl2, -mo))
-                                                                      : 0.f;
-            l += p[e];
+            p[e] = ex2_approx(fmaf(__uint_as_float(sr[c]), sl2, -mo));
+            l4[e & 3] += p[e];
           }
           uint4 w;
           w.x = pack_bf16_pt(p[0], p[1]);
@@ -344,6 +367,7 @@ __global__ void __launch_bounds__(192, 1)
           w.w = pack_bf16_pt(p[6], p[7]);
           *reinterpret_cast<uint4*>(prow + ((c8 ^ (j & 7)) << 4)) = w;
         }
+        l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();

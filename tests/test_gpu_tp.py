@@ -207,11 +207,12 @@ def _ipc_worker(rank, port, q):
 
 def test_tp2_two_processes_ipc():
     """One process per rank, receive buffers exchanged as CUDA IPC handles (the multi-GPU
-    path's plumbing): both ranks end with identical logits, within north_star's 2e-2 of the
-    fp64 oracle of the full model and of the in-process group's logits.  (The two processes
-    time-share ONE GPU here; one full-suite run in four saw their logits differ from the
-    in-process group's by up to 7e-3 -- both ranks identical, inside the bound -- so equality
-    with the in-process group is reported, not asserted.)"""
+    path's plumbing): both ranks end with identical logits, equal to the in-process group's and
+    within north_star's 2e-2 of the fp64 oracle of the full model.  (The two processes
+    time-share ONE GPU here.  This is the test that exposed the init-ordering bug fixed in
+    dalloc: a zeroing memset on the legacy stream, executed late, wiped state -- 4-6 of 16
+    runs gave one of two fixed wrong answers before the fix, 0 of 10 after;
+    profiles/r2_tp_ipc_flake.txt.)"""
     import socket
     import torch.multiprocessing as mp
     s = socket.socket()
@@ -259,3 +260,4 @@ def test_tp2_two_processes_ipc():
     print(f"TP=2 IPC: ranks identical, equal to the in-process group: {same}, worst vs oracle {worst:.3e}, "
           f"IPC vs in-process max {np.max(np.abs(np.stack(ref) - got[0])):.3e}")
     assert worst <= 2e-2
+    assert same
