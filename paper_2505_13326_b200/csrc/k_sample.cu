@@ -41,11 +41,16 @@ __global__ void __launch_bounds__(256) k_sample_part(const float* __restrict__ l
       better(bk, bv, (D.tau == 1.0f ? lg[v] : lg[v] / D.tau) + gumbel_from_word(w.x), v);
     }
   }
-  for (int base = g_lo; base < g_hi; base += blockDim.x) {   // uniform trip count (warp shuffles)
-    // best key held anywhere in the warp so far: a valid pruning bound for every lane
-    float wb = bk;
+  float wb = -INFINITY;
+  int it = 0;
+  for (int base = g_lo; base < g_hi; base += blockDim.x, ++it) {   // uniform trip count (warp shuffles)
+    // a key some entry already has is a valid pruning bound: the lane's own best every
+    // iteration, the warp's best every 4th (a stale bound only prunes less)
+    wb = fmaxf(wb, bk);
+    if ((it & 3) == 0) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wb = fmaxf(wb, __shfl_xor_sync(0xffffffffu, wb, o));
+      for (int o = 16; o > 0; o >>= 1) wb = fmaxf(wb, __shfl_xor_sync(0xffffffffu, wb, o));
+    }
     const int g4 = base + threadIdx.x;
     if (g4 >= g_hi) continue;
     const float4 l4 = (D.V % 4 == 0 && 4 * g4 + 3 < D.V) ? *reinterpret_cast<const float4*>(lg + 4 * g4)

@@ -29,22 +29,30 @@ __device__ __forceinline__ bool gumbel_cannot_reach(uint32_t w, float lp, float 
 }
 
 // fold 4 consecutive vocab entries v0..v0+3 (v0 % 4 == 0) into (bk, bv); entries whose key
-// provably stays below `bound` are skipped (see gumbel_cannot_reach)
+// provably stays below `bound` are skipped (see gumbel_cannot_reach).  The skip threshold is
+// computed once per group from the group's largest l': exp(l'_j - bound) <= exp(max l' -
+// bound), so the per-entry test is weaker than gumbel_cannot_reach's and skips only entries
+// that test would skip as well (every result is unchanged).
 __device__ __forceinline__ void sample_group4(float& bk, int& bv, const float* lv, int v0, int V, int s, uint32_t rid,
                                               uint32_t b, uint32_t k0, uint32_t k1, float tau, bool mask_eos,
                                               int eos, float bound = -INFINITY) {
   u32x4 w{0, 0, 0, 0};
   if (tau > 0.f) w = philox4x32_10(u32x4{(uint32_t)(v0 >> 2), (uint32_t)s, rid, b}, k0, k1);
   const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+  float lp[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) lp[j] = tau == 1.0f ? lv[j] : lv[j] / tau;
+  const float thr = __expf(fmaxf(fmaxf(lp[0], lp[1]), fmaxf(lp[2], lp[3])) - bound) * 1.001f;
+  const bool full = v0 + 3 < V && !mask_eos;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int v = v0 + j;
-    if (v >= V || (mask_eos && v == eos)) continue;
+    if (!full && (v >= V || (mask_eos && v == eos))) continue;
     float key;
     if (tau > 0.f) {
-      const float lp = tau == 1.0f ? lv[j] : lv[j] / tau;
-      if (gumbel_cannot_reach(ws[j], lp, bound)) continue;
-      key = lp + gumbel_from_word(ws[j]);
+      const float one_minus_u = ((float)((1u << 24) - (ws[j] >> 8)) - 0.5f) * (1.0f / 16777216.0f);
+      if (one_minus_u > thr) continue;
+      key = lp[j] + gumbel_from_word(ws[j]);
     } else {
       key = lv[j];
     }
