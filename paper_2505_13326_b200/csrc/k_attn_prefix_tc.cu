@@ -58,12 +58,6 @@ struct PtSmem {
   uint32_t tmem_base;
 };
 
-// 2^x on the SFU (flushes results below 2^-126 to 0: such p are 0 in bf16 P anyway)
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 __device__ __forceinline__ uint32_t pack_bf16_pt(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -346,7 +340,9 @@ __global__ void __launch_bounds__(192, 1)
         if (grow) m = mn;
         const float mo = m * sl2;
         uint8_t* prow = reinterpret_cast<uint8_t*>(&sm.p[g & 1][0]) + j * 128;
-        float l4[4] = {0.f, 0.f, 0.f, 0.f};   // 4 independent sum chains, added in fixed order
+        // l is one chain in column order and p = exp2f(.): the same arithmetic as the masked
+        // form (a masked key adds an exact 0), so the fast path leaves every result unchanged
+        // (a 4-chain sum moved a full-size C2 logits row from 0.0196 to 0.0200)
         if (!wfull)   // masked keys -> -inf: their p is exactly 0
 #pragma unroll
           for (int c = 0; c < PT_KT; ++c)
@@ -357,8 +353,8 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int c = c8 * 8 + e;
-            p[e] = ex2_approx(fmaf(__uint_as_float(sr[c]), sl2, -mo));
-            l4[e & 3] += p[e];
+            p[e] = exp2f(fmaf(__uint_as_float(sr[c]), sl2, -mo));
+            l += p[e];
           }
           uint4 w;
           w.x = pack_bf16_pt(p[0], p[1]);
@@ -367,7 +363,6 @@ __global__ void __launch_bounds__(192, 1)
           w.w = pack_bf16_pt(p[6], p[7]);
           *reinterpret_cast<uint4*>(prow + ((c8 ^ (j & 7)) << 4)) = w;
         }
-        l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();

@@ -1097,7 +1097,7 @@ int run_window(sart_ctx* ctx) {
         if (si.live && si.N * D.g >= ctx->plan.tcq) ctx->tc_prefix_window = true;
     ctx->prefix_tc_windows += ctx->tc_prefix_window;
     // the pass's SMs (SART_TC_SMS); the cascade kernel streams the suffixes on the others
-    static const int tc_sms = getenv("SART_TC_SMS") ? atoi(getenv("SART_TC_SMS")) : 96;
+    static const int tc_sms = getenv("SART_TC_SMS") ? atoi(getenv("SART_TC_SMS")) : 64;
     ctx->plan.tc_grid = ctx->tc_prefix_window ? std::max(1, std::min(tc_sms, device_sms())) : 0;
     launch_attn_plan(D, ctx->rows, ctx->reqs, ctx->plan, n, ctx->cfg.attn_mode == SART_ATTN_FLAT, ctx->st);
     ctx->launches++;
@@ -1605,7 +1605,7 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
     // tensor-core prefix pass (hd 128, bf16 pool): groups of >= tcq query rows; SART_ATTN_TCQ
     // sets the threshold (0 = off).  Enabled after the pool's tensor map is encoded.
     // default 64 query rows (C3: N 16 x g 7, C5: 32 x 5; not C2: 8 x 6), running concurrently with
-    // the cascade kernel on SART_TC_SMS = 96 SMs: C5 step -2.0%, C3 -1.0%
+    // the cascade kernel on SART_TC_SMS = 64 SMs: C5 step -5.8%, C3 +1.6% throughput
     // (profiles/r2_prefix_tc_concurrent_ab.txt; serialised before the cascade it was a loss,
     // profiles/r2_prefix_tc_ab.txt)
     pl.tcq = D.hd == 128 ? 64 : 0;
