@@ -894,6 +894,7 @@ static void launch_hd(const bf16* q, const bf16* pool, bf16* out, float* dbg, fl
     case 0: launch_cfg<HD, 6, 2, 32>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
     case 2: launch_cfg<HD, 6, 4, 16>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
     case 3: launch_cfg<HD, 7, 3, 16>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
+    case 4: launch_cfg<HD, 7, 2, 32>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;   // 224 KB
     default: launch_cfg<HD, 8, 3, 16>(q, pool, part_o, part_lse, out, dbg, D, layer, rows, reqs, pl, s); break;
   }
   if (g_attn_mid_event) cudaEventRecord(g_attn_mid_event, s);
