@@ -36,26 +36,41 @@
 // PRM pass: the rows are one batch row's new suffix entries, the keys its prefix pages
 // (padding slots masked) followed by its suffix entries.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "umma.cuh"
 
 namespace {
 constexpr int PT_KT = 64;    // key tokens per KV tile (one S buffer = 64 TMEM columns)
-constexpr int PT_NS = 4;     // KV tile stages
 constexpr int PT_M = 128;    // query rows per item (TMEM lanes)
 constexpr float PT_LAZY = 8.f;   // rescale O only when the max grows by more than 2^8 (log2 units)
 
-template <int HD>
-struct PtSmem {
+// NS KV tile stages, NP P buffers (P(g) in buffer g % NP); (NS, NP) = (4, 2): one CTA per SM
+// (~194 KB), (2, 1): two CTAs per SM (112 KB each, 256 TMEM columns each) whose softmax and
+// MMA phases interleave.  Layout from a 1024-byte aligned base: q | k | v | p (all 1024-byte
+// multiples, as the SW128 UMMA descriptors need) | mbarriers | TMEM base address.
+template <int HD, int NS, int NP>
+struct PtView {
   static constexpr int NH = HD / 64;                   // 128-byte column halves of a row
-  alignas(1024) bf16 q[NH][PT_M * 64];                 // Q, K-major SW128: [half][row][64]
-  alignas(1024) bf16 k[PT_NS][NH][PT_KT * 64];         // K tile: [half][token][64] (K-major B of S)
-  alignas(1024) bf16 v[PT_NS][NH][PT_KT * 64];         // V tile: same bytes, MN-major B of O
-  alignas(1024) bf16 p[2][PT_M * PT_KT];               // P, K-major SW128: [row][64 tokens], double-buffered
-  uint64_t kv_full[PT_NS], kv_empty[PT_NS], s_full[2], s_free[2];
-  uint64_t p_full[2], o_done[2], q_full;   // [tile & 1]
-  uint32_t tmem_base;
+  static constexpr size_t QB = (size_t)NH * PT_M * 64 * 2, KB = (size_t)NS * NH * PT_KT * 64 * 2,
+                          PB = (size_t)NP * PT_M * PT_KT * 2, NBAR = 2 * NS + 4 + 2 * NP + 1;
+  static constexpr size_t BYTES = QB + 2 * KB + PB + 8 * NBAR + 16;
+  bf16 (*q)[PT_M * 64];                                // Q, K-major SW128: [half][row][64]
+  bf16 (*k)[NH][PT_KT * 64];                           // K tile: [half][token][64] (K-major B of S)
+  bf16 (*v)[NH][PT_KT * 64];                           // V tile: same bytes, MN-major B of O
+  bf16 (*p)[PT_M * PT_KT];                             // P, K-major SW128: [row][64 tokens]
+  uint64_t *kv_full, *kv_empty, *s_full, *s_free, *p_full, *o_done;   // [NS] [NS] [2] [2] [NP] [NP]
+  uint64_t& q_full;
+  uint32_t& tmem_base;
+  __device__ explicit PtView(uint8_t* b)
+      : q(reinterpret_cast<bf16 (*)[PT_M * 64]>(b)),
+        k(reinterpret_cast<bf16 (*)[NH][PT_KT * 64]>(b + QB)),
+        v(reinterpret_cast<bf16 (*)[NH][PT_KT * 64]>(b + QB + KB)),
+        p(reinterpret_cast<bf16 (*)[PT_M * PT_KT]>(b + QB + 2 * KB)),
+        kv_full(reinterpret_cast<uint64_t*>(b + QB + 2 * KB + PB)),
+        kv_empty(kv_full + NS), s_full(kv_empty + NS), s_free(s_full + 2), p_full(s_free + 2), o_done(p_full + NP),
+        q_full(o_done[NP]), tmem_base(*reinterpret_cast<uint32_t*>(o_done + NP + 1)) {}
 };
 
 __device__ __forceinline__ uint32_t pack_bf16_pt(float lo, float hi) {
@@ -116,20 +131,25 @@ __device__ __forceinline__ PtItem pt_item(const AttnPlan& pl, const Dims& D, con
   return it;
 }
 
-template <int HD, int MODE>
-__global__ void __launch_bounds__(192, 1)
+template <int HD, int MODE, int NS, int NP, int MINB>
+__global__ void __launch_bounds__(192, MINB)
     k_attn_prefix_tc(const __grid_constant__ CUtensorMap kvmap, const bf16* __restrict__ q, float* __restrict__ part_o,
                      float* __restrict__ part_lse, bf16* __restrict__ out, const int4* __restrict__ blocks, int nblocks,
                      Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl) {
   constexpr int NH = HD / 64;
   constexpr uint32_t TMEM_COLS = 256;                  // S0 | S1 | O (HD <= 128 columns)
   constexpr uint32_t O_COL = 128;
-  extern __shared__ __align__(16) uint8_t pt_raw[];
-  PtSmem<HD>& sm = *reinterpret_cast<PtSmem<HD>*>((reinterpret_cast<uintptr_t>(pt_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t pt_raw[];
+  // one CTA per SM: the launch adds 1024 bytes of slack to align the base here; two per SM
+  // have no room for it, and rely on the dynamic window starting 1024-aligned (checked)
+  uint8_t* base = pt_raw;
+  if constexpr (MINB == 1) base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(pt_raw) + 1023) & ~uintptr_t(1023));
+  else if (smem_u32(pt_raw) & 1023) __trap();
+  PtView<HD, NS, NP> sm(base);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < PT_NS; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&sm.kv_full[i], 1);
       mbar_init(&sm.kv_empty[i], 1);
     }
@@ -137,7 +157,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&sm.s_full[i], 1);
       mbar_init(&sm.s_free[i], 4);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NP; ++i) {
       mbar_init(&sm.p_full[i], 4);
       mbar_init(&sm.o_done[i], 1);
     }
@@ -150,7 +170,7 @@ __global__ void __launch_bounds__(192, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   // stale V rows of a partial last tile are multiplied by P = 0: keep them finite
-  for (int e = threadIdx.x; e < PT_NS * NH * PT_KT * 64 / 8; e += blockDim.x) {
+  for (int e = threadIdx.x; e < NS * NH * PT_KT * 64 / 8; e += blockDim.x) {
     reinterpret_cast<uint4*>(&sm.k[0][0][0])[e] = make_uint4(0, 0, 0, 0);
     reinterpret_cast<uint4*>(&sm.v[0][0][0])[e] = make_uint4(0, 0, 0, 0);
   }
@@ -175,8 +195,8 @@ __global__ void __launch_bounds__(192, 1)
         const int* tab = reqs.prefix + it.tab;
         const int* rtab = rows.table + it.rtab;            // PT_SUF: keys >= pbase are suffix entries
         for (int s0 = it.t0; s0 < it.t1; s0 += PT_KT, ++tile) {
-          const int st = tile % PT_NS;
-          mbar_wait(&sm.kv_empty[st], ((tile / PT_NS) & 1) ^ 1);
+          const int st = tile % NS;
+          mbar_wait(&sm.kv_empty[st], ((tile / NS) & 1) ^ 1);
           const int ntok = min(PT_KT, it.t1 - s0);
           const int pieces = (ntok + tpb - 1) / tpb;
           mbar_expect_tx(&sm.kv_full[st], (uint32_t)(pieces * tpb * 2 * HD * 2));
@@ -201,11 +221,11 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t idesc_o =
         (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(PT_M >> 4) << 24);
     const uint32_t qa = smem_u32(&sm.q[0][0]);
-    // PV of tile g reads P buffer g & 1 and completes on o_done[g & 1] (phase g >> 1)
+    // PV of tile g reads P buffer g % NP and completes on o_done[g % NP] (phase g / NP)
     auto issue_pv = [&](uint32_t g, bool first) {
-      const int st = g % PT_NS;
-      const uint32_t pa = smem_u32(&sm.p[g & 1][0]);
-      mbar_wait(&sm.p_full[g & 1], (g >> 1) & 1);
+      const int st = g % NS;
+      const uint32_t pa = smem_u32(&sm.p[g % NP][0]);
+      mbar_wait(&sm.p_full[g % NP], (g / NP) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (lane == 0) {
         const uint32_t va = smem_u32(&sm.v[st][0][0]);
@@ -214,7 +234,7 @@ __global__ void __launch_bounds__(192, 1)
           umma_bf16(tmem + O_COL, umma_desc_k(pa + kk * 32), umma_desc_mn(va + kk * 16 * 128, PT_KT * 128), idesc_o,
                     (first && kk == 0) ? 0u : 1u);
         umma_commit(&sm.kv_empty[st]);
-        umma_commit(&sm.o_done[g & 1]);
+        umma_commit(&sm.o_done[g % NP]);
       }
       __syncwarp();
     };
@@ -225,8 +245,8 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&sm.q_full, icnt & 1);
       for (int kt = 0; kt < nt; ++kt) {
         const uint32_t g = tile + kt;
-        const int st = g % PT_NS, b = g & 1;
-        mbar_wait(&sm.kv_full[st], (g / PT_NS) & 1);
+        const int st = g % NS, b = g & 1;
+        mbar_wait(&sm.kv_full[st], (g / NS) & 1);
         mbar_wait(&sm.s_free[b], ((g >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (lane == 0) {
@@ -315,11 +335,11 @@ __global__ void __launch_bounds__(192, 1)
                                fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         const float mn = fmaxf(m, mx);
         const bool grow = kt == 0 || (mn - m) * sl2 > PT_LAZY;
-        // P buffer g & 1 is free once PV(g - 2) has completed; O may be rescaled only after
-        // PV(g - 1).  (Neither barrier can be two phases ahead of a wait: PV(t + 2) needs
-        // P(t + 2), which is written only after PV(t) was waited for.)
-        auto wait_pv = [&](uint32_t t) { mbar_wait(&sm.o_done[t & 1], (t >> 1) & 1); };
-        if (g >= 2) wait_pv(g - 2);
+        // P buffer g % NP is free once PV(g - NP) has completed; O may be rescaled only after
+        // PV(g - 1).  (No barrier can be two phases ahead of a wait: PV(t + NP) needs
+        // P(t + NP), which is written only after PV(t) was waited for.)
+        auto wait_pv = [&](uint32_t t) { mbar_wait(&sm.o_done[t % NP], (t / NP) & 1); };
+        if (g >= NP) wait_pv(g - NP);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (kt > 0 && __any_sync(0xffffffffu, grow)) {
           wait_pv(g - 1);
@@ -339,7 +359,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         if (grow) m = mn;
         const float mo = m * sl2;
-        uint8_t* prow = reinterpret_cast<uint8_t*>(&sm.p[g & 1][0]) + j * 128;
+        uint8_t* prow = reinterpret_cast<uint8_t*>(&sm.p[g % NP][0]) + j * 128;
         // l is one chain in column order and p = exp2f(.): the same arithmetic as the masked
         // form (a masked key adds an exact 0), so the fast path leaves every result unchanged
         // (a 4-chain sum moved a full-size C2 logits row from 0.0196 to 0.0200)
@@ -366,11 +386,11 @@ __global__ void __launch_bounds__(192, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.p_full[g & 1]);
+        if (lane == 0) mbar_arrive(&sm.p_full[g % NP]);
       }
       // item done: O / l and the lse into the partial slot of (row, head)
       const uint32_t glast = tile + nt - 1;
-      mbar_wait(&sm.o_done[glast & 1], (glast >> 1) & 1);
+      mbar_wait(&sm.o_done[glast % NP], (glast / NP) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const float inv = 1.f / l;
       if constexpr (CAUSAL) {   // the prefill's attention output, bf16 [row][qh][hd]
@@ -441,23 +461,35 @@ bool make_kv_map(void* map_out, const bf16* pool, long long token_rows, int hd, 
 
 void launch_attn_prefix_tc(const bf16* q, const void* kv_map, float* part_o, float* part_lse, Dims D, int layer,
                            Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s) {
-  const size_t smem = sizeof(PtSmem<128>) + 1024;
-  ensure_dyn_smem(k_attn_prefix_tc<128, PT_PREFIX>, (int)smem);
-  launch_pdl(k_attn_prefix_tc<128, PT_PREFIX>, dim3(pl.tc_grid), dim3(192), smem, s,
+  const size_t smem = PtView<128, 4, 2>::BYTES + 1024;
+  ensure_dyn_smem(k_attn_prefix_tc<128, PT_PREFIX, 4, 2, 1>, (int)smem);
+  launch_pdl(k_attn_prefix_tc<128, PT_PREFIX, 4, 2, 1>, dim3(pl.tc_grid), dim3(192), smem, s,
              *reinterpret_cast<const CUtensorMap*>(kv_map), q, part_o, part_lse, (bf16*)nullptr, (const int4*)nullptr, 0,
              D, layer, rows, reqs, pl);
 }
 
+// causal modes: two CTAs per SM (2 KV stages, one P buffer each) unless SART_PF_CTA2=0
 template <int MODE>
 static void launch_causal(const bf16* q, const void* kv_map, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
                           const int4* blocks, int nblocks, cudaStream_t s) {
   if (nblocks <= 0) return;
-  const size_t smem = sizeof(PtSmem<128>) + 1024;
-  ensure_dyn_smem(k_attn_prefix_tc<128, MODE>, (int)smem);
+  static const bool two = !(getenv("SART_PF_CTA2") && atoi(getenv("SART_PF_CTA2")) == 0);
   const int items = nblocks * D.qh;
-  launch_pdl(k_attn_prefix_tc<128, MODE>, dim3(std::min(items, device_sms())), dim3(192), smem, s,
-             *reinterpret_cast<const CUtensorMap*>(kv_map), q, (float*)nullptr, (float*)nullptr, out, blocks, nblocks,
-             D, layer, rows, reqs, AttnPlan{});
+  const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(kv_map);
+  if (two) {
+    const size_t smem = PtView<128, 2, 1>::BYTES;
+    ensure_dyn_smem(k_attn_prefix_tc<128, MODE, 2, 1, 2>, (int)smem);
+    static bool carve = false;   // the largest shared-memory carveout: room for two CTAs per SM
+    if (!carve) carve = cudaFuncSetAttribute(k_attn_prefix_tc<128, MODE, 2, 1, 2>,
+                                             cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess;
+    launch_pdl(k_attn_prefix_tc<128, MODE, 2, 1, 2>, dim3(std::min(items, 2 * device_sms())), dim3(192), smem, s, map,
+               q, (float*)nullptr, (float*)nullptr, out, blocks, nblocks, D, layer, rows, reqs, AttnPlan{});
+  } else {
+    const size_t smem = PtView<128, 4, 2>::BYTES + 1024;
+    ensure_dyn_smem(k_attn_prefix_tc<128, MODE, 4, 2, 1>, (int)smem);
+    launch_pdl(k_attn_prefix_tc<128, MODE, 4, 2, 1>, dim3(std::min(items, device_sms())), dim3(192), smem, s, map,
+               q, (float*)nullptr, (float*)nullptr, out, blocks, nblocks, D, layer, rows, reqs, AttnPlan{});
+  }
 }
 void launch_attn_prefill_umma(const bf16* q, const void* kv_map, bf16* out, Dims D, int layer, Reqs reqs,
                               const int4* blocks, int nblocks, cudaStream_t s) {
