@@ -22,6 +22,7 @@
 
 #include "kernels.h"
 #include "umma.cuh"
+#include "sample_math.cuh"
 
 namespace {
 constexpr int BM = 128, BK = 64;
@@ -41,7 +42,7 @@ template <int BN, int MS> struct Tmem {
 #define SART_GEMM_NEPI_SWIGLU 8   // the SwiGLU epilogue (2 MUFU ops per output, one tile per CTA) runs alone
 #endif                            // after the mainloop: two warps per lane quarter halve it
 template <int MODE> struct Epi {
-  static constexpr int NEPI = MODE == GEMM_SWIGLU ? SART_GEMM_NEPI_SWIGLU : SART_GEMM_NEPI;
+  static constexpr int NEPI = MODE == GEMM_SWIGLU ? SART_GEMM_NEPI_SWIGLU : (MODE == GEMM_SAMPLE ? 8 : SART_GEMM_NEPI);
   static constexpr int NTHREADS = 64 + 32 * NEPI;
   static constexpr int CSTEP = 32 * (NEPI / 4);   // chunk stride of one epilogue warp
   static constexpr int SLAB = MODE == GEMM_SWIGLU ? 1 : NEPI;   // transpose slabs (store epilogues)
@@ -522,6 +523,44 @@ __global__ void __launch_bounds__(Epi<MODE>::NTHREADS, 1)
             }
           }
         }
+      } else if (MODE == GEMM_SAMPLE) {
+        // phase 1 of the sampler on this tile: the thread owns row gm and, with its twin warp,
+        // half of the tile's columns (32-column chunks half, half + 2, ...); its own best key
+        // so far is the pruning bound (sample_math.cuh: skipped entries cannot win)
+        if (Cs) store_tile_f32<BN, GEMM_STORE>(tbase, Cs, m0 + q * 32, n0, M, N, nullptr, smem_u32(sm.slab[warp - 2]),
+                                                lane, half * 32, CSTEP);
+        const Dims& D = epi.D;
+        bool live = false, mask_eos = false;
+        int s_ = 0, b_ = 0;
+        uint32_t rid = 0;
+        if (gm < M && epi.rows.status[gm] == RUNNING_ST) {
+          const int slot = epi.rows.slot[gm];
+          b_ = epi.rows.b[gm];
+          s_ = epi.rows.ell[gm] + 1;
+          const int fl = epi.reqs.sc_len[(long long)slot * SART_MAXN + b_];
+          live = !(fl > 0 && s_ == fl);   // a scripted EOS step needs no sample (phase 2 sets it)
+          mask_eos = fl > 0;
+          rid = (uint32_t)epi.reqs.id[slot];
+        }
+        const uint32_t k0 = (uint32_t)D.seed, k1 = (uint32_t)(D.seed >> 32);
+        float bk = -INFINITY;
+        int bv = 0x7fffffff;
+#pragma unroll 1
+        for (int c = half * 32; c < BN; c += CSTEP) {
+          float v[32];
+          tmem_ld32(tbase + c, v);
+          if (live)
+#pragma unroll
+            for (int g4 = 0; g4 < 8; ++g4)
+              if (n0 + c + 4 * g4 < N)
+                sample_group4(bk, bv, v + 4 * g4, n0 + c + 4 * g4, N, s_, rid, (uint32_t)b_, k0, k1, D.tau, mask_eos,
+                              D.eos, bk);
+        }
+        if (live) {
+          const long long si = (long long)gm * epi.nsl + (n0 / BN) * (NEPI / 4) + half;
+          epi.skey[si] = bk;
+          epi.sv[si] = bv;
+        }
       } else if (tp.tp > 1) {
         float* dsts[SART_MAX_TP];
         for (int p = 0; p < tp.tp; ++p) dsts[p] = tp.dst[p] + ((size_t)tp.rank * S + sp) * M * N;
@@ -898,6 +937,14 @@ bool launch_gemm_2sm(const bf16* A, const bf16* B, const float* bias, float* C, 
   if (mode == GEMM_STORE && NP == 512) return launch_2sm<512, GEMM_STORE>(A, B, bias, C, act, M, N, K, S, s);
   return false;
 }
+
+bool launch_gemm_sample(const bf16* A, const bf16* B, float* C, int M, int N, int K, const QkvEpi& epi,
+                        cudaStream_t s) {
+  if (M <= 0) return true;
+  if (K % 8) return false;
+  return launch_bn<256, GEMM_SAMPLE, 1>(A, B, nullptr, C, nullptr, M, N, K, 1, s, &epi);
+}
+int gemm_sample_slots(int V) { return (V + 255) / 256 * (Epi<GEMM_SAMPLE>::NEPI / 4); }
 
 bool launch_gemm_tc(const bf16* A, const bf16* B, const float* bias, float* C, bf16* act, int M, int N, int K,
                     int mode, cudaStream_t s, const bf16* Bt) {

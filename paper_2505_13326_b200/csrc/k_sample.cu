@@ -131,6 +131,11 @@ void launch_sample(const float* logits, Dims D, Rows rows, Reqs reqs, Ctr* ctr, 
   launch_pdl(k_sample_final, dim3(n), dim3(32), 0, s, D, rows, reqs, ctr, pkey, pv, nchunk, dbg_tok);
 }
 int sample_chunks(int V) { return (V + SCHUNK - 1) / SCHUNK; }
+void launch_sample_final(Dims D, Rows rows, Reqs reqs, Ctr* ctr, int n, int* dbg_tok, const float* pkey, const int* pv,
+                         int nchunk, cudaStream_t s) {
+  if (n <= 0) return;
+  launch_pdl(k_sample_final, dim3(n), dim3(32), 0, s, D, rows, reqs, ctr, pkey, pv, nchunk, dbg_tok);
+}
 
 
 // Start of a decode step.  es_every_step (reading R43): a running row whose request already

@@ -50,7 +50,8 @@ enum { GEMM_STORE = 0, GEMM_ACCUM = 1, GEMM_SWIGLU = 2, GEMM_QKV = 3,
        // QKV epilogue on half-head tiles (hd = 128, BN = 64): tile (head, p) holds head dims
        // [32p, 32p + 32) and [64 + 32p, 64 + 32p + 32) -- the rotate-half pairs stay in one tile,
        // so a head is split over 2 CTAs (2x the CTAs of the one-head tiling at small M)
-       GEMM_QKV_HALF = 4 };
+       GEMM_QKV_HALF = 4,
+       GEMM_SAMPLE = 5 };   // LM head with the sampler's per-(row, tile) Gumbel argmax in the epilogue
 // QKV epilogue: bias, rotate-half RoPE, q -> qout (bf16), k/v -> paged pool (decode: running
 // rows only; prefill: prefix positions p0 + row)
 struct QkvEpi {
@@ -66,7 +67,18 @@ struct QkvEpi {
   float* parts;   // split-K partials [S][M][N] (S > 1)
   int* cnt;       // per (head, m-tile, lane quarter) arrival counters, zero between launches
   int cnt_cap;    // entries in cnt (split-K is used only when heads x m-tiles x 4 fits)
+  float* skey;    // GEMM_SAMPLE: best key per (row, slot), nsl slots per row
+  int* sv;        //              and its vocab id
+  int nsl;
 };
+// LM head + sampler phase 1 (GEMM_SAMPLE): every running row's best Gumbel key over each
+// 128-column half of every 256-wide vocab tile -> skey / sv[row][2 * tile + half]; C (debug
+// capture only, else null) also receives the fp32 logits.  Then launch_sample_final(nsl).
+bool launch_gemm_sample(const bf16* A, const bf16* B, float* C, int M, int N, int K, const QkvEpi& epi,
+                        cudaStream_t s);
+int gemm_sample_slots(int V);
+void launch_sample_final(Dims D, Rows rows, Reqs reqs, Ctr* ctr, int n, int* dbg_tok, const float* pkey, const int* pv,
+                         int nchunk, cudaStream_t s);
 // Tensor parallelism (row f4): the split-K partials of an O / down projection are partial sums
 // over the tp ranks.  The GEMM epilogue stores partial tile (rank, split) into EVERY rank's
 // receive buffer (dst[p] + (rank * S + split) * M * N, remote stores over NVLink), then each CTA

@@ -76,6 +76,7 @@ struct sart_ctx {
   alignas(64) unsigned char kv_map[128] = {};   // CUtensorMap of the pool (tensor-core prefix pass)
   bool tc_prefix_window = false;
   bool kv_map_ok = false;   // kv_map describes this ctx's pool (bf16, hd 128)
+  bool fused_sample = false;   // GEMM_SAMPLE: LM head + sampler phase 1 (SART_FUSED_SAMPLE)
   bool pf_umma = false;     // causal prefill on tcgen05 (k_attn_prefix_tc<CAUSAL>); SART_PF_UMMA=0: mma.sync
   long long prefix_tc_windows = 0;
   bool gemm_failed = false;
@@ -516,6 +517,24 @@ void decode_step(sart_ctx* ctx, int n) {
     ctx->launches += 1;
   }
   norm<T>(ctx, res, ctx->W_<T>(t_final(D)), (T*)ctx->zT, ctx->z32, ctx->rows.status, n);
+  if constexpr (std::is_same<T, bf16>::value) {
+    if (ctx->fused_sample && !(ab & (AB_HEAD | AB_SAMPLE))) {   // LM head + sampler phase 1 in one kernel
+      QkvEpi e{};
+      e.D = D;
+      e.rows = ctx->rows;
+      e.reqs = ctx->reqs;
+      e.skey = ctx->skey;
+      e.sv = ctx->sv;
+      e.nsl = gemm_sample_slots(D.V);
+      if (!launch_gemm_sample((bf16*)ctx->zT, ctx->W_<bf16>(t_lm(D)), ctx->cfg.debug_capture ? ctx->logits : nullptr, n,
+                              D.V, D.d, e, s))
+        ctx->gemm_failed = true;
+      launch_sample_final(D, ctx->rows, ctx->reqs, ctx->ctr, n, ctx->dbg_tok, ctx->skey, ctx->sv, e.nsl, s);
+      ctx->launches += 2;
+      g_attn_skip_merge = false;
+      return;
+    }
+  }
   if (!(ab & AB_HEAD)) gemm<T>(ctx, (T*)ctx->zT, ctx->W_<T>(t_lm(D)), nullptr, ctx->logits, n, D.V, D.d, GEMM_STORE);
   if (!(ab & AB_SAMPLE))
     launch_sample(ctx->logits, D, ctx->rows, ctx->reqs, ctx->ctr, n, ctx->dbg_tok, ctx->skey, ctx->sv, s);
@@ -1577,8 +1596,13 @@ int sart_init(const sart_config* cfg_in, sart_ctx** out) {
   // ---- workspaces
   IC(dalloc(ctx, &ctx->logits, (size_t)D.R * D.V * 4));
   IC(dalloc(ctx, &ctx->dbg_tok, (size_t)D.R * 4));
-  IC(dalloc(ctx, &ctx->skey, (size_t)D.R * sample_chunks(D.V) * 4));
-  IC(dalloc(ctx, &ctx->sv, (size_t)D.R * sample_chunks(D.V) * 4));
+  // LM head with the sampler's first phase in its epilogue (SART_FUSED_SAMPLE=1; bf16)
+  ctx->fused_sample = ctx->bf16 && getenv("SART_FUSED_SAMPLE") && atoi(getenv("SART_FUSED_SAMPLE")) != 0;
+  {
+    const int nsl = std::max(sample_chunks(D.V), ctx->bf16 ? gemm_sample_slots(D.V) : 0);
+    IC(dalloc(ctx, &ctx->skey, (size_t)D.R * nsl * 4));
+    IC(dalloc(ctx, &ctx->sv, (size_t)D.R * nsl * 4));
+  }
   IC(dalloc(ctx, &ctx->dbg_slot, (size_t)D.R * 4));
   IC(dalloc(ctx, &ctx->dbg_b, (size_t)D.R * 4));
   ctx->pf_cap = (int)std::min<long long>((long long)D.S * cfg.max_prompt, 1LL << 24);

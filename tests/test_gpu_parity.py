@@ -304,21 +304,32 @@ def test_multi_chunk_suffix_production_ch():
     print("tiny CH=512 1600 steps worst", w)
 
 
-@pytest.mark.parametrize("tau", [1.0, 0.6])
-def test_sampler_full_vocab_1p5b(tau):
+@pytest.mark.parametrize("tau,fused", [(1.0, 0), (0.6, 0), (1.0, 1), (0.6, 1)])
+def test_sampler_full_vocab_1p5b(tau, fused):
     """PP3 at the full C2 vocabulary (V = 151,936: 10 sampler chunks of 16,384 entries, the
     pilot-bound pruning across loop iterations, the 10-way final reduction): the oracle
     sampler applied to the GPU's own fp32 logits must give the GPU's token at >= 500
     row-steps, except near-ties (top-2 perturbed-key gap < 1e-6 relative, PP3).  Half of the
-    requests carry a script (EOS masked except at the forced step)."""
+    requests carry a script (EOS masked except at the forced step).  fused = 1: the sampler's
+    first phase runs in the LM-head GEMM epilogue (SART_FUSED_SAMPLE; 1,188 (row, tile, half)
+    partial argmaxes per row, a ragged last vocab tile)."""
+    import os
     from synth import gen_script
     shape = SHAPES["1.5B"].with_layers(2)
     weights = gen_weights(shape, "bf16", std=0.02, root_seed=5)
     seed = 0x5EED_0000_1234
     steps = 24
-    g = gpu_engine(shape, "bf16", weights, block_size=64, num_blocks=2048, max_rows=64, max_requests=8,
-                   max_prompt=128, T=1, cap=steps + 4, eos_id=EOS, temperature=tau, sampler_seed=seed,
-                   debug_capture=True)
+    old = os.environ.get("SART_FUSED_SAMPLE")
+    os.environ["SART_FUSED_SAMPLE"] = str(fused)
+    try:
+        g = gpu_engine(shape, "bf16", weights, block_size=64, num_blocks=2048, max_rows=64, max_requests=8,
+                       max_prompt=128, T=1, cap=steps + 4, eos_id=EOS, temperature=tau, sampler_seed=seed,
+                       debug_capture=True)
+    finally:
+        if old is None:
+            os.environ.pop("SART_FUSED_SAMPLE", None)
+        else:
+            os.environ["SART_FUSED_SAMPLE"] = old
     forced_len = {}
     for rid in range(4):
         sc = None
@@ -352,7 +363,7 @@ def test_sampler_full_vocab_1p5b(tau):
                 assert (top[1] - top[0]) <= 1e-6 * abs(top[1]), (rid, b, s, y, int(tk[i]))
                 n_tie += 1
     g.close()
-    print(f"PP3 full vocab tau={tau}: {n_cmp} row-steps, {n_tie} near-ties, {n_eos} scripted EOS")
+    print(f"PP3 full vocab tau={tau} fused={fused}: {n_cmp} row-steps, {n_tie} near-ties, {n_eos} scripted EOS")
     assert n_cmp >= 500 and n_tie <= 2 and n_eos >= 4
 
 
