@@ -468,12 +468,14 @@ void launch_attn_prefix_tc(const bf16* q, const void* kv_map, float* part_o, flo
              D, layer, rows, reqs, pl);
 }
 
-// causal modes: two CTAs per SM (2 KV stages, one P buffer each) unless SART_PF_CTA2=0
+// causal modes: one CTA per SM (4 KV stages, two P buffers); SART_PF_CTA2=1: two CTAs per SM
+// (2 KV stages, one P buffer each) -- measured neutral (14B 8K prefill 252.3 vs 252.6 ms,
+// profiles/r2_prefill_umma_ab.txt), kept as an option
 template <int MODE>
 static void launch_causal(const bf16* q, const void* kv_map, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
                           const int4* blocks, int nblocks, cudaStream_t s) {
   if (nblocks <= 0) return;
-  static const bool two = !(getenv("SART_PF_CTA2") && atoi(getenv("SART_PF_CTA2")) == 0);
+  static const bool two = getenv("SART_PF_CTA2") && atoi(getenv("SART_PF_CTA2")) != 0;
   const int items = nblocks * D.qh;
   const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(kv_map);
   if (two) {
