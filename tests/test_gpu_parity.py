@@ -229,7 +229,7 @@ def test_7b_14b_geometry_bf16_teacher_forced(name):
     print(name, "worst", w)
 
 
-@pytest.mark.parametrize("attn_mode,tcq", [(0, 0), (1, None), (0, 64)])
+@pytest.mark.parametrize("attn_mode,tcq", [(0, 0), pytest.param(1, None, marks=pytest.mark.gpu_long), (0, 64)])
 def test_long_prefix_many_branches(attn_mode, tcq):
     """C5-like: one long shared prompt, 16 branches (80 query rows at g=5), prefix chunks of
     512 (the last one ragged) -- mma.sync prefix tasks (tcq 0: two groups of <= 12 rows,
@@ -243,11 +243,11 @@ def test_long_prefix_many_branches(attn_mode, tcq):
 
 
 @pytest.mark.parametrize("name,N,P,bs,ch,std", [
-    ("14B", 32, 1300, 64, None, 0.02),   # two groups of 16 rows (80 query rows each), 3 chunks, ragged last tile
-    ("14B", 13, 700, 16, None, 0.02),    # 65 query rows, 16-token pages (4 TMA boxes per 64-token tile)
+    pytest.param("14B", 32, 1300, 64, None, 0.02, marks=pytest.mark.gpu_long),   # two groups of 16 rows (80 query rows each), 3 chunks, ragged last tile
+    pytest.param("14B", 13, 700, 16, None, 0.02, marks=pytest.mark.gpu_long),    # 65 query rows, 16-token pages (4 TMA boxes per 64-token tile)
     ("small", 32, 600, 32, 128, 0.02),   # g = 4: a full 128-row item; CH 128 -> 5 chunks per request
     ("7B", 10, 66, 64, None, 0.02),      # g = 7, 70 rows; P - 1 = 65: one full tile + a 1-token tile
-    ("70B", 8, 300, 64, 64, 0.01),       # g = 8, 64 rows (the threshold); 5 single-tile chunks (std: R39)
+    pytest.param("70B", 8, 300, 64, 64, 0.01, marks=pytest.mark.gpu_long),       # g = 8, 64 rows (the threshold); 5 single-tile chunks (std: R39)
 ])
 def test_prefix_tc_pass(name, N, P, bs, ch, std):
     """The tensor-core prefix pass (k_attn_prefix_tc: tcgen05 S = Q K^T and O += P V over every
@@ -271,6 +271,7 @@ def test_multi_chunk_suffix_small_ch64():
     print("small CH=64 320 steps worst", w)
 
 
+@pytest.mark.gpu_long
 def test_multi_chunk_suffix_1p5b_geometry_ch64():
     """The C2 attention geometry (1.5B: GQA 12/2, hd 128, full vocab, 64-token blocks) with
     suffixes over 3+ chunks (CH = 64, 208 steps) and a prefix of several chunks."""
@@ -280,7 +281,7 @@ def test_multi_chunk_suffix_1p5b_geometry_ch64():
     print("1.5B-L2 CH=64 208 steps worst", w)
 
 
-@pytest.mark.parametrize("name,piece", [("small", 16), ("1.5B", 32)])
+@pytest.mark.parametrize("name,piece", [("small", 16), pytest.param("1.5B", 32, marks=pytest.mark.gpu_long)])
 def test_multi_chunk_suffix_pieces(name, piece):
     """SART_ATTN_PIECE: whole CH = 64 chunks stay items, the partial last chunk of every row is
     cut into pieces of 16 / 32 tokens (slots npc_max + nfull + p, up to 4 / 2 pieces) -- the
@@ -304,7 +305,7 @@ def test_multi_chunk_suffix_production_ch():
     print("tiny CH=512 1600 steps worst", w)
 
 
-@pytest.mark.parametrize("tau,fused", [(1.0, 0), (0.6, 0), (1.0, 1), (0.6, 1)])
+@pytest.mark.parametrize("tau,fused", [(1.0, 0), (0.6, 0), (1.0, 1), pytest.param(0.6, 1, marks=pytest.mark.gpu_long)])
 def test_sampler_full_vocab_1p5b(tau, fused):
     """PP3 at the full C2 vocabulary (V = 151,936: 10 sampler chunks of 16,384 entries, the
     pilot-bound pruning across loop iterations, the 10-way final reduction): the oracle

@@ -123,7 +123,7 @@ def test_tp2_small_teacher_forced():
     print("TP=2 small worst", w)
 
 
-@pytest.mark.parametrize("name", ["7B", "70B"])
+@pytest.mark.parametrize("name", ["7B", pytest.param("70B", marks=pytest.mark.gpu_long)])
 def test_tp2_geometry_teacher_forced(name):
     """7B (28/4 heads -> 14/2 per rank, F 18944 -> 9472) and the paper's 70B (64/8 ->
     32/4, d 8192, F 28672 -> 14336): one layer, small vocab."""
