@@ -59,6 +59,19 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                "l"(src), "r"(bytes), "r"(s_u32(bar))
                : "memory");
 }
+// suffix KV is read exactly once per step: stream it with an L2 evict-first policy so it does
+// not push the step's partials, q and the shared prefix (re-read by the prefix m-tiles) out of L2
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(s_u32(bar)), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -155,6 +168,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   WarpSmem<HD, NS, SW>& sm = reinterpret_cast<WarpSmem<HD, NS, SW>*>(sraw)[warp];
   int* work = pl.work + layer;
   const float sl2 = 1.4426950408889634f * rsqrtf((float)HD);   // log2(e) / sqrt(hd)
+  const uint64_t pol = l2_evict_first();
 
   // zero the ring once (masked tokens multiply V by 0, so stale smem must be finite)
   for (int e = lane; e < NS * SW * HD / 8; e += 32) {
@@ -217,8 +231,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
           const int inblk = tok % D.bs;
           const bf16* kt = pool + kv_tile_off(D, layer, blk, 0, it.h) + (long long)inblk * HD;
           const bf16* vt = pool + kv_tile_off(D, layer, blk, 1, it.h) + (long long)inblk * HD;
-          bulk_g2s(s_u32(sm.k[slot] + p * tpb * HD), kt, tpb * HD * 2, &sm.full[slot]);
-          bulk_g2s(s_u32(sm.v[slot] + p * tpb * HD), vt, tpb * HD * 2, &sm.full[slot]);
+          if (it.type == 0 && pl.evict) {
+            bulk_g2s_hint(s_u32(sm.k[slot] + p * tpb * HD), kt, tpb * HD * 2, &sm.full[slot], pol);
+            bulk_g2s_hint(s_u32(sm.v[slot] + p * tpb * HD), vt, tpb * HD * 2, &sm.full[slot], pol);
+          } else {
+            bulk_g2s(s_u32(sm.k[slot] + p * tpb * HD), kt, tpb * HD * 2, &sm.full[slot]);
+            bulk_g2s(s_u32(sm.v[slot] + p * tpb * HD), vt, tpb * HD * 2, &sm.full[slot]);
+          }
         }
       }
       iss_s0 += SW;

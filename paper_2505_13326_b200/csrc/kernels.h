@@ -156,6 +156,7 @@ struct AttnPlan {
                     // CTA, waits for tc_done == tc_grid, so the merge sees both kernels' partials)
   int qr_grp;       // branch rows per group of the mma.sync prefix tasks (16-row m-tiles)
   int qr_max, CH, npc_max, nslot;   // qr_max: row stride of grp_rows (>= every group size)
+  int evict;        // 1: suffix KV streamed with an L2 evict-first policy (SART_ATTN_EVICT)
   int PC;           // suffix piece length (0: off): a row's whole CH-chunks stay items, its last
                     // partial chunk is cut into PC-token pieces so the queue ends with short items
 };
