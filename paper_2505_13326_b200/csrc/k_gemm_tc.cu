@@ -15,6 +15,7 @@
 #include <cuda.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include <map>
 #include <mutex>
@@ -259,6 +260,7 @@ __global__ void __launch_bounds__(Epi<MODE>::NTHREADS, 1)
       if (!Bt) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
       // weights: pre-tiled (Bt: [n-tile][k-block] images of the swizzled shared tile, one
       // contiguous bulk copy each) or row-major through the 2-D tensor map
+      const uint64_t polb = l2_policy_evict_first();
       auto load_b = [&](int st, int kbi, int n0_) {
         if constexpr (MODE == GEMM_QKV_HALF) {
           // half-head tile: weight rows [32p, 32p + 32) and [64 + 32p, ...) of head n0_ / 128
@@ -269,6 +271,8 @@ __global__ void __launch_bounds__(Epi<MODE>::NTHREADS, 1)
           tma_load_2d(sm.b[st] + 32 * BK, &tmB, &sm.full[st], kbi * BK, hb + 64);
         } else if (Bt) {
           bulk_load(sm.b[st], Bt + ((size_t)(n0_ / BN) * kb_all + kbi) * (BN * BK), BN * BK * 2, &sm.full[st]);
+        } else if (epi.evict_b) {
+          tma_load_2d_hint(sm.b[st], &tmB, &sm.full[st], kbi * BK, n0_, polb);
         } else {
           tma_load_2d(sm.b[st], &tmB, &sm.full[st], kbi * BK, n0_);
         }
@@ -888,6 +892,8 @@ bool launch_bn(const bf16* A, const bf16* B, const float* bias, float* C, bf16* 
   const int grid = ntiles < g_num_sms ? ntiles : g_num_sms;
   QkvEpi e{};
   if (epi) e = *epi;
+  static const int evict_b = getenv("SART_GEMM_EVICT") ? atoi(getenv("SART_GEMM_EVICT")) : 0;
+  e.evict_b = evict_b;
   TpOut t{};
   if (tpo) t = *tpo;
   launch_pdl(k_gemm_tc<BN, MODE, MS>, dim3(grid), dim3(Epi<MODE>::NTHREADS), smem, s, *ma, *mb, Bt, C, bias, act, M, N, K, S, e,

@@ -67,6 +67,7 @@ struct QkvEpi {
   float* parts;   // split-K partials [S][M][N] (S > 1)
   int* cnt;       // per (head, m-tile, lane quarter) arrival counters, zero between launches
   int cnt_cap;    // entries in cnt (split-K is used only when heads x m-tiles x 4 fits)
+  int evict_b;    // weights (B) loaded with an L2 evict-first policy (SART_GEMM_EVICT)
   float* skey;    // GEMM_SAMPLE: best key per (row, slot), nsl slots per row
   int* sv;        //              and its vocab id
   int nsl;
