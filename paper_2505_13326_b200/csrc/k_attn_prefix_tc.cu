@@ -56,6 +56,7 @@ struct PtView {
   static constexpr size_t QB = (size_t)NH * PT_M * 64 * 2, KB = (size_t)NS * NH * PT_KT * 64 * 2,
                           PB = (size_t)NP * PT_M * PT_KT * 2, NBAR = 2 * NS + 4 + 2 * NP + 1;
   static constexpr size_t BYTES = QB + 2 * KB + PB + 8 * NBAR + 16;
+  static constexpr size_t XBYTES = 4 * 4 * PT_M;     // pair-exchange arrays (NSM = 8 only)
   bf16 (*q)[PT_M * 64];                                // Q, K-major SW128: [half][row][64]
   bf16 (*k)[NH][PT_KT * 64];                           // K tile: [half][token][64] (K-major B of S)
   bf16 (*v)[NH][PT_KT * 64];                           // V tile: same bytes, MN-major B of O
@@ -63,6 +64,7 @@ struct PtView {
   uint64_t *kv_full, *kv_empty, *s_full, *s_free, *p_full, *o_done;   // [NS] [NS] [2] [2] [NP] [NP]
   uint64_t& q_full;
   uint32_t& tmem_base;
+  float* xch;     // [4][PT_M] two softmax warps per row (NSM = 8): max of each half, l after half 0, l
   __device__ explicit PtView(uint8_t* b)
       : q(reinterpret_cast<bf16 (*)[PT_M * 64]>(b)),
         k(reinterpret_cast<bf16 (*)[NH][PT_KT * 64]>(b + QB)),
@@ -70,7 +72,8 @@ struct PtView {
         p(reinterpret_cast<bf16 (*)[PT_M * PT_KT]>(b + QB + 2 * KB)),
         kv_full(reinterpret_cast<uint64_t*>(b + QB + 2 * KB + PB)),
         kv_empty(kv_full + NS), s_full(kv_empty + NS), s_free(s_full + 2), p_full(s_free + 2), o_done(p_full + NP),
-        q_full(o_done[NP]), tmem_base(*reinterpret_cast<uint32_t*>(o_done + NP + 1)) {}
+        q_full(o_done[NP]), tmem_base(*reinterpret_cast<uint32_t*>(o_done + NP + 1)),
+        xch(reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(o_done + NP + 1) + 16)) {}
 };
 
 __device__ __forceinline__ uint32_t pack_bf16_pt(float lo, float hi) {
@@ -131,8 +134,8 @@ __device__ __forceinline__ PtItem pt_item(const AttnPlan& pl, const Dims& D, con
   return it;
 }
 
-template <int HD, int MODE, int NS, int NP, int MINB>
-__global__ void __launch_bounds__(192, MINB)
+template <int HD, int MODE, int NS, int NP, int MINB, int NSM = 4>
+__global__ void __launch_bounds__(64 + 32 * NSM, MINB)
     k_attn_prefix_tc(const __grid_constant__ CUtensorMap kvmap, const bf16* __restrict__ q, float* __restrict__ part_o,
                      float* __restrict__ part_lse, bf16* __restrict__ out, const int4* __restrict__ blocks, int nblocks,
                      Dims D, int layer, Rows rows, Reqs reqs, AttnPlan pl) {
@@ -155,13 +158,13 @@ __global__ void __launch_bounds__(192, MINB)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.s_full[i], 1);
-      mbar_init(&sm.s_free[i], 4);
+      mbar_init(&sm.s_free[i], NSM);
     }
     for (int i = 0; i < NP; ++i) {
-      mbar_init(&sm.p_full[i], 4);
+      mbar_init(&sm.p_full[i], NSM);
       mbar_init(&sm.o_done[i], 1);
     }
-    mbar_init(&sm.q_full, 4);
+    mbar_init(&sm.q_full, NSM);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -267,9 +270,20 @@ __global__ void __launch_bounds__(192, MINB)
     }
   } else {
     // ---------------------------------------------------------------- softmax (one row / thread)
+    // NSM = 8: two warps per TMEM lane quarter share each row, half of the 64 key columns each;
+    // they exchange the half maxima and hand the row sum over in column order (half 0's chain
+    // continues in half 1), so every value is the same as with one warp per row
+    constexpr int HH = NSM / 4, KC = PT_KT / HH;
     const int quarter = warp & 3;
+    const int hf = HH == 1 ? 0 : (warp - 2) >> 2;      // which key-column half this warp owns
     const int j = quarter * 32 + lane;                 // query row of the item = TMEM lane
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    float* xmax = sm.xch;                              // [2][PT_M]
+    float* xl0 = sm.xch + 2 * PT_M;                    // l after half 0's columns
+    float* xlf = sm.xch + 3 * PT_M;                    // l after the whole tile
+    auto pair_sync = [&]() {
+      if constexpr (HH == 2) asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+    };
     uint32_t tile = 0, icnt = 0;
     for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++icnt) {
       const PtItem it = pt_item<MODE>(pl, D, rows, reqs, blocks, i);
@@ -286,12 +300,14 @@ __global__ void __launch_bounds__(192, MINB)
       {
         const uint4* src = row >= 0 ? reinterpret_cast<const uint4*>(q + ((long long)row * D.qh + head) * HD) : nullptr;
 #pragma unroll
-        for (int hh = 0; hh < NH; ++hh)
+        for (int hh = 0; hh < NH; ++hh) {
+          if (HH == 2 && (hh & 1) != hf) continue;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const uint4 v = src ? __ldg(src + hh * 8 + c) : make_uint4(0, 0, 0, 0);
             *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(&sm.q[hh][0]) + j * 128 + ((c ^ (j & 7)) << 4)) = v;
           }
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -303,36 +319,44 @@ __global__ void __launch_bounds__(192, MINB)
         const int b = g & 1;
         mbar_wait(&sm.s_full[b], (g >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        uint32_t sr[PT_KT];
-        tmem_ld32_nw(tmem + lane_off + b * PT_KT, sr);
-        tmem_ld32_nw(tmem + lane_off + b * PT_KT + 32, sr + 32);
+        uint32_t sr[KC];
+#pragma unroll
+        for (int c = 0; c < KC; c += 32) tmem_ld32_nw(tmem + lane_off + b * PT_KT + hf * KC + c, sr + c);
         tmem_wait_ld();
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.s_free[b]);
         // keys of this tile the row may see: >= 1 in its first tile (key 0 precedes every
-        // position); causal: key index <= the row's position p0 + j
+        // position); causal: key index <= the row's position p0 + j.  Column c of this
+        // warp's half is key column hf * KC + c of the tile.
         int nvalid = it.t1 - (it.t0 + kt * PT_KT);
         if constexpr (CAUSAL) nvalid = min(nvalid, it.p0 + j - kt * PT_KT + 1);
+        nvalid -= hf * KC;
         // PT_SUF: the prefix pages' padding slots [npre, pbase) of this tile are masked
-        const int h0 = it.npre - (it.t0 + kt * PT_KT), h1 = it.pbase - (it.t0 + kt * PT_KT);
-        // warp-uniform fast path: every key of the tile is visible to every row of the warp
+        const int h0 = it.npre - (it.t0 + kt * PT_KT) - hf * KC, h1 = it.pbase - (it.t0 + kt * PT_KT) - hf * KC;
+        // warp-uniform fast path: every key of the half is visible to every row of the warp
         // (all but the diagonal / ragged / padding tiles) -- no per-element predicates
-        const bool wfull = __all_sync(0xffffffffu, nvalid >= PT_KT && (MODE != PT_SUF || h1 <= 0 || h0 >= PT_KT));
+        const bool wfull = __all_sync(0xffffffffu, nvalid >= KC && (MODE != PT_SUF || h1 <= 0 || h0 >= KC));
         auto vis = [&](int c) { return wfull || (c < nvalid && (MODE != PT_SUF || c < h0 || c >= h1)); };
         float mx8[8];   // 8 independent max chains (max is order-free)
 #pragma unroll
         for (int e = 0; e < 8; ++e) mx8[e] = -INFINITY;
         if (wfull) {
 #pragma unroll
-          for (int c = 0; c < PT_KT; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
+          for (int c = 0; c < KC; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
         } else {
 #pragma unroll
-          for (int c = 0; c < PT_KT; ++c)
+          for (int c = 0; c < KC; ++c)
             if (vis(c)) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
         }
-        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        if constexpr (HH == 2) {
+          xmax[hf * PT_M + j] = mx;
+          pair_sync();                                   // B1: both halves' maxima are written
+          mx = fmaxf(mx, xmax[(1 - hf) * PT_M + j]);
+          if (hf == 0 && kt > 0) l = xlf[j];             // the row sum through the previous tile
+        }
         const float mn = fmaxf(m, mx);
         const bool grow = kt == 0 || (mn - m) * sl2 > PT_LAZY;
         // P buffer g % NP is free once PV(g - NP) has completed; O may be rescaled only after
@@ -346,7 +370,7 @@ __global__ void __launch_bounds__(192, MINB)
           asm volatile("tcgen05.fence::after_thread_sync;");
           const float c = grow ? exp2f((m - mn) * sl2) : 1.f;
 #pragma unroll 1
-          for (int cb = 0; cb < HD; cb += 32) {
+          for (int cb = hf * (HD / HH); cb < (hf + 1) * (HD / HH); cb += 32) {   // this warp's O columns
             uint32_t o[32];
             tmem_ld32_nw(tmem + lane_off + O_COL + cb, o);
             tmem_wait_ld();
@@ -365,28 +389,46 @@ __global__ void __launch_bounds__(192, MINB)
         // (a 4-chain sum moved a full-size C2 logits row from 0.0196 to 0.0200)
         if (!wfull)   // masked keys -> -inf: their p is exactly 0
 #pragma unroll
-          for (int c = 0; c < PT_KT; ++c)
+          for (int c = 0; c < KC; ++c)
             if (!vis(c)) sr[c] = __float_as_uint(-INFINITY);
+        float pk[KC];
 #pragma unroll
-        for (int c8 = 0; c8 < PT_KT / 8; ++c8) {
-          float p[8];
+        for (int c8 = 0; c8 < KC / 8; ++c8) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int c = c8 * 8 + e;
-            p[e] = exp2f(fmaf(__uint_as_float(sr[c]), sl2, -mo));
-            l += p[e];
-          }
+          for (int e = 0; e < 8; ++e) pk[c8 * 8 + e] = exp2f(fmaf(__uint_as_float(sr[c8 * 8 + e]), sl2, -mo));
           uint4 w;
-          w.x = pack_bf16_pt(p[0], p[1]);
-          w.y = pack_bf16_pt(p[2], p[3]);
-          w.z = pack_bf16_pt(p[4], p[5]);
-          w.w = pack_bf16_pt(p[6], p[7]);
-          *reinterpret_cast<uint4*>(prow + ((c8 ^ (j & 7)) << 4)) = w;
+          w.x = pack_bf16_pt(pk[c8 * 8 + 0], pk[c8 * 8 + 1]);
+          w.y = pack_bf16_pt(pk[c8 * 8 + 2], pk[c8 * 8 + 3]);
+          w.z = pack_bf16_pt(pk[c8 * 8 + 4], pk[c8 * 8 + 5]);
+          w.w = pack_bf16_pt(pk[c8 * 8 + 6], pk[c8 * 8 + 7]);
+          const int cg = hf * (KC / 8) + c8;             // 16-byte chunk of the 64-key P row
+          *reinterpret_cast<uint4*>(prow + ((cg ^ (j & 7)) << 4)) = w;
+        }
+        if constexpr (HH == 2) {                         // B2: half 0's running sum -> half 1
+          if (hf == 0) {
+#pragma unroll
+            for (int c = 0; c < KC; ++c) l += pk[c];
+            xl0[j] = l;
+            pair_sync();
+          } else {
+            pair_sync();
+            l = xl0[j];
+#pragma unroll
+            for (int c = 0; c < KC; ++c) l += pk[c];
+            xlf[j] = l;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < KC; ++c) l += pk[c];
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.p_full[g % NP]);
+      }
+      if constexpr (HH == 2) {                           // the whole row sum to both halves
+        pair_sync();
+        if (hf == 0) l = xlf[j];
       }
       // item done: O / l and the lse into the partial slot of (row, head)
       const uint32_t glast = tile + nt - 1;
@@ -396,7 +438,7 @@ __global__ void __launch_bounds__(192, MINB)
       if constexpr (CAUSAL) {   // the prefill's attention output, bf16 [row][qh][hd]
         bf16* dst = row >= 0 ? out + ((long long)row * D.qh + head) * HD : nullptr;
 #pragma unroll 1
-        for (int cb = 0; cb < HD; cb += 32) {
+        for (int cb = hf * (HD / HH); cb < (hf + 1) * (HD / HH); cb += 32) {
           uint32_t o[32];
           tmem_ld32_nw(tmem + lane_off + O_COL + cb, o);
           tmem_wait_ld();
@@ -414,7 +456,7 @@ __global__ void __launch_bounds__(192, MINB)
       } else {
         float* dst = row >= 0 ? part_o + (((long long)row * D.qh + head) * pl.nslot + it.slot_idx) * HD : nullptr;
 #pragma unroll 1
-        for (int cb = 0; cb < HD; cb += 32) {
+        for (int cb = hf * (HD / HH); cb < (hf + 1) * (HD / HH); cb += 32) {
           uint32_t o[32];
           tmem_ld32_nw(tmem + lane_off + O_COL + cb, o);
           tmem_wait_ld();
@@ -425,7 +467,7 @@ __global__ void __launch_bounds__(192, MINB)
                   make_float4(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv,
                               __uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
         }
-        if (dst) part_lse[((long long)row * D.qh + head) * pl.nslot + it.slot_idx] = m * sl2 + log2f(l);
+        if (dst && hf == HH - 1) part_lse[((long long)row * D.qh + head) * pl.nslot + it.slot_idx] = m * sl2 + log2f(l);
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       tile += nt;
@@ -459,18 +501,29 @@ bool make_kv_map(void* map_out, const bf16* pool, long long token_rows, int hd, 
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+static bool tc_pair() {   // SART_TC_PAIR=1: two softmax warps per row (8 softmax warps per CTA)
+  static const bool on = getenv("SART_TC_PAIR") && atoi(getenv("SART_TC_PAIR")) != 0;
+  return on;
+}
 void launch_attn_prefix_tc(const bf16* q, const void* kv_map, float* part_o, float* part_lse, Dims D, int layer,
                            Rows rows, Reqs reqs, AttnPlan pl, cudaStream_t s) {
+  const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(kv_map);
+  if (tc_pair()) {
+    const size_t smem = PtView<128, 4, 2>::BYTES + PtView<128, 4, 2>::XBYTES + 1024;
+    ensure_dyn_smem(k_attn_prefix_tc<128, PT_PREFIX, 4, 2, 1, 8>, (int)smem);
+    launch_pdl(k_attn_prefix_tc<128, PT_PREFIX, 4, 2, 1, 8>, dim3(pl.tc_grid), dim3(64 + 32 * 8), smem, s, map, q, part_o,
+               part_lse, (bf16*)nullptr, (const int4*)nullptr, 0, D, layer, rows, reqs, pl);
+    return;
+  }
   const size_t smem = PtView<128, 4, 2>::BYTES + 1024;
   ensure_dyn_smem(k_attn_prefix_tc<128, PT_PREFIX, 4, 2, 1>, (int)smem);
-  launch_pdl(k_attn_prefix_tc<128, PT_PREFIX, 4, 2, 1>, dim3(pl.tc_grid), dim3(192), smem, s,
-             *reinterpret_cast<const CUtensorMap*>(kv_map), q, part_o, part_lse, (bf16*)nullptr, (const int4*)nullptr, 0,
-             D, layer, rows, reqs, pl);
+  launch_pdl(k_attn_prefix_tc<128, PT_PREFIX, 4, 2, 1>, dim3(pl.tc_grid), dim3(192), smem, s, map, q, part_o, part_lse,
+             (bf16*)nullptr, (const int4*)nullptr, 0, D, layer, rows, reqs, pl);
 }
 
 // causal modes: one CTA per SM (4 KV stages, two P buffers); SART_PF_CTA2=1: two CTAs per SM
 // (2 KV stages, one P buffer each) -- measured neutral (14B 8K prefill 252.3 vs 252.6 ms,
-// profiles/r2_prefill_umma_ab.txt), kept as an option
+// profiles/r2_prefill_umma_ab.txt), kept as an option; SART_TC_PAIR=1: 8 softmax warps
 template <int MODE>
 static void launch_causal(const bf16* q, const void* kv_map, bf16* out, Dims D, int layer, Rows rows, Reqs reqs,
                           const int4* blocks, int nblocks, cudaStream_t s) {
@@ -478,7 +531,12 @@ static void launch_causal(const bf16* q, const void* kv_map, bf16* out, Dims D, 
   static const bool two = getenv("SART_PF_CTA2") && atoi(getenv("SART_PF_CTA2")) != 0;
   const int items = nblocks * D.qh;
   const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(kv_map);
-  if (two) {
+  if (tc_pair()) {
+    const size_t smem = PtView<128, 4, 2>::BYTES + PtView<128, 4, 2>::XBYTES + 1024;
+    ensure_dyn_smem(k_attn_prefix_tc<128, MODE, 4, 2, 1, 8>, (int)smem);
+    launch_pdl(k_attn_prefix_tc<128, MODE, 4, 2, 1, 8>, dim3(std::min(items, device_sms())), dim3(64 + 32 * 8), smem, s,
+               map, q, (float*)nullptr, (float*)nullptr, out, blocks, nblocks, D, layer, rows, reqs, AttnPlan{});
+  } else if (two) {
     const size_t smem = PtView<128, 2, 1>::BYTES;
     ensure_dyn_smem(k_attn_prefix_tc<128, MODE, 2, 1, 2>, (int)smem);
     static bool carve = false;   // the largest shared-memory carveout: room for two CTAs per SM
